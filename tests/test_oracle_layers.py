@@ -1,0 +1,110 @@
+"""Pins for oracle/layers.py and oracle/datagen.py: published splitmix64
+test vectors, bf16 rounding cases worked by hand, finite differences of the
+loss (independent of the backward formulas), closed forms for special
+cases (identity weights, one linear layer, lr = 0)."""
+import numpy as np
+import pytest
+
+from oracle import datagen as DG
+from oracle import layers as LY
+from workloads import TRAIN, INFER, make_job
+
+
+def test_splitmix64_published_vectors():
+    # SplittableRandom / splitmix64 reference outputs for state 0, 1*gamma, 2*gamma
+    # (Vigna, "splitmix64.c"; the sequence x += 0x9E3779B97F4A7C15 from x = 0).
+    out = DG.splitmix64(np.array([0, 0x9E3779B97F4A7C15, (2 * 0x9E3779B97F4A7C15) % 2**64],
+                                 dtype=np.uint64))
+    assert [int(v) for v in out] == [0xE220A8397B1DCDAF, 0x6E789E6AA1B965F4, 0x06C45D188009454F]
+
+
+def test_bf16_rne_cases():
+    v = np.array([1.0, 1 + 2**-8, 1 + 3 * 2**-8, -1 - 2**-8, 1 + 2**-7, 3.0e38, 2**-130],
+                 dtype=np.float32)
+    exp = [1.0, 1.0, 1 + 2**-6, -1.0, 1 + 2**-7, None, None]
+    got = DG.bf16_rne(v)
+    for g, e in zip(got[:5], exp[:5]):
+        assert g == np.float32(e)
+    # every output is bf16-representable: low 16 bits clear
+    assert np.all((got.view(np.uint32) & 0xFFFF) == 0)
+
+
+def test_gen_distribution_and_determinism():
+    s = DG.scale_for(256)
+    a = DG.gen(7, 3, DG.KIND_W, 1, 0, 256, 256, s)
+    b = DG.gen(7, 3, DG.KIND_W, 1, 0, 256, 256, s)
+    c = DG.gen(7, 4, DG.KIND_W, 1, 0, 256, 256, s)
+    assert np.array_equal(a, b) and not np.array_equal(a, c)
+    assert np.all(np.abs(a) <= float(s)) and a.dtype == np.float64
+    assert abs(a.mean()) < 0.01 * float(s)
+    assert abs(a.var() / float(s) ** 2 - 1.0 / 3.0) < 0.01      # U(-1,1) variance
+    assert np.all(DG.bf16_rne(a.astype(np.float32)) == a.astype(np.float32))
+    # element idx = row * cols + col of the logical tensor
+    flat = DG.gen(7, 3, DG.KIND_W, 1, 0, 1, 256 * 256, s).reshape(256, 256)
+    assert np.array_equal(flat, a)
+
+
+def _tiny_job(dims, B, kind=TRAIN, lr=0.05):
+    return make_job(0, kind, 0, dims, B, 3, lr=lr, seed=9, request_ticks=(0, 1, 2) if kind else ())
+
+
+@pytest.mark.parametrize("dims", [(5, 4, 3), (6, 7, 5, 4), (3, 2)])
+def test_gradients_match_finite_differences(dims):
+    job = _tiny_job(dims, 4)
+    W = LY.init_weights(job)
+    X, T = LY.inputs(job, 0)
+    X = X * 3.0
+    _, dW = LY.gradients(W, X, T)
+    eps = 1e-6
+    for l, Wl in enumerate(W):
+        num = np.zeros_like(Wl)
+        for idx in np.ndindex(Wl.shape):
+            Wp = [w.copy() for w in W]
+            Wm = [w.copy() for w in W]
+            Wp[l][idx] += eps
+            Wm[l][idx] -= eps
+            num[idx] = (LY.loss(Wp, X, T) - LY.loss(Wm, X, T)) / (2 * eps)
+        assert np.max(np.abs(num - dW[l])) <= 1e-6 * max(1.0, np.max(np.abs(num))), l
+
+
+def test_one_linear_layer_closed_form():
+    """L = 1: textbook least squares gradient X^T (X W - T) / B."""
+    job = _tiny_job((8, 5), 6)
+    W = LY.init_weights(job)
+    X, T = LY.inputs(job, 0)
+    _, dW = LY.gradients(W, X, T)
+    assert np.allclose(dW[0], X.T @ (X @ W[0] - T) / 6, rtol=0, atol=1e-14)
+
+
+def test_identity_weights_give_relu():
+    """W_1 = W_2 = I  =>  A_2 = ReLU(X) (A_L has no ReLU; A_1 does)."""
+    X = np.array([[1.0, -2.0, 0.5], [-0.25, 3.0, -1.0]])
+    A = LY.forward([np.eye(3), np.eye(3)], X)
+    assert np.array_equal(A[-1], np.maximum(X, 0))
+
+
+def test_lr_zero_keeps_weights():
+    job = _tiny_job((16, 8, 4), 5, lr=0.0)
+    outs, W = LY.run_job(job)
+    W0 = LY.init_weights(job)
+    assert all(np.array_equal(a, b) for a, b in zip(W, W0))
+
+
+def test_sgd_step_is_minus_lr_grad_and_reduces_loss_on_fixed_batch():
+    job = _tiny_job((16, 12, 4), 8, lr=0.1)
+    W = LY.init_weights(job)
+    X, T = LY.inputs(job, 0)
+    before = LY.loss(W, X, T)
+    W0 = [w.copy() for w in W]
+    _, dW = LY.gradients(W, X, T)
+    LY.train_step(W, job, 0)
+    for a, b, g in zip(W, W0, dW):
+        assert np.allclose(a, b - np.float32(0.1) * g, rtol=0, atol=1e-15)
+    assert LY.loss(W, X, T) < before
+
+
+def test_inference_is_forward_of_init_weights():
+    job = _tiny_job((16, 8, 4), 2, kind=INFER)
+    outs, W = LY.run_job(job)
+    X1, _ = LY.inputs(job, 1)
+    assert np.array_equal(outs[1], LY.forward(LY.init_weights(job), X1)[-1])
