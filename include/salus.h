@@ -1,0 +1,251 @@
+/*
+ * salus.h — C ABI of the B200-native Salus execution service (libsalus.so).
+ *
+ * What it implements (PAPER.md = LaTeX source of arXiv 1902.04610):
+ *   - a singleton execution service that consolidates all GPU access
+ *     (§3.1) — here one persistent sm_100a kernel per GPU;
+ *   - sessions created per job — salus_submit_job();
+ *   - lane requests queued by the memory manager, Algorithm 1 "GPU Lane
+ *     Assignment" (§3.3.2) under the safety condition
+ *     sum P_i + sum L_j <= C, L_j = max_{i in j} E_i;
+ *   - iteration-granularity scheduling per lane (§3.2.2
+ *     P:353-354) with FIFO / SRTF / PACK / FAIR (§4);
+ *   - persistent memory kept resident so a switch is only the next
+ *     iteration record (Observations 1-2).
+ *
+ * Ambiguities of the paper are resolved by the readings A1..A30 of
+ * SURVEY.md §8(c), restated in DESIGN.md; the ones visible at this
+ * boundary are cited below.
+ *
+ * Conventions
+ *   - Every call returns int: SALUS_OK (0) or a negative SALUS_E_* code.
+ *     No call aborts the process.  salus_last_error() gives a message.
+ *   - Pointers documented "device" are CUDA device pointers owned by the
+ *     caller (in this repo: torch tensors); "host" pointers are ordinary
+ *     host memory.  The library never cudaMalloc()s device memory and never
+ *     frees caller buffers.  It owns only the host-side context and a few
+ *     bytes of pinned host memory for the abort flag.
+ *   - A context has a single owner; calls on one context must not overlap.
+ *     Separate contexts on separate devices may run concurrently.
+ *   - Sizes are bytes unless the name says pages.  Logical time is int64
+ *     ticks (1 tick = 1 ns nominal, A17).
+ */
+#ifndef SALUS_H_
+#define SALUS_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SALUS_ABI_VERSION 1
+
+/* Scheduling policies (§4; FIFO baseline P:504, 612-613). */
+enum { SALUS_FIFO = 0, SALUS_SRTF = 1, SALUS_PACK = 2, SALUS_FAIR = 3 };
+
+/* Job kinds: a training job runs forward+backward+SGD per iteration; an
+ * inference job runs one forward pass per request (§2.1, §5.3). */
+enum { SALUS_TRAIN = 0, SALUS_INFER = 1 };
+
+enum {
+  SALUS_OK = 0,
+  SALUS_E_INVAL = -1,          /* bad argument / descriptor                     */
+  SALUS_E_DUPLICATE = -2,      /* job id already submitted               */
+  SALUS_E_UNSCHEDULABLE = -3,  /* p + e > C pages: can never run alone (A22)    */
+  SALUS_E_STATE = -4,          /* call not valid in the context's state          */
+  SALUS_E_CAPACITY = -5,       /* a caller buffer / table is too small          */
+  SALUS_E_CUDA = -6,           /* CUDA runtime error (message has the string)   */
+  SALUS_E_STUCK = -7,          /* no event left with jobs unfinished (device)   */
+  SALUS_E_TIMEOUT = -8         /* salus_run exceeded cfg.timeout_ms; kernel was
+                                  told to abort and has exited                   */
+};
+
+/* salus_config.flags */
+enum {
+  SALUS_FLAG_LOG = 1,        /* record the canonical schedule log + wall stamps  */
+  SALUS_FLAG_NULL_WORK = 2,  /* schedule only: no iteration work is executed     */
+  SALUS_FLAG_CHECK = 4       /* device asserts the safety invariants every tick  */
+};
+
+/* salus_job.dump */
+enum {
+  SALUS_DUMP_OUTPUTS = 1,    /* keep fp32 A_L of every iteration / request       */
+  SALUS_DUMP_WEIGHTS = 2     /* keep fp32 master weights after the last iteration */
+};
+
+/* ---------------------------------------------------------------------
+ * Canonical schedule log: fixed-width little-endian 32-byte records.
+ * The byte-compare of this log against the CPU oracle is the schedule
+ * parity test (north star: "schedules must match the oracle bit-exactly").
+ * Order within a tick follows the phases of A15: completions/finishes,
+ * arrivals, admission, dispatch.
+ * ------------------------------------------------------------------- */
+typedef struct {
+  int64_t  tick;
+  uint32_t kind;   /* SALUS_REC_*                                   */
+  uint32_t lane;   /* lane id (monotonic, never reused, I5); NONE = 0xFFFFFFFF */
+  uint32_t job;    /* job id                                        */
+  uint32_t a;
+  uint64_t b;
+} salus_log_rec;
+
+enum {
+  SALUS_REC_DISPATCH = 1,    /* a = iteration index, b = global dispatch seq     */
+  SALUS_REC_LANE_OPEN = 2,   /* FindLane branch 1; a = L pages        */
+  SALUS_REC_LANE_REUSE = 3,  /* branch 2 (A1/A2); a = L pages          */
+  SALUS_REC_LANE_RESIZE = 4, /* branch 3 (A3); a = new L, b = old L    */
+  SALUS_REC_LANE_SHRINK = 5, /* JobFinish, residents remain (A4); a = new, b = old */
+  SALUS_REC_LANE_CLOSE = 6,  /* JobFinish, ref(lane) == 0             */
+  SALUS_REC_JOB_QUEUED = 7,  /* JobArrive: Q <- Q u {(P,E)}           */
+  SALUS_REC_JOB_ADMIT = 8,   /* ProcessRequests assigns a lane; a = p, b = e pages */
+  SALUS_REC_JOB_FINISH = 9   /* last iteration ended; a = n, b = completion_seq    */
+};
+
+/* Physical timing of one dispatched iteration (not part of the compared log):
+ * globaltimer ns of its first tile start and last tile end. */
+typedef struct {
+  uint64_t seq;
+  uint32_t lane, job;
+  uint64_t start_ns, end_ns;
+} salus_wall_rec;
+
+/* ---------------------------------------------------------------------
+ * Configuration
+ * ------------------------------------------------------------------- */
+typedef struct {
+  int32_t  device;           /* CUDA ordinal the arena/meta live on              */
+  uint32_t policy;           /* SALUS_FIFO..SALUS_FAIR                           */
+  void    *arena;            /* device, caller-owned, >= 256-byte aligned. The
+                                HBM arena all persistent regions and lanes are
+                                carved from (two-region layout P:365-369, paged
+                                per A18).                                        */
+  uint64_t arena_bytes;      /* >= floor(capacity_bytes/page_bytes)*page_bytes   */
+  void    *stream;           /* cudaStream_t the kernel is launched on (NULL =
+                                legacy default stream)                           */
+  uint64_t capacity_bytes;   /* C of the safety condition            */
+  uint32_t page_bytes;       /* 0 -> 65536. P_i, E_i and C are rounded to pages
+                                before every check: p = ceil(P/G), e = ceil(E/G),
+                                Cp = floor(C/G) (A18). Must be 65536 in v1.      */
+  uint32_t max_lanes;        /* 0 -> policy default (FIFO 1, SRTF 1, PACK 64,
+                                FAIR 1; A9); at most 64                           */
+  uint32_t max_jobs;         /* submit capacity; <= 4096                          */
+  uint32_t flags;            /* SALUS_FLAG_*                                      */
+  uint64_t switch_ticks;     /* logical switch penalty per job change in a lane
+                                (A16); 0 in parity tests                          */
+  uint64_t log_capacity;     /* records reserved for the log and for wall stamps */
+  uint64_t dump_bytes;       /* bytes reserved for SALUS_DUMP_* data             */
+  uint32_t n_workers;        /* worker CTAs; 0 -> (#SMs - 1)                      */
+  uint32_t timeout_ms;       /* salus_run watchdog; 0 -> 600000                   */
+} salus_config;
+
+typedef struct salus_ctx salus_ctx;
+
+/* Create a context.  Copies *cfg.  Errors: E_INVAL (bad policy, page size,
+ * capacity > arena, max_jobs out of range), E_CUDA. */
+int salus_open(const salus_config *cfg, salus_ctx **out);
+
+/* ---------------------------------------------------------------------
+ * Jobs ("sessions").  A job is a dense MLP with n_layers
+ * layers of widths dims[0..n_layers] (the "small-model forward/backward
+ * dense layers" of the north star), batch rows per iteration.
+ * ------------------------------------------------------------------- */
+typedef struct {
+  uint32_t job_id;           /* unique per context                               */
+  uint32_t kind;             /* SALUS_TRAIN | SALUS_INFER                        */
+  int64_t  arrival_tick;     /* JobArrive time                            */
+  uint64_t persistent_bytes; /* declared P_i: model + framework-internal (P:292-306,
+                                484); must be >= the job's device footprint       */
+  uint64_t ephemeral_bytes;  /* declared E_i: per-iteration scratch   */
+  uint32_t n_iters;          /* TRAIN: iterations; INFER: number of requests      */
+  uint32_t n_layers;         /* 1..8                                              */
+  uint64_t iter_ticks;       /* known per-iteration duration; the job's duration is
+                                n_iters*iter_ticks ("we assume the job
+                                execution time is known")                        */
+  uint32_t dims[9];          /* d_0..d_L, each 1..8192                            */
+  uint32_t batch;            /* 1..8192                                           */
+  float    lr;               /* SGD learning rate (TRAIN)                          */
+  uint32_t dump;             /* SALUS_DUMP_* bits                                  */
+  uint64_t seed;             /* data generator seed (A29)                          */
+  const int64_t *request_ticks; /* host; INFER: n_iters non-decreasing ticks
+                                   >= arrival_tick; copied at submit              */
+} salus_job;
+
+/* Footprint of a job in the device layout, so a
+ * caller can declare P_i/E_i >= it.  Host-only; no context needed. */
+int salus_job_footprint(const salus_job *job, uint64_t *persistent_bytes,
+                        uint64_t *ephemeral_bytes);
+
+/* Copy a job into the context.  Only before salus_prepare (else E_STATE).
+ * Errors: E_INVAL (shape/ticks/declared size below footprint), E_DUPLICATE,
+ * E_UNSCHEDULABLE (p + e > Cp, A22), E_CAPACITY (max_jobs / dump_bytes). */
+int salus_submit_job(salus_ctx *ctx, const salus_job *job);
+
+/* Device scratch ("meta") the context needs for the submitted jobs: job
+ * tables, page tables, free-page stack, lane slots, task ring, log, stats,
+ * dump area.  Valid after the last submit. */
+int salus_meta_bytes(const salus_ctx *ctx, uint64_t *bytes);
+
+/* Bind the caller-owned device buffer `meta` (>= salus_meta_bytes, 256-byte
+ * aligned) and upload the job tables on cfg.stream (host->device copies).
+ * After this no more jobs can be submitted. Errors: E_STATE, E_CAPACITY, E_CUDA. */
+int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes);
+
+/* Run the whole trace once: launch the persistent kernel on cfg.stream and
+ * wait for it (device-resident scheduler: no host round-trip per iteration).
+ * Every call is an independent, deterministic replay of the submitted jobs
+ * from an empty GPU.  `stats` (host, may be NULL) receives one record per
+ * job in submission order, *n_stats the count.  Errors: E_STATE (not
+ * prepared), E_CAPACITY (log/ring overflow), E_STUCK, E_TIMEOUT, E_CUDA. */
+typedef struct {
+  uint32_t job_id;
+  uint32_t first_lane;        /* lane the job was admitted to (one for life, I6) */
+  int64_t  admit_tick;
+  int64_t  first_start_tick;
+  int64_t  completion_tick;   /* JCT = completion_tick - arrival_tick            */
+  uint64_t completion_seq;    /* dispatch seq of its final iteration (A25)       */
+  uint64_t wall_start_ns;     /* globaltimer at its first tile start              */
+  uint64_t wall_end_ns;       /* globaltimer at its last tile end                 */
+} salus_job_stat;
+
+int salus_run(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats);
+
+/* Whole-run counters of the last salus_run. */
+typedef struct {
+  uint64_t n_dispatch;        /* iterations executed                              */
+  uint64_t n_ticks;           /* scheduler ticks processed                        */
+  uint64_t n_log;             /* log records written                              */
+  uint64_t n_tasks;           /* tile tasks executed by workers                   */
+  uint64_t kernel_ns;         /* CUDA-event time of the persistent kernel         */
+  uint64_t wall_first_ns, wall_last_ns;   /* globaltimer at kernel start / end   */
+  uint64_t sched_wait_ns;     /* scheduler time spent waiting for iterations      */
+  int32_t  status;            /* SALUS_OK or the device error code               */
+  uint32_t n_workers;
+} salus_run_stats;
+
+int salus_read_run_stats(const salus_ctx *ctx, salus_run_stats *out);
+
+/* Copy the canonical log of the last run (SALUS_FLAG_LOG) into buf (host).
+ * *n_bytes = bytes written.  E_CAPACITY if cap_bytes is too small. */
+int salus_read_log(salus_ctx *ctx, void *buf, uint64_t cap_bytes, uint64_t *n_bytes);
+
+/* Copy the wall stamps (salus_wall_rec, in dispatch-seq order). */
+int salus_read_wall(salus_ctx *ctx, salus_wall_rec *buf, uint64_t cap_recs, uint64_t *n_recs);
+
+/* Dumped fp32 data of a job submitted with `dump`:
+ *   iter <  n_iters   : A_L of that iteration/request, batch x d_L row-major
+ *   iter == 0xFFFFFFFF: final weights W_1..W_L concatenated, each
+ *                       d_{l-1} x d_l row-major (Z = A W orientation)
+ * *n = floats written.  E_INVAL if the job did not dump that item. */
+int salus_read_layers(salus_ctx *ctx, uint32_t job_id, uint32_t iter, float *buf,
+                      uint64_t cap_floats, uint64_t *n);
+
+const char *salus_last_error(const salus_ctx *ctx);
+
+/* Release the host context (NULL-safe).  Never frees caller buffers. */
+int salus_close(salus_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SALUS_H_ */

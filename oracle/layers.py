@@ -16,17 +16,31 @@ hidden layers, MSE loss and plain SGD (SURVEY §8(c) "Math per DISPATCH"):
                 W_l -= lr * dW_l
 
 Plain numpy float64; `@` (a library matmul) is the only primitive used.
-The schedule never influences the math of a job except through iteration
-order, which is always k = 0, 1, ..., n-1 (jobs switch only at
-iteration boundaries).
+
+Precision modes (reading A31).  `store=None` is the definition
+above in fp64.  The ReLU mask [A > 0] is a floating-point value deciding an
+integer (0/1); by the parity rules both sides must take that decision in the
+same precision, the kernel's.  `store=bf16` therefore rounds (fp64 -> fp32 ->
+bf16, round-to-nearest-even) exactly the tensors the kernel keeps in bf16:
+the weight copy used by the GEMMs, A_l for l >= 1, and every G_l; the master
+weights, Z_l and all sums stay fp64.  Nothing else changes.
 """
-from typing import List
+from typing import Callable, List, Optional
 
 import numpy as np
 
 from . import datagen as DG
 
 TRAIN, INFER = 0, 1
+
+
+def bf16(x: np.ndarray) -> np.ndarray:
+    """Storage rounding of the kernel: fp64 -> fp32 (RNE) -> bf16 (RNE)."""
+    return DG.bf16_rne(np.asarray(x, dtype=np.float64).astype(np.float32)).astype(np.float64)
+
+
+def _ident(x):
+    return x
 
 
 def init_weights(job) -> List[np.ndarray]:
@@ -43,12 +57,13 @@ def inputs(job, k: int):
     return X, T
 
 
-def forward(W: List[np.ndarray], X: np.ndarray) -> List[np.ndarray]:
+def forward(W: List[np.ndarray], X: np.ndarray, store: Optional[Callable] = None) -> List[np.ndarray]:
+    rnd = store or _ident
     A = [X]
     L = len(W)
     for l in range(1, L + 1):
-        Z = A[l - 1] @ W[l - 1]
-        A.append(np.maximum(Z, 0.0) if l < L else Z)
+        Z = A[l - 1] @ rnd(W[l - 1])
+        A.append(rnd(np.maximum(Z, 0.0)) if l < L else Z)
     return A
 
 
@@ -57,36 +72,37 @@ def loss(W, X, T) -> float:
     return float(0.5 / X.shape[0] * np.sum((A[-1] - T) ** 2))
 
 
-def gradients(W: List[np.ndarray], X: np.ndarray, T: np.ndarray):
+def gradients(W: List[np.ndarray], X: np.ndarray, T: np.ndarray, store: Optional[Callable] = None):
     """Returns (A list, [dW_1..dW_L]) for the loss 1/(2B)||A_L - T||^2."""
-    A = forward(W, X)
+    rnd = store or _ident
+    A = forward(W, X, store)
     L = len(W)
     B = X.shape[0]
-    G = (A[L] - T) / B
+    G = rnd((A[L] - T) / B)
     dW = [None] * L
     for l in range(L, 0, -1):
         dW[l - 1] = A[l - 1].T @ G
         if l > 1:
-            G = (G @ W[l - 1].T) * (A[l - 1] > 0)
+            G = rnd((G @ rnd(W[l - 1]).T) * (A[l - 1] > 0))
     return A, dW
 
 
-def train_step(W: List[np.ndarray], job, k: int) -> np.ndarray:
+def train_step(W: List[np.ndarray], job, k: int, store: Optional[Callable] = None) -> np.ndarray:
     """One SGD iteration in place; returns the output A_L (B x d_L)."""
     X, T = inputs(job, k)
-    A, dW = gradients(W, X, T)
+    A, dW = gradients(W, X, T, store)
     lr = float(np.float32(job.lr))
     for l in range(len(W)):
         W[l] -= lr * dW[l]
     return A[-1]
 
 
-def infer_step(W: List[np.ndarray], job, k: int) -> np.ndarray:
+def infer_step(W: List[np.ndarray], job, k: int, store: Optional[Callable] = None) -> np.ndarray:
     X, _ = inputs(job, k)
-    return forward(W, X)[-1]
+    return forward(W, X, store)[-1]
 
 
-def run_job(job, iters=None):
+def run_job(job, iters=None, store: Optional[Callable] = None):
     """Run iterations 0..n-1 (or the listed prefix) of one job.
 
     Returns (outputs {k: A_L}, final weights)."""
@@ -94,5 +110,5 @@ def run_job(job, iters=None):
     n = job.n_iters if iters is None else iters
     outs = {}
     for k in range(n):
-        outs[k] = train_step(W, job, k) if job.kind == TRAIN else infer_step(W, job, k)
+        outs[k] = train_step(W, job, k, store) if job.kind == TRAIN else infer_step(W, job, k, store)
     return outs, W

@@ -189,7 +189,8 @@ def simulate(jobs, capacity_bytes: int, policy: int, *, page_bytes: int = 65536,
     stats: Dict[int, JobStat] = {}
 
     by_arrival = sorted(J.values(), key=lambda j: (j.arrival_tick, j.job_id))
-    infer_ids = sorted(jid for jid, j in J.items() if j.kind == INFER)
+    # inference jobs are visited in (arrival, id) order, like every other tie (A15)
+    infer_ids = [j.job_id for j in by_arrival if j.kind == INFER]
     arr_ptr = 0
     lanes: List[_Lane] = []          # kept in lane-id order
     lane_by_id: Dict[int, _Lane] = {}

@@ -1,0 +1,112 @@
+// salus_dev.h — internal structures shared by the host library and the
+// persistent kernel (never by oracle/).  Layouts are described in DESIGN.md
+// ("Data layout in HBM", "Meta buffer").
+#pragma once
+#include <stdint.h>
+#include "../../include/salus.h"
+
+namespace salus {
+
+constexpr int MAX_LANES = 64;          // lane table (A9)
+constexpr int MAX_JOBS = 2048;         // scheduler SMEM tables
+constexpr int MAX_LAYERS = 8;
+constexpr int MAX_STAGES = 2 + 2 * MAX_LAYERS;   // INIT, GEN, F_1..F_L, B_L..B_1
+constexpr uint32_t PAGE_SHIFT = 16;    // 64 KiB pages (A18)
+constexpr uint32_t PAGE_BYTES = 1u << PAGE_SHIFT;
+constexpr uint32_t NONE32 = 0xFFFFFFFFu;
+constexpr uint32_t TASK_EXIT = 0xFFFFFFFFu;
+
+// Job states (oracle: NOT_ARRIVED, QUEUED, ADMITTED, DONE)
+enum : uint8_t { ST_NOT_ARRIVED = 0, ST_QUEUED = 1, ST_ADMITTED = 2, ST_DONE = 3 };
+
+// Static per-job descriptor, uploaded by salus_prepare.  The dense index of
+// a job is its rank in (arrival_tick, job_id) order, so every "(arrival, id)"
+// tie-break of the readings (A11-A15) is a comparison of dense indices.
+struct DevJob {
+  uint32_t job_id, kind, n_layers, batch;
+  int64_t arrival, iter_ticks;
+  uint32_t n_iters, p_pages, e_pages;     // declared sizes in pages (schedule)
+  uint32_t ap_pages, ae_pages;            // actual backing pages (device layout)
+  uint32_t bpad;                          // batch padded to 128
+  uint32_t dims[MAX_LAYERS + 1];          // logical widths
+  uint32_t dpad[MAX_LAYERS + 1];          // padded to 128
+  float lr;
+  uint32_t dump;
+  uint64_t seed;
+  uint32_t req_off;                       // index into request tick array
+  uint32_t pt_off;                        // index into the persistent page-table pool
+  uint64_t dump_out_off;                  // float offset of outputs in the dump area
+  uint64_t dump_w_off;                    // float offset of final weights
+  // byte offsets inside the job's persistent space: per layer W32, Wb[0], Wb[1]
+  uint32_t w32_off[MAX_LAYERS], wb_off[MAX_LAYERS][2];
+  // byte offsets inside the lane's ephemeral space: act[0]=X, act[l]=A_l; g[2]
+  uint32_t act_off[MAX_LAYERS + 1], g_off[2];
+  uint32_t n_stages;                      // stages of a non-first iteration path
+  uint32_t stage_tiles[MAX_STAGES];       // tiles per stage
+};
+
+// One physical lane slot: the dispatch record the scheduler writes and the
+// per-stage completion counters the worker CTAs update.  256-B aligned.
+struct alignas(256) Slot {
+  uint32_t job;             // dense job index of the in-flight iteration
+  uint32_t iter;            // iteration index k
+  uint64_t seq;             // global dispatch seq
+  uint64_t start_ns;        // min globaltimer over first-stage tiles (atomicMin)
+  uint64_t end_ns;          // globaltimer when the last stage completed
+  uint64_t done_seq;        // seq + 1 once the iteration is physically complete
+  uint32_t stage_done[MAX_STAGES + 2];
+};
+
+// Control block at the start of meta.
+struct alignas(256) Ctrl {
+  unsigned long long q_head;     // task ring: next position to publish
+  unsigned long long q_tail;     // next position to claim
+  unsigned long long n_tasks;
+  uint32_t abort;                // set on device error or host abort
+  int32_t status;                // SALUS_OK or SALUS_E_*
+  uint32_t err_info[4];
+  uint64_t n_dispatch, n_ticks, n_log, sched_wait_ns;
+  uint64_t wall_first_ns, wall_last_ns;
+  uint32_t log_overflow, n_workers;
+};
+
+struct Params {
+  uint8_t *arena;
+  Ctrl *ctrl;
+  const DevJob *jobs;
+  const int64_t *req_ticks;
+  const uint16_t *infer_list;      // dense indices of INFER jobs, ascending
+  uint32_t *ppt;                   // persistent page tables (pool)
+  uint32_t *lpt;                   // lane page tables: MAX_LANES x lpt_stride
+  uint32_t lpt_stride;
+  uint32_t *free_stack;            // Cp entries
+  Slot *slots;                     // MAX_LANES
+  unsigned long long *ring;        // task ring (seq << 32 | payload)
+  uint32_t ring_mask;
+  salus_log_rec *log;
+  salus_wall_rec *wall;
+  uint64_t log_cap;
+  salus_job_stat *stats;           // dense order
+  float *dump;
+  const volatile uint32_t *host_abort;   // mapped pinned host flag
+  uint32_t n_jobs, n_infer, Cp, policy, max_lanes, flags, n_workers;
+  int64_t switch_ticks;
+  uint64_t timeout_ns;
+};
+
+// task payload: slot (6 bits) | stage (5 bits) | tile (21 bits)
+__host__ __device__ inline uint32_t task_pack(uint32_t slot, uint32_t stage, uint32_t tile) {
+  return (slot << 26) | (stage << 21) | tile;
+}
+
+// Stage numbering: 0 INIT (first iteration only), 1 GEN, 2..L+1 F_1..F_L,
+// L+2..2L+1 B_L..B_1 (TRAIN only).
+__host__ __device__ inline uint32_t last_stage(uint32_t kind, uint32_t L) {
+  return kind == SALUS_TRAIN ? 2 * L + 1 : L + 1;
+}
+
+__host__ __device__ inline uint32_t ntile_for(uint32_t dpad) {   // GEMM N tile
+  return (dpad % 256 == 0) ? 256 : 128;
+}
+
+}  // namespace salus

@@ -1,0 +1,524 @@
+// salus_host.cpp — host side of the C ABI (include/salus.h): validation,
+// page rounding (A18), device-layout footprints, meta-buffer layout, job
+// table upload, cooperative launch of the persistent kernel, watchdog, and
+// readback.  No per-iteration host work: one launch per salus_run.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <unordered_map>
+#include <vector>
+
+#include "salus_dev.h"
+
+namespace salus {
+int launch_persistent(const Params &P, uint32_t grid, cudaStream_t stream);
+int max_coresident_grid(int device, int *grid);
+}  // namespace salus
+
+using namespace salus;
+
+namespace {
+
+inline uint64_t pad128(uint64_t x) { return (x + 127) / 128 * 128; }
+inline uint64_t align_up(uint64_t x, uint64_t a) { return (x + a - 1) / a * a; }
+
+struct Footprint {
+  uint64_t p, e;
+};
+
+Footprint footprint(const salus_job &j) {
+  const uint32_t L = j.n_layers;
+  uint64_t dp[MAX_LAYERS + 1], mx = 0;
+  for (uint32_t l = 0; l <= L; l++) { dp[l] = pad128(j.dims[l]); mx = std::max(mx, dp[l]); }
+  const uint64_t bp = pad128(j.batch);
+  uint64_t w = 0;
+  for (uint32_t l = 1; l <= L; l++) w += dp[l - 1] * dp[l];
+  Footprint f;
+  if (j.kind == SALUS_TRAIN) {
+    uint64_t inner = 0;
+    for (uint32_t l = 1; l < L; l++) inner += dp[l];
+    f.p = 8 * w;
+    f.e = 2 * bp * (dp[0] + inner) + 2 * (2 * bp * mx);
+  } else {
+    uint64_t s = 0;
+    for (uint32_t l = 0; l <= L; l++) s += dp[l];
+    f.p = 2 * w;
+    f.e = 2 * bp * s;
+  }
+  return f;
+}
+
+struct HostJob {
+  salus_job j;
+  std::vector<int64_t> req;
+  Footprint fp;
+  uint32_t submit_idx;
+};
+
+}  // namespace
+
+struct salus_ctx {
+  salus_config cfg{};
+  int state = 0;                       // 0 open, 1 prepared
+  std::vector<HostJob> jobs;
+  std::unordered_map<uint32_t, uint32_t> id_to_submit;
+  std::string err;
+  uint32_t Cp = 0;
+  uint64_t dump_floats = 0;
+  // prepared state
+  uint8_t *meta = nullptr;
+  uint64_t meta_bytes = 0;
+  Params P{};
+  std::vector<DevJob> djobs;           // dense order
+  std::vector<uint32_t> dense_to_submit;
+  std::unordered_map<uint32_t, uint32_t> id_to_dense;
+  uint32_t grid = 0;
+  uint64_t ring_cap = 0, log_cap = 0;
+  uint64_t off_ctrl = 0, off_jobs = 0, off_req = 0, off_inf = 0, off_ppt = 0, off_lpt = 0, off_free = 0,
+           off_slots = 0, off_ring = 0, off_log = 0, off_wall = 0, off_stats = 0, off_dump = 0, total = 0;
+  uint32_t lpt_stride = 0;
+  uint32_t *host_abort = nullptr;
+  uint32_t *host_abort_dev = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  salus_run_stats last{};
+  bool ran = false;
+};
+
+namespace {
+
+int fail(salus_ctx *c, int code, const std::string &msg) {
+  if (c) c->err = msg;
+  return code;
+}
+int cuda_fail(salus_ctx *c, cudaError_t e, const char *where) {
+  return fail(c, SALUS_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+uint32_t default_max_lanes(uint32_t policy) {
+  switch (policy) {
+    case SALUS_PACK: return 64;
+    default: return 1;   // FIFO, SRTF, FAIR (A9)
+  }
+}
+
+int validate_job(const salus_job *j, bool null_work, std::string *why) {
+  if (j->kind > SALUS_INFER) { *why = "kind"; return SALUS_E_INVAL; }
+  if (j->n_layers < 1 || j->n_layers > MAX_LAYERS) { *why = "n_layers must be 1..8"; return SALUS_E_INVAL; }
+  for (uint32_t l = 0; l <= j->n_layers; l++)
+    if (j->dims[l] < 1 || j->dims[l] > 8192) { *why = "dims must be 1..8192"; return SALUS_E_INVAL; }
+  if (j->batch < 1 || j->batch > 8192) { *why = "batch must be 1..8192"; return SALUS_E_INVAL; }
+  if (j->n_iters < 1 || j->iter_ticks < 1) { *why = "n_iters and iter_ticks must be >= 1"; return SALUS_E_INVAL; }
+  if (j->arrival_tick < 0 || j->arrival_tick > (int64_t)1 << 60) { *why = "arrival_tick"; return SALUS_E_INVAL; }
+  if ((long double)j->n_iters * (long double)j->iter_ticks >= (long double)(1ull << 52)) {
+    *why = "n_iters * iter_ticks must be < 2^52";
+    return SALUS_E_INVAL;
+  }
+  if (j->kind == SALUS_INFER) {
+    if (!j->request_ticks) { *why = "INFER job needs request_ticks"; return SALUS_E_INVAL; }
+    int64_t prev = j->arrival_tick;
+    for (uint32_t k = 0; k < j->n_iters; k++) {
+      if (j->request_ticks[k] < prev) { *why = "request_ticks must be sorted and >= arrival"; return SALUS_E_INVAL; }
+      prev = j->request_ticks[k];
+    }
+  }
+  if (!std::isfinite(j->lr)) { *why = "lr"; return SALUS_E_INVAL; }
+  Footprint f = footprint(*j);
+  if (!null_work && (j->persistent_bytes < f.p || j->ephemeral_bytes < f.e)) {
+    *why = "declared persistent/ephemeral bytes below the device footprint (salus_job_footprint)";
+    return SALUS_E_INVAL;
+  }
+  return SALUS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int salus_job_footprint(const salus_job *job, uint64_t *persistent_bytes, uint64_t *ephemeral_bytes) {
+  if (!job || job->n_layers < 1 || job->n_layers > MAX_LAYERS) return SALUS_E_INVAL;
+  Footprint f = footprint(*job);
+  if (persistent_bytes) *persistent_bytes = f.p;
+  if (ephemeral_bytes) *ephemeral_bytes = f.e;
+  return SALUS_OK;
+}
+
+int salus_open(const salus_config *cfg, salus_ctx **out) {
+  if (!cfg || !out) return SALUS_E_INVAL;
+  *out = nullptr;
+  salus_config c = *cfg;
+  if (c.page_bytes == 0) c.page_bytes = PAGE_BYTES;
+  if (c.page_bytes != PAGE_BYTES) return SALUS_E_INVAL;
+  if (c.policy > SALUS_FAIR) return SALUS_E_INVAL;
+  if (c.max_lanes == 0) c.max_lanes = default_max_lanes(c.policy);
+  if (c.max_lanes > MAX_LANES) return SALUS_E_INVAL;
+  if (c.max_jobs == 0 || c.max_jobs > MAX_JOBS) return SALUS_E_INVAL;
+  const uint64_t Cp = c.capacity_bytes / c.page_bytes;
+  if (Cp == 0 || Cp > 0xFFFFFFF0ull) return SALUS_E_INVAL;
+  if (!c.arena || (reinterpret_cast<uintptr_t>(c.arena) & 255) || c.arena_bytes < Cp * c.page_bytes)
+    return SALUS_E_INVAL;
+  if (c.timeout_ms == 0) c.timeout_ms = 600000;
+  salus_ctx *ctx = new salus_ctx();
+  ctx->cfg = c;
+  ctx->Cp = (uint32_t)Cp;
+  *out = ctx;
+  return SALUS_OK;
+}
+
+int salus_submit_job(salus_ctx *ctx, const salus_job *job) {
+  if (!ctx || !job) return SALUS_E_INVAL;
+  if (ctx->state != 0) return fail(ctx, SALUS_E_STATE, "submit after prepare");
+  if (ctx->id_to_submit.count(job->job_id)) return fail(ctx, SALUS_E_DUPLICATE, "duplicate job id");
+  std::string why;
+  int rc = validate_job(job, (ctx->cfg.flags & SALUS_FLAG_NULL_WORK) != 0, &why);
+  if (rc) return fail(ctx, rc, "job " + std::to_string(job->job_id) + ": " + why);
+  const uint64_t G = ctx->cfg.page_bytes;
+  const uint64_t p = (job->persistent_bytes + G - 1) / G, e = (job->ephemeral_bytes + G - 1) / G;
+  if (p + e > ctx->Cp) return fail(ctx, SALUS_E_UNSCHEDULABLE, "p + e > C pages (A22)");
+  if (ctx->jobs.size() >= ctx->cfg.max_jobs) return fail(ctx, SALUS_E_CAPACITY, "max_jobs reached");
+  uint64_t df = 0;
+  if (job->dump & SALUS_DUMP_OUTPUTS) df += (uint64_t)job->n_iters * job->batch * job->dims[job->n_layers];
+  if (job->dump & SALUS_DUMP_WEIGHTS)
+    for (uint32_t l = 1; l <= job->n_layers; l++) df += (uint64_t)job->dims[l - 1] * job->dims[l];
+  if (ctx->cfg.dump_bytes && (ctx->dump_floats + df) * 4 > ctx->cfg.dump_bytes)
+    return fail(ctx, SALUS_E_CAPACITY, "dump_bytes exceeded");
+  HostJob h;
+  h.j = *job;
+  if (job->kind == SALUS_INFER) h.req.assign(job->request_ticks, job->request_ticks + job->n_iters);
+  h.j.request_ticks = nullptr;
+  h.fp = footprint(*job);
+  h.submit_idx = (uint32_t)ctx->jobs.size();
+  ctx->dump_floats += df;
+  ctx->id_to_submit[job->job_id] = h.submit_idx;
+  ctx->jobs.push_back(std::move(h));
+  return SALUS_OK;
+}
+
+static void compute_layout(salus_ctx *c) {
+  const uint32_t n = (uint32_t)c->jobs.size();
+  // dense order = (arrival, id) rank
+  std::vector<uint32_t> order(n);
+  for (uint32_t i = 0; i < n; i++) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    const salus_job &x = c->jobs[a].j, &y = c->jobs[b].j;
+    return x.arrival_tick != y.arrival_tick ? x.arrival_tick < y.arrival_tick : x.job_id < y.job_id;
+  });
+  c->dense_to_submit = order;
+  c->djobs.assign(n, DevJob{});
+  c->id_to_dense.clear();
+  const uint64_t G = c->cfg.page_bytes;
+  uint64_t req_total = 0, ppt_total = 0, dump_cur = 0, max_ae = 1, max_tiles = 1, dispatches = 0;
+  for (uint32_t d = 0; d < n; d++) {
+    const HostJob &h = c->jobs[order[d]];
+    const salus_job &j = h.j;
+    DevJob &D = c->djobs[d];
+    c->id_to_dense[j.job_id] = d;
+    D.job_id = j.job_id; D.kind = j.kind; D.n_layers = j.n_layers; D.batch = j.batch;
+    D.arrival = j.arrival_tick; D.iter_ticks = (int64_t)j.iter_ticks; D.n_iters = j.n_iters;
+    D.p_pages = (uint32_t)((j.persistent_bytes + G - 1) / G);
+    D.e_pages = (uint32_t)((j.ephemeral_bytes + G - 1) / G);
+    // backing pages: the device footprint (<= declared, so the pool of Cp pages
+    // can never run dry under the safety condition); in NULL_WORK mode the
+    // allocator still runs, bounded by the declared sizes
+    D.ap_pages = (uint32_t)std::min<uint64_t>((h.fp.p + G - 1) / G, D.p_pages);
+    D.ae_pages = (uint32_t)std::min<uint64_t>((h.fp.e + G - 1) / G, D.e_pages);
+    D.bpad = (uint32_t)pad128(j.batch);
+    const uint32_t L = j.n_layers;
+    for (uint32_t l = 0; l <= MAX_LAYERS; l++) {
+      D.dims[l] = l <= L ? j.dims[l] : 0;
+      D.dpad[l] = l <= L ? (uint32_t)pad128(j.dims[l]) : 0;
+    }
+    D.lr = j.lr; D.dump = j.dump; D.seed = j.seed;
+    D.req_off = (uint32_t)req_total;
+    if (j.kind == SALUS_INFER) req_total += j.n_iters;
+    D.pt_off = (uint32_t)ppt_total;
+    ppt_total += D.ap_pages;
+    // persistent tensors
+    uint64_t off = 0;
+    for (uint32_t l = 1; l <= L; l++) {
+      const uint64_t w = (uint64_t)D.dpad[l - 1] * D.dpad[l];
+      if (j.kind == SALUS_TRAIN) {
+        D.w32_off[l - 1] = (uint32_t)off; off += 4 * w;
+        D.wb_off[l - 1][0] = (uint32_t)off; off += 2 * w;
+        D.wb_off[l - 1][1] = (uint32_t)off; off += 2 * w;
+      } else {
+        D.w32_off[l - 1] = 0;
+        D.wb_off[l - 1][0] = D.wb_off[l - 1][1] = (uint32_t)off; off += 2 * w;
+      }
+    }
+    // ephemeral tensors
+    off = 0;
+    const uint64_t bp = D.bpad;
+    const uint32_t nact = j.kind == SALUS_TRAIN ? L : L + 1;   // act[0..nact-1]
+    uint32_t mx = 0;
+    for (uint32_t l = 0; l <= L; l++) mx = std::max(mx, D.dpad[l]);
+    for (uint32_t l = 0; l < nact; l++) { D.act_off[l] = (uint32_t)off; off += 2 * bp * D.dpad[l]; }
+    if (j.kind == SALUS_TRAIN) {
+      D.g_off[0] = (uint32_t)off; off += 2 * bp * mx;
+      D.g_off[1] = (uint32_t)off; off += 2 * bp * mx;
+    }
+    // stage tiles
+    uint32_t ti = 0;
+    for (uint32_t l = 1; l <= L; l++) ti += (D.dpad[l] / 128) * (D.dpad[l - 1] / 128);
+    D.stage_tiles[0] = ti;
+    D.stage_tiles[1] = (D.bpad / 128) * (D.dpad[0] / 128);
+    for (uint32_t l = 1; l <= L; l++) D.stage_tiles[1 + l] = (D.bpad / 128) * (D.dpad[l] / ntile_for(D.dpad[l]));
+    if (j.kind == SALUS_TRAIN) {
+      for (uint32_t l = L; l >= 1; l--) {
+        const uint32_t s = L + 2 + (L - l), nt = ntile_for(D.dpad[l - 1]);
+        D.stage_tiles[s] = (D.dpad[l] / 128) * (D.dpad[l - 1] / nt) + (l > 1 ? (D.bpad / 128) * (D.dpad[l - 1] / nt) : 0);
+      }
+    }
+    D.n_stages = last_stage(j.kind, L) + 1;
+    for (uint32_t s = 0; s < D.n_stages; s++) max_tiles = std::max<uint64_t>(max_tiles, D.stage_tiles[s]);
+    D.dump_out_off = dump_cur;
+    if (j.dump & SALUS_DUMP_OUTPUTS) dump_cur += (uint64_t)j.n_iters * j.batch * j.dims[L];
+    D.dump_w_off = dump_cur;
+    if (j.dump & SALUS_DUMP_WEIGHTS)
+      for (uint32_t l = 1; l <= L; l++) dump_cur += (uint64_t)j.dims[l - 1] * j.dims[l];
+    max_ae = std::max<uint64_t>(max_ae, D.ae_pages);
+    dispatches += j.n_iters;
+  }
+  c->lpt_stride = (uint32_t)max_ae;
+  uint64_t rc = 1024;
+  const uint64_t need = 2 * (MAX_LANES * max_tiles + 4096);
+  while (rc < need) rc <<= 1;
+  c->ring_cap = rc;
+  c->log_cap = 0;
+  if (c->cfg.flags & SALUS_FLAG_LOG)
+    c->log_cap = c->cfg.log_capacity ? c->cfg.log_capacity : dispatches + 6ull * n + 16;
+  uint64_t o = 0;
+  auto take = [&](uint64_t bytes) { uint64_t r = o; o = align_up(o + bytes, 256); return r; };
+  c->off_ctrl = take(sizeof(Ctrl));
+  c->off_jobs = take(sizeof(DevJob) * std::max<uint64_t>(n, 1));
+  c->off_req = take(8 * std::max<uint64_t>(req_total, 1));
+  c->off_inf = take(2 * std::max<uint64_t>(n, 1));
+  c->off_ppt = take(4 * std::max<uint64_t>(ppt_total, 1));
+  c->off_lpt = take(4ull * MAX_LANES * c->lpt_stride);
+  c->off_free = take(4ull * c->Cp);
+  c->off_slots = take(sizeof(Slot) * MAX_LANES);
+  c->off_ring = take(8 * c->ring_cap);
+  c->off_log = take(sizeof(salus_log_rec) * std::max<uint64_t>(c->log_cap, 1));
+  c->off_wall = take(sizeof(salus_wall_rec) * std::max<uint64_t>(c->log_cap, 1));
+  c->off_stats = take(sizeof(salus_job_stat) * std::max<uint64_t>(n, 1));
+  c->off_dump = take(4 * std::max<uint64_t>(dump_cur, 1));
+  c->total = o;
+}
+
+int salus_meta_bytes(const salus_ctx *ctx, uint64_t *bytes) {
+  if (!ctx || !bytes) return SALUS_E_INVAL;
+  compute_layout(const_cast<salus_ctx *>(ctx));
+  *bytes = ctx->total;
+  return SALUS_OK;
+}
+
+int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
+  if (!ctx) return SALUS_E_INVAL;
+  if (ctx->state != 0) return fail(ctx, SALUS_E_STATE, "already prepared");
+  if (ctx->jobs.empty()) return fail(ctx, SALUS_E_STATE, "no jobs submitted");
+  compute_layout(ctx);
+  if (!meta || (reinterpret_cast<uintptr_t>(meta) & 255)) return fail(ctx, SALUS_E_INVAL, "meta must be 256-B aligned");
+  if (meta_bytes < ctx->total) return fail(ctx, SALUS_E_CAPACITY, "meta buffer too small");
+  cudaError_t e = cudaSetDevice(ctx->cfg.device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  int grid = 0;
+  int rc = max_coresident_grid(ctx->cfg.device, &grid);
+  if (rc) return cuda_fail(ctx, (cudaError_t)rc, "occupancy");
+  if (grid < 2) return fail(ctx, SALUS_E_CUDA, "persistent kernel does not fit one CTA per SM");
+  if (ctx->cfg.n_workers && (int)ctx->cfg.n_workers + 1 < grid) grid = (int)ctx->cfg.n_workers + 1;
+  ctx->grid = (uint32_t)grid;
+  ctx->meta = static_cast<uint8_t *>(meta);
+  ctx->meta_bytes = meta_bytes;
+  const uint32_t n = (uint32_t)ctx->jobs.size();
+  cudaStream_t st = static_cast<cudaStream_t>(ctx->cfg.stream);
+  std::vector<int64_t> req;
+  std::vector<uint16_t> inf;
+  for (uint32_t d = 0; d < n; d++) {
+    const HostJob &h = ctx->jobs[ctx->dense_to_submit[d]];
+    if (h.j.kind == SALUS_INFER) {
+      req.insert(req.end(), h.req.begin(), h.req.end());
+      inf.push_back((uint16_t)d);
+    }
+  }
+  uint8_t *m = ctx->meta;
+  if ((e = cudaMemcpyAsync(m + ctx->off_jobs, ctx->djobs.data(), sizeof(DevJob) * n, cudaMemcpyHostToDevice, st)))
+    return cuda_fail(ctx, e, "upload jobs");
+  if (!req.empty() &&
+      (e = cudaMemcpyAsync(m + ctx->off_req, req.data(), 8 * req.size(), cudaMemcpyHostToDevice, st)))
+    return cuda_fail(ctx, e, "upload requests");
+  if (!inf.empty() &&
+      (e = cudaMemcpyAsync(m + ctx->off_inf, inf.data(), 2 * inf.size(), cudaMemcpyHostToDevice, st)))
+    return cuda_fail(ctx, e, "upload infer list");
+  if ((e = cudaStreamSynchronize(st))) return cuda_fail(ctx, e, "sync");
+  if ((e = cudaHostAlloc(reinterpret_cast<void **>(&ctx->host_abort), 4, cudaHostAllocMapped)))
+    return cuda_fail(ctx, e, "cudaHostAlloc");
+  *reinterpret_cast<volatile uint32_t *>(ctx->host_abort) = 0;
+  if ((e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&ctx->host_abort_dev), ctx->host_abort, 0)))
+    return cuda_fail(ctx, e, "cudaHostGetDevicePointer");
+  if ((e = cudaEventCreate(&ctx->ev0)) || (e = cudaEventCreate(&ctx->ev1))) return cuda_fail(ctx, e, "events");
+
+  Params &P = ctx->P;
+  P.arena = static_cast<uint8_t *>(ctx->cfg.arena);
+  P.ctrl = reinterpret_cast<Ctrl *>(m + ctx->off_ctrl);
+  P.jobs = reinterpret_cast<const DevJob *>(m + ctx->off_jobs);
+  P.req_ticks = reinterpret_cast<const int64_t *>(m + ctx->off_req);
+  P.infer_list = reinterpret_cast<const uint16_t *>(m + ctx->off_inf);
+  P.ppt = reinterpret_cast<uint32_t *>(m + ctx->off_ppt);
+  P.lpt = reinterpret_cast<uint32_t *>(m + ctx->off_lpt);
+  P.lpt_stride = ctx->lpt_stride;
+  P.free_stack = reinterpret_cast<uint32_t *>(m + ctx->off_free);
+  P.slots = reinterpret_cast<Slot *>(m + ctx->off_slots);
+  P.ring = reinterpret_cast<unsigned long long *>(m + ctx->off_ring);
+  P.ring_mask = (uint32_t)(ctx->ring_cap - 1);
+  P.log = reinterpret_cast<salus_log_rec *>(m + ctx->off_log);
+  P.wall = reinterpret_cast<salus_wall_rec *>(m + ctx->off_wall);
+  P.log_cap = ctx->log_cap;
+  P.stats = reinterpret_cast<salus_job_stat *>(m + ctx->off_stats);
+  P.dump = reinterpret_cast<float *>(m + ctx->off_dump);
+  P.host_abort = ctx->host_abort_dev;
+  P.n_jobs = n;
+  P.n_infer = (uint32_t)inf.size();
+  P.Cp = ctx->Cp;
+  P.policy = ctx->cfg.policy;
+  P.max_lanes = ctx->cfg.max_lanes;
+  P.flags = ctx->cfg.flags;
+  P.n_workers = ctx->grid - 1;
+  P.switch_ticks = (int64_t)ctx->cfg.switch_ticks;
+  P.timeout_ns = (uint64_t)ctx->cfg.timeout_ms * 1000000ull;
+  ctx->state = 1;
+  return SALUS_OK;
+}
+
+int salus_run(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats) {
+  if (!ctx) return SALUS_E_INVAL;
+  if (ctx->state != 1) return fail(ctx, SALUS_E_STATE, "salus_prepare first");
+  cudaError_t e = cudaSetDevice(ctx->cfg.device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  cudaStream_t st = static_cast<cudaStream_t>(ctx->cfg.stream);
+  uint8_t *m = ctx->meta;
+  if ((e = cudaMemsetAsync(m + ctx->off_ctrl, 0, sizeof(Ctrl), st)) ||
+      (e = cudaMemsetAsync(m + ctx->off_slots, 0, sizeof(Slot) * MAX_LANES, st)) ||
+      (e = cudaMemsetAsync(m + ctx->off_ring, 0, 8 * ctx->ring_cap, st)))
+    return cuda_fail(ctx, e, "reset");
+  *reinterpret_cast<volatile uint32_t *>(ctx->host_abort) = 0;
+  if ((e = cudaEventRecord(ctx->ev0, st))) return cuda_fail(ctx, e, "event");
+  int rc = launch_persistent(ctx->P, ctx->grid, st);
+  if (rc) return cuda_fail(ctx, (cudaError_t)rc, "cooperative launch");
+  if ((e = cudaEventRecord(ctx->ev1, st))) return cuda_fail(ctx, e, "event");
+  // host watchdog: poll, then ask the kernel to abort (mapped pinned flag)
+  const auto t0 = std::chrono::steady_clock::now();
+  bool timed_out = false;
+  for (;;) {
+    e = cudaEventQuery(ctx->ev1);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) return cuda_fail(ctx, e, "kernel");
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (!timed_out && ms > ctx->cfg.timeout_ms) {
+      *reinterpret_cast<volatile uint32_t *>(ctx->host_abort) = 1;
+      timed_out = true;
+    }
+    if (timed_out && ms > ctx->cfg.timeout_ms + 20000.0)
+      return fail(ctx, SALUS_E_TIMEOUT, "kernel did not exit after abort");
+    std::this_thread::sleep_for(std::chrono::microseconds(20));
+  }
+  Ctrl ctrl;
+  if ((e = cudaMemcpy(&ctrl, m + ctx->off_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost)))
+    return cuda_fail(ctx, e, "readback");
+  float ms = 0;
+  cudaEventElapsedTime(&ms, ctx->ev0, ctx->ev1);
+  salus_run_stats &rs = ctx->last;
+  rs.n_dispatch = ctrl.n_dispatch; rs.n_ticks = ctrl.n_ticks; rs.n_log = std::min<uint64_t>(ctrl.n_log, ctx->log_cap);
+  rs.n_tasks = ctrl.n_tasks; rs.kernel_ns = (uint64_t)((double)ms * 1e6);
+  rs.wall_first_ns = ctrl.wall_first_ns; rs.wall_last_ns = ctrl.wall_last_ns;
+  rs.sched_wait_ns = ctrl.sched_wait_ns; rs.status = ctrl.status; rs.n_workers = ctx->grid - 1;
+  ctx->ran = true;
+  const uint32_t n = (uint32_t)ctx->jobs.size();
+  if (stats) {
+    std::vector<salus_job_stat> dense(n);
+    if ((e = cudaMemcpy(dense.data(), m + ctx->off_stats, sizeof(salus_job_stat) * n, cudaMemcpyDeviceToHost)))
+      return cuda_fail(ctx, e, "readback stats");
+    const uint64_t k = std::min<uint64_t>(max_stats, n);
+    for (uint32_t d = 0; d < n; d++) {
+      const uint32_t s = ctx->dense_to_submit[d];
+      if (s < k) stats[s] = dense[d];
+    }
+    if (n_stats) *n_stats = k;
+  } else if (n_stats) {
+    *n_stats = 0;
+  }
+  if (timed_out) return fail(ctx, SALUS_E_TIMEOUT, "run exceeded timeout_ms");
+  if (ctrl.status) return fail(ctx, ctrl.status, "device error, info " + std::to_string(ctrl.err_info[0]));
+  if (ctrl.log_overflow) return fail(ctx, SALUS_E_CAPACITY, "log capacity exceeded");
+  return SALUS_OK;
+}
+
+int salus_read_run_stats(const salus_ctx *ctx, salus_run_stats *out) {
+  if (!ctx || !out) return SALUS_E_INVAL;
+  if (!ctx->ran) return SALUS_E_STATE;
+  *out = ctx->last;
+  return SALUS_OK;
+}
+
+int salus_read_log(salus_ctx *ctx, void *buf, uint64_t cap_bytes, uint64_t *n_bytes) {
+  if (!ctx || !n_bytes) return SALUS_E_INVAL;
+  if (!ctx->ran || !(ctx->cfg.flags & SALUS_FLAG_LOG)) return fail(ctx, SALUS_E_STATE, "no log");
+  const uint64_t bytes = ctx->last.n_log * sizeof(salus_log_rec);
+  *n_bytes = bytes;
+  if (!buf) return SALUS_OK;
+  if (cap_bytes < bytes) return fail(ctx, SALUS_E_CAPACITY, "log buffer too small");
+  cudaError_t e = cudaMemcpy(buf, ctx->meta + ctx->off_log, bytes, cudaMemcpyDeviceToHost);
+  return e ? cuda_fail(ctx, e, "read log") : SALUS_OK;
+}
+
+int salus_read_wall(salus_ctx *ctx, salus_wall_rec *buf, uint64_t cap_recs, uint64_t *n_recs) {
+  if (!ctx || !n_recs) return SALUS_E_INVAL;
+  if (!ctx->ran || !(ctx->cfg.flags & SALUS_FLAG_LOG)) return fail(ctx, SALUS_E_STATE, "no wall log");
+  const uint64_t n = std::min<uint64_t>(ctx->last.n_dispatch, ctx->log_cap);
+  *n_recs = n;
+  if (!buf) return SALUS_OK;
+  if (cap_recs < n) return fail(ctx, SALUS_E_CAPACITY, "wall buffer too small");
+  cudaError_t e = cudaMemcpy(buf, ctx->meta + ctx->off_wall, n * sizeof(salus_wall_rec), cudaMemcpyDeviceToHost);
+  return e ? cuda_fail(ctx, e, "read wall") : SALUS_OK;
+}
+
+int salus_read_layers(salus_ctx *ctx, uint32_t job_id, uint32_t iter, float *buf, uint64_t cap_floats,
+                      uint64_t *n) {
+  if (!ctx || !n) return SALUS_E_INVAL;
+  if (!ctx->ran) return fail(ctx, SALUS_E_STATE, "not run");
+  auto it = ctx->id_to_dense.find(job_id);
+  if (it == ctx->id_to_dense.end()) return fail(ctx, SALUS_E_INVAL, "unknown job");
+  const DevJob &D = ctx->djobs[it->second];
+  uint64_t off, cnt;
+  if (iter == 0xFFFFFFFFu) {
+    if (!(D.dump & SALUS_DUMP_WEIGHTS)) return fail(ctx, SALUS_E_INVAL, "job did not dump weights");
+    off = D.dump_w_off;
+    cnt = 0;
+    for (uint32_t l = 1; l <= D.n_layers; l++) cnt += (uint64_t)D.dims[l - 1] * D.dims[l];
+  } else {
+    if (!(D.dump & SALUS_DUMP_OUTPUTS) || iter >= D.n_iters) return fail(ctx, SALUS_E_INVAL, "no such output");
+    cnt = (uint64_t)D.batch * D.dims[D.n_layers];
+    off = D.dump_out_off + (uint64_t)iter * cnt;
+  }
+  *n = cnt;
+  if (!buf) return SALUS_OK;
+  if (cap_floats < cnt) return fail(ctx, SALUS_E_CAPACITY, "buffer too small");
+  cudaError_t e = cudaMemcpy(buf, ctx->meta + ctx->off_dump + 4 * off, 4 * cnt, cudaMemcpyDeviceToHost);
+  return e ? cuda_fail(ctx, e, "read layers") : SALUS_OK;
+}
+
+const char *salus_last_error(const salus_ctx *ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int salus_close(salus_ctx *ctx) {
+  if (!ctx) return SALUS_OK;
+  if (ctx->host_abort) cudaFreeHost(ctx->host_abort);
+  if (ctx->ev0) cudaEventDestroy(ctx->ev0);
+  if (ctx->ev1) cudaEventDestroy(ctx->ev1);
+  delete ctx;
+  return SALUS_OK;
+}
+
+}  // extern "C"

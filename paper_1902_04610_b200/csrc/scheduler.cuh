@@ -1,0 +1,570 @@
+// scheduler.cuh — the device-resident Salus scheduler: one warp of CTA 0 of
+// the persistent kernel runs Algorithm 1 (GPU Lane Assignment, PAPER.md
+// P:415-477) under the safety condition, the FIFO/SRTF/PACK/FAIR
+// policies (§4) and the event loop "reacting when jobs arrive or
+// finish, or at iteration boundaries", with the readings of
+// DESIGN.md.
+//
+// Control flow is warp-uniform: every thread of the warp holds the same
+// scalar state; scans over lanes / jobs / the pending queue are spread over
+// the 32 threads (ballot / shuffle reductions); shared-memory writes of
+// scalar state are done by thread 0 followed by __syncwarp().
+//
+// Coupled execution (A30 mode 1): tick t is processed only after every
+// iteration whose logical end is <= t has physically completed, so memory
+// freed at t is physically free when it is re-handed out at t.
+#pragma once
+#include "salus_dev.h"
+#include "ptx.cuh"
+
+namespace salus {
+
+constexpr int64_t IDLE_T = INT64_MAX;
+constexpr uint16_t NONE16 = 0xFFFF;
+constexpr uint32_t KEY_BITS = 11;          // dense job index < 2048 in key low bits
+
+struct SchedShared {
+  // lane table, index order == lane id order
+  uint32_t lane_id[MAX_LANES], lane_L[MAX_LANES], lane_slot[MAX_LANES], lane_back[MAX_LANES];
+  int64_t lane_busy[MAX_LANES];
+  uint64_t lane_seq[MAX_LANES];
+  uint16_t lane_cur[MAX_LANES], lane_last[MAX_LANES];
+  // per job (dense index = (arrival, id) rank)
+  int64_t svc[MAX_JOBS];
+  int64_t c[MAX_JOBS];
+  int64_t nrt[MAX_JOBS];                    // next request tick (INFER)
+  uint32_t done[MAX_JOBS], pending[MAX_JOBS], next_req[MAX_JOBS];
+  uint32_t n[MAX_JOBS], p[MAX_JOBS], e[MAX_JOBS], ap[MAX_JOBS], ae[MAX_JOBS];
+  uint32_t id[MAX_JOBS];
+  uint16_t Q[MAX_JOBS];
+  uint16_t adm[MAX_JOBS];                   // admitted, unfinished
+  uint8_t st[MAX_JOBS], jslot[MAX_JOBS], kind[MAX_JOBS];
+};
+
+__device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    int64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w < v ? w : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint32_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+struct Sched {
+  const Params &P;
+  SchedShared &S;
+  uint32_t tid;
+  // warp-uniform scalar state
+  int64_t t = 0;
+  uint64_t seq = 0, n_log = 0, n_ticks = 0, wait_ns = 0;
+  uint32_t nl = 0, qn = 0, an = 0, next_lane = 0, sumP = 0, sumL = 0, arr_ptr = 0, n_done = 0;
+  uint32_t free_top = 0, max_lanes = 0, err = 0;
+  uint64_t slot_free = ~0ull;
+  int64_t next_arrival = IDLE_T;
+  bool dirty = false;
+
+  __device__ Sched(const Params &p_, SchedShared &s_) : P(p_), S(s_), tid(threadIdx.x & 31) {}
+
+  __device__ void fail(int32_t code, uint32_t info) {
+    if (tid == 0 && err == 0) {
+      atomicCAS(reinterpret_cast<int *>(&P.ctrl->status), 0, code);
+      P.ctrl->err_info[0] = info;
+      atomicExch(&P.ctrl->abort, 1u);
+    }
+    err = 1;
+    __syncwarp();
+  }
+
+  __device__ void emit(uint32_t kind, uint32_t lane, uint32_t job, uint32_t a, uint64_t b) {
+    if ((P.flags & SALUS_FLAG_LOG) && tid == 0 && n_log < P.log_cap) {
+      salus_log_rec r;
+      r.tick = t; r.kind = kind; r.lane = lane; r.job = job; r.a = a; r.b = b;
+      P.log[n_log] = r;
+    }
+    n_log++;
+  }
+
+  // ------------------------------------------------------------ page pool
+  // A18: the arena is a pool of 64 KiB pages; a lane / persistent region is a
+  // page list, so "auto defragmentation" never moves data.
+  __device__ void pop_pages(uint32_t *dst, uint32_t k) {
+    if (k > free_top) { fail(SALUS_E_CAPACITY, 1); return; }
+    for (uint32_t i = tid; i < k; i += 32) dst[i] = P.free_stack[free_top - k + i];
+    free_top -= k;
+    __syncwarp();
+  }
+  __device__ void push_pages(const uint32_t *src, uint32_t k) {
+    for (uint32_t i = tid; i < k; i += 32) P.free_stack[free_top + i] = src[i];
+    free_top += k;
+    __syncwarp();
+  }
+  __device__ uint32_t *lane_table(uint32_t slot) { return P.lpt + (uint64_t)slot * P.lpt_stride; }
+  __device__ uint32_t *job_table(uint32_t j) { return P.ppt + P.jobs[j].pt_off; }
+
+  // ------------------------------------------------------------ FindLane
+  // Algorithm 1 FindLane with A1 (branch 2 keeps the safety
+  // condition), A2 (best match = smallest L >= E, lowest id), A3 (branch 3
+  // only for L_r < E, ascending (L_r, id)), A9 (max_lanes).
+  // Returns 0 = none, 1 = new, 2 = reuse, 3 = resize; *li = lane index.
+  __device__ int find_lane(uint32_t p, uint32_t e, uint32_t *li) const {
+    const int64_t S_ = (int64_t)sumP + (int64_t)sumL, Cp = P.Cp;
+    if (nl < max_lanes && S_ + p + e <= Cp) return 1;
+    if (S_ + p <= Cp) {
+      uint32_t bestL = NONE32, bi = NONE32;
+      for (uint32_t i = 0; i < nl; i++) {
+        uint32_t L = S.lane_L[i];
+        if (L >= e && L < bestL) { bestL = L; bi = i; }
+      }
+      if (bi != NONE32) { *li = bi; return 2; }
+    }
+    const int64_t thr = S_ + p + e - Cp;   // S - L + p + e <= C  <=>  L >= thr
+    uint32_t bestL = NONE32, bi = NONE32;
+    for (uint32_t i = 0; i < nl; i++) {
+      uint32_t L = S.lane_L[i];
+      if (L < e && (int64_t)L >= thr && L < bestL) { bestL = L; bi = i; }
+    }
+    if (bi != NONE32) { *li = bi; return 3; }
+    return 0;
+  }
+
+  // ------------------------------------------------------------ helpers
+  __device__ bool runnable(uint32_t j) const { return S.kind[j] == SALUS_TRAIN || S.pending[j] > 0; }
+
+  // min svc over admitted jobs in `slot` (excluding `skip`, optionally only
+  // runnable ones); IDLE_T if none
+  __device__ int64_t min_svc_in(uint32_t slot, uint32_t skip, bool only_runnable) const {
+    int64_t m = IDLE_T;
+    for (uint32_t a = tid; a < an; a += 32) {
+      uint32_t j = S.adm[a];
+      if (S.jslot[j] == slot && j != skip && (!only_runnable || runnable(j))) m = min(m, S.svc[j]);
+    }
+    return warp_min_i64(m);
+  }
+
+  __device__ void enqueue(uint32_t slot, uint32_t stage, uint32_t ntiles) {
+    unsigned long long base = 0;
+    if (tid == 0) base = atomicAdd(&P.ctrl->q_head, (unsigned long long)ntiles);
+    base = __shfl_sync(0xffffffffu, base, 0);
+    for (uint32_t k = tid; k < ntiles; k += 32) {
+      unsigned long long pos = base + k;
+      ptx::st_release_u64(&P.ring[pos & P.ring_mask], ((pos + 1) << 32) | task_pack(slot, stage, k));
+    }
+    __syncwarp();
+  }
+
+  __device__ bool host_abort() const { return P.host_abort && ptx::ld_volatile_u32(P.host_abort) != 0; }
+
+  // Spin until the iteration `sq` in `slot` is physically complete (A30 mode 1)
+  __device__ void wait_slot(uint32_t slot, uint64_t sq) {
+    uint64_t t0 = ptx::globaltimer();
+    uint32_t ok = 0, spins = 0;
+    while (true) {
+      if (tid == 0) ok = ptx::ld_acquire_u64(&P.slots[slot].done_seq) == sq + 1;
+      ok = __shfl_sync(0xffffffffu, ok, 0);
+      if (ok) break;
+      if ((++spins & 1023) == 0) {
+        uint32_t bad = 0;
+        if (tid == 0) bad = host_abort() || (ptx::globaltimer() - t0 > P.timeout_ns) ||
+                            *(volatile uint32_t *)&P.ctrl->abort;
+        bad = __shfl_sync(0xffffffffu, bad, 0);
+        if (bad) { fail(host_abort() ? SALUS_E_TIMEOUT : SALUS_E_STUCK, 2); return; }
+      }
+    }
+    wait_ns += ptx::globaltimer() - t0;
+  }
+
+  // ------------------------------------------------------------ phases
+  __device__ void init() {
+    const uint32_t N = P.n_jobs;
+    for (uint32_t j = tid; j < N; j += 32) {
+      const DevJob &J = P.jobs[j];
+      S.svc[j] = 0; S.c[j] = J.iter_ticks; S.done[j] = 0; S.pending[j] = 0; S.next_req[j] = 0;
+      S.n[j] = J.n_iters; S.p[j] = J.p_pages; S.e[j] = J.e_pages; S.ap[j] = J.ap_pages; S.ae[j] = J.ae_pages;
+      S.id[j] = J.job_id; S.st[j] = ST_NOT_ARRIVED; S.jslot[j] = 0xFF; S.kind[j] = (uint8_t)J.kind;
+      S.nrt[j] = J.kind == SALUS_INFER ? P.req_ticks[J.req_off] : IDLE_T;
+      salus_job_stat &st = P.stats[j];
+      st.job_id = J.job_id; st.first_lane = NONE32; st.admit_tick = -1; st.first_start_tick = -1;
+      st.completion_tick = -1; st.completion_seq = ~0ull; st.wall_start_ns = 0; st.wall_end_ns = 0;
+    }
+    for (uint32_t i = tid; i < P.Cp; i += 32) P.free_stack[i] = P.Cp - 1 - i;
+    free_top = P.Cp;
+    max_lanes = P.max_lanes;
+    next_arrival = N ? P.jobs[0].arrival : IDLE_T;
+    __syncwarp();
+  }
+
+  __device__ int64_t next_event() {
+    int64_t m = IDLE_T;
+    for (uint32_t i = tid; i < nl; i += 32) m = min(m, S.lane_busy[i]);
+    for (uint32_t k = tid; k < P.n_infer; k += 32) {
+      uint32_t j = P.infer_list[k];
+      if (S.st[j] == ST_QUEUED || S.st[j] == ST_ADMITTED) m = min(m, S.nrt[j]);
+    }
+    m = warp_min_i64(m);
+    return min(m, next_arrival);
+  }
+
+  __device__ void remove_lane(uint32_t i) {     // keep id order
+    for (uint32_t k = i; k + 1 < nl; k++) {
+      if (tid == 0) {
+        S.lane_id[k] = S.lane_id[k + 1]; S.lane_L[k] = S.lane_L[k + 1]; S.lane_slot[k] = S.lane_slot[k + 1];
+        S.lane_back[k] = S.lane_back[k + 1]; S.lane_busy[k] = S.lane_busy[k + 1];
+        S.lane_seq[k] = S.lane_seq[k + 1]; S.lane_cur[k] = S.lane_cur[k + 1]; S.lane_last[k] = S.lane_last[k + 1];
+      }
+    }
+    nl--;
+    __syncwarp();
+  }
+
+  __device__ void remove_adm(uint32_t j) {
+    uint32_t pos = NONE32;
+    for (uint32_t a = tid; a < an; a += 32)
+      if (S.adm[a] == j) pos = a;
+    pos = warp_max_u32(pos == NONE32 ? 0 : pos + 1) - 1;
+    if (tid == 0) S.adm[pos] = S.adm[an - 1];
+    an--;
+    __syncwarp();
+  }
+
+  // P1: iteration completions and JobFinish (A4)
+  __device__ void phase_completions() {
+    for (uint32_t i = 0; i < nl;) {
+      if (S.lane_busy[i] != t) { i++; continue; }
+      const uint32_t slot = S.lane_slot[i];
+      if (!(P.flags & SALUS_FLAG_NULL_WORK)) {
+        wait_slot(slot, S.lane_seq[i]);
+        if (err) return;
+        if ((P.flags & SALUS_FLAG_LOG) && tid == 0 && S.lane_seq[i] < P.log_cap) {
+          salus_wall_rec w;
+          w.seq = S.lane_seq[i]; w.lane = S.lane_id[i]; w.job = S.id[S.lane_cur[i]];
+          w.start_ns = P.slots[slot].start_ns; w.end_ns = P.slots[slot].end_ns;
+          P.wall[S.lane_seq[i]] = w;
+        }
+      }
+      const uint32_t j = S.lane_cur[i];
+      if (tid == 0) {
+        S.done[j] += 1; S.svc[j] += S.c[j]; S.lane_busy[i] = IDLE_T;
+        if (!(P.flags & SALUS_FLAG_NULL_WORK)) {
+          salus_job_stat &st = P.stats[j];
+          if (st.wall_start_ns == 0) st.wall_start_ns = P.slots[slot].start_ns;
+          st.wall_end_ns = P.slots[slot].end_ns;
+        }
+      }
+      __syncwarp();
+      if (S.done[j] == S.n[j]) {
+        if (tid == 0) {
+          S.st[j] = ST_DONE;
+          P.stats[j].completion_tick = t;
+        }
+        n_done++; dirty = true; sumP -= S.p[j];
+        __syncwarp();
+        remove_adm(j);
+        emit(SALUS_REC_JOB_FINISH, S.lane_id[i], S.id[j], S.n[j], P.stats[j].completion_seq);
+        push_pages(job_table(j), S.ap[j]);
+        // residents left in this lane: count, max e, max actual e
+        uint32_t cnt = 0, maxe = 0, maxae = 0;
+        for (uint32_t a = tid; a < an; a += 32) {
+          uint32_t r = S.adm[a];
+          if (S.jslot[r] == slot) { cnt++; maxe = max(maxe, S.e[r]); maxae = max(maxae, S.ae[r]); }
+        }
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        maxe = warp_max_u32(maxe);
+        maxae = warp_max_u32(maxae);
+        if (cnt == 0) {                           // ref(lane) == 0: delete lane
+          emit(SALUS_REC_LANE_CLOSE, S.lane_id[i], S.id[j], 0, 0);
+          push_pages(lane_table(slot), S.lane_back[i]);
+          sumL -= S.lane_L[i];
+          slot_free |= (1ull << slot);
+          remove_lane(i);
+          continue;
+        }
+        if (maxe < S.lane_L[i]) {                 // A4: L_j = max E_i of residents
+          emit(SALUS_REC_LANE_SHRINK, S.lane_id[i], S.id[j], maxe, S.lane_L[i]);
+          sumL -= S.lane_L[i] - maxe;
+          if (tid == 0) S.lane_L[i] = maxe;
+        }
+        if (maxae < S.lane_back[i]) {
+          push_pages(lane_table(slot) + maxae, S.lane_back[i] - maxae);
+          if (tid == 0) S.lane_back[i] = maxae;
+        }
+        __syncwarp();
+      }
+      i++;
+    }
+  }
+
+  __device__ void q_insert(uint32_t j) {
+    uint32_t pos = qn;
+    if (P.policy == SALUS_SRTF) {            // A10: key (n*c, arrival, id)
+      const int64_t kj = (int64_t)S.n[j] * S.c[j];
+      uint32_t cnt = 0;
+      for (uint32_t q = tid; q < qn; q += 32) {
+        uint32_t r = S.Q[q];
+        if ((int64_t)S.n[r] * S.c[r] <= kj) cnt++;   // r arrived earlier: rank(r) < j
+      }
+      pos = __reduce_add_sync(0xffffffffu, cnt);
+      // shift [pos, qn) right by one, high chunks first
+      for (int64_t b = (int64_t)((qn - 1) & ~31u); qn > 0 && b >= (int64_t)(pos & ~31u); b -= 32) {
+        uint32_t k = (uint32_t)b + tid;
+        uint16_t v = (k < qn && k >= pos) ? S.Q[k] : 0;
+        __syncwarp();
+        if (k < qn && k >= pos) S.Q[k + 1] = v;
+        __syncwarp();
+      }
+    }
+    if (tid == 0) S.Q[pos] = (uint16_t)j;
+    qn++;
+    __syncwarp();
+  }
+
+  __device__ void q_remove(uint32_t pos) {
+    for (uint32_t b = pos & ~31u; b < qn; b += 32) {
+      uint32_t k = b + tid;
+      uint16_t v = (k >= pos && k + 1 < qn) ? S.Q[k + 1] : 0;
+      __syncwarp();
+      if (k >= pos && k + 1 < qn) S.Q[k] = v;
+      __syncwarp();
+    }
+    qn--;
+    __syncwarp();
+  }
+
+  // P2: JobArrive and inference request arrivals (A27, A28)
+  __device__ void phase_arrivals() {
+    while (arr_ptr < P.n_jobs && next_arrival == t) {
+      const uint32_t j = arr_ptr;
+      if (tid == 0) S.st[j] = ST_QUEUED;
+      __syncwarp();
+      q_insert(j);
+      emit(SALUS_REC_JOB_QUEUED, NONE32, S.id[j], 0, 0);
+      dirty = true;
+      arr_ptr++;
+      next_arrival = arr_ptr < P.n_jobs ? P.jobs[arr_ptr].arrival : IDLE_T;
+    }
+    for (uint32_t k0 = 0; k0 < P.n_infer; k0 += 32) {
+      const uint32_t k = k0 + tid;
+      uint32_t j = 0, cnt = 0;
+      if (k < P.n_infer) {
+        j = P.infer_list[k];
+        if ((S.st[j] == ST_QUEUED || S.st[j] == ST_ADMITTED) && S.nrt[j] == t) {
+          const uint32_t off = P.jobs[j].req_off;
+          uint32_t nr = S.next_req[j];
+          while (nr < S.n[j] && P.req_ticks[off + nr] == t) { nr++; cnt++; }
+          S.next_req[j] = nr;
+          S.nrt[j] = nr < S.n[j] ? P.req_ticks[off + nr] : IDLE_T;
+        }
+      }
+      uint32_t mask = __ballot_sync(0xffffffffu, cnt > 0);
+      __syncwarp();
+      while (mask) {                          // sequential in (arrival, id) order
+        const int b = __ffs(mask) - 1;
+        mask &= mask - 1;
+        const uint32_t jj = __shfl_sync(0xffffffffu, j, b);
+        const uint32_t cc = __shfl_sync(0xffffffffu, cnt, b);
+        const bool was_idle = S.pending[jj] == 0;
+        __syncwarp();
+        if (tid == 0) S.pending[jj] += cc;
+        __syncwarp();
+        if (P.policy == SALUS_FAIR && S.st[jj] == ST_ADMITTED && was_idle) {
+          // A28: an idle inference job re-enters at the min service of its
+          // lane's runnable co-residents
+          const uint32_t slot = S.jslot[jj];
+          bool running = false;
+          for (uint32_t i = 0; i < nl; i++)
+            if (S.lane_slot[i] == slot) running = S.lane_busy[i] != IDLE_T && S.lane_cur[i] == jj;
+          if (!running) {
+            const int64_t co = min_svc_in(slot, jj, true);
+            if (co != IDLE_T && tid == 0 && co > S.svc[jj]) S.svc[jj] = co;
+            __syncwarp();
+          }
+        }
+      }
+    }
+  }
+
+  __device__ void admit(uint32_t j, int branch, uint32_t li) {
+    uint32_t slot;
+    if (branch == 1) {                                   // new lane
+      slot = __ffsll((long long)slot_free) - 1;
+      slot_free &= ~(1ull << slot);
+      li = nl;
+      if (tid == 0) {
+        S.lane_id[li] = next_lane; S.lane_L[li] = S.e[j]; S.lane_slot[li] = slot; S.lane_back[li] = 0;
+        S.lane_busy[li] = IDLE_T; S.lane_cur[li] = NONE16; S.lane_last[li] = NONE16; S.lane_seq[li] = 0;
+      }
+      next_lane++; nl++; sumL += S.e[j];
+      __syncwarp();
+      emit(SALUS_REC_LANE_OPEN, S.lane_id[li], S.id[j], S.e[j], 0);
+    } else if (branch == 2) {                            // existing lane
+      slot = S.lane_slot[li];
+      emit(SALUS_REC_LANE_REUSE, S.lane_id[li], S.id[j], S.lane_L[li], 0);
+    } else {                                             // replace
+      slot = S.lane_slot[li];
+      const uint32_t old = S.lane_L[li];
+      sumL += S.e[j] - old;
+      __syncwarp();
+      if (tid == 0) S.lane_L[li] = S.e[j];
+      __syncwarp();
+      emit(SALUS_REC_LANE_RESIZE, S.lane_id[li], S.id[j], S.e[j], old);
+    }
+    // physical backing: the lane grows to the max actual E of its residents,
+    // the job's persistent tensors get their own pages (Observation 2)
+    if (S.ae[j] > S.lane_back[li]) {
+      pop_pages(lane_table(slot) + S.lane_back[li], S.ae[j] - S.lane_back[li]);
+      if (tid == 0) S.lane_back[li] = S.ae[j];
+    }
+    pop_pages(job_table(j), S.ap[j]);
+    if (P.policy == SALUS_FAIR) {                        // A12: virtual-time start
+      const int64_t m = min_svc_in(slot, NONE32, false);
+      if (tid == 0) S.svc[j] = (m == IDLE_T) ? 0 : m;
+    }
+    if (tid == 0) {
+      S.adm[an] = (uint16_t)j; S.jslot[j] = (uint8_t)slot; S.st[j] = ST_ADMITTED;
+      P.stats[j].admit_tick = t; P.stats[j].first_lane = S.lane_id[li];
+    }
+    an++; sumP += S.p[j];
+    __syncwarp();
+    emit(SALUS_REC_JOB_ADMIT, S.lane_id[li], S.id[j], S.p[j], S.e[j]);
+  }
+
+  // P3: ProcessRequests — one in-order pass over Q (A5, A7, A8, A14)
+  __device__ void phase_admission() {
+    uint32_t pos = 0;
+    while (pos < qn && !err) {
+      uint32_t first = NONE32;
+      if (P.policy == SALUS_FIFO) {                      // A14: exclusive, strict HOL
+        if (an > 0) break;
+        uint32_t li;
+        if (find_lane(S.p[S.Q[0]], S.e[S.Q[0]], &li) == 0) break;
+        first = 0;
+      } else {
+        for (uint32_t b = pos; b < qn && first == NONE32; b += 32) {
+          const uint32_t k = b + tid;
+          uint32_t li;
+          const bool ok = k < qn && find_lane(S.p[S.Q[k]], S.e[S.Q[k]], &li) != 0;
+          const uint32_t m = __ballot_sync(0xffffffffu, ok);
+          if (m) first = b + __ffs(m) - 1;
+        }
+        if (first == NONE32) break;
+      }
+      const uint32_t j = S.Q[first];
+      uint32_t li = 0;
+      const int br = find_lane(S.p[j], S.e[j], &li);
+      __syncwarp();
+      q_remove(first);
+      admit(j, br, li);
+      pos = first;
+    }
+  }
+
+  __device__ void dispatch_physical(uint32_t slot, uint32_t j) {
+    Slot &sl = P.slots[slot];
+    if (tid == 0) {
+      sl.job = j; sl.iter = S.done[j]; sl.seq = seq; sl.start_ns = ~0ull; sl.end_ns = 0;
+    }
+    for (uint32_t k = tid; k < MAX_STAGES + 2; k += 32) sl.stage_done[k] = 0;
+    __threadfence();
+    __syncwarp();
+    const uint32_t first = S.done[j] == 0 ? 0u : 1u;    // INIT only before the first iteration
+    enqueue(slot, first, P.jobs[j].stage_tiles[first]);
+  }
+
+  // P4: every idle lane dispatches its next iteration
+  __device__ void phase_dispatch() {
+    for (uint32_t i = 0; i < nl; i++) {
+      if (S.lane_busy[i] != IDLE_T) continue;
+      const uint32_t slot = S.lane_slot[i];
+      uint64_t best = ~0ull;
+      for (uint32_t a = tid; a < an; a += 32) {
+        const uint32_t j = S.adm[a];
+        if (S.jslot[j] != slot || !runnable(j)) continue;
+        uint64_t key;
+        if (P.policy == SALUS_SRTF)        // A11: remaining = (n - done) * c
+          key = ((uint64_t)((int64_t)(S.n[j] - S.done[j]) * S.c[j]) << KEY_BITS) | j;
+        else if (P.policy == SALUS_FAIR)   // least service
+          key = ((uint64_t)S.svc[j] << KEY_BITS) | j;
+        else                               // FIFO / PACK (A13): earliest arrival
+          key = j;
+        best = key < best ? key : best;
+      }
+      best = warp_min_u64(best);
+      if (best == ~0ull) continue;
+      const uint32_t j = (uint32_t)(best & ((1u << KEY_BITS) - 1));
+      const uint16_t last = S.lane_last[i];
+      const int64_t pen = (last != NONE16 && last != j) ? P.switch_ticks : 0;   // A16
+      if (tid == 0) {
+        S.lane_busy[i] = t + pen + S.c[j];
+        S.lane_cur[i] = (uint16_t)j; S.lane_last[i] = (uint16_t)j; S.lane_seq[i] = seq;
+        if (S.kind[j] == SALUS_INFER) S.pending[j] -= 1;
+        salus_job_stat &st = P.stats[j];
+        if (st.first_start_tick < 0) st.first_start_tick = t;
+        st.completion_seq = seq;
+      }
+      __syncwarp();
+      emit(SALUS_REC_DISPATCH, S.lane_id[i], S.id[j], S.done[j], seq);
+      if (!(P.flags & SALUS_FLAG_NULL_WORK)) dispatch_physical(slot, j);
+      seq++;
+    }
+  }
+
+  __device__ void check_safety() {
+    if ((uint64_t)sumP + sumL > P.Cp) fail(SALUS_E_STATE, 3);   // I1
+  }
+
+  __device__ void run() {
+    init();
+    const uint64_t wall0 = ptx::globaltimer();
+    while (n_done < P.n_jobs && !err) {
+      const int64_t tn = next_event();
+      if (tn == IDLE_T) { fail(SALUS_E_STUCK, 4); break; }
+      t = tn;
+      n_ticks++;
+      dirty = false;
+      phase_completions();
+      if (err) break;
+      phase_arrivals();
+      if (qn > 0 && dirty) phase_admission();
+      if (P.flags & SALUS_FLAG_CHECK) check_safety();
+      phase_dispatch();
+      if ((n_ticks & 255) == 0) {
+        uint32_t bad = 0;
+        if (tid == 0) bad = host_abort();
+        if (__shfl_sync(0xffffffffu, bad, 0)) fail(SALUS_E_TIMEOUT, 5);
+      }
+    }
+    // release the workers
+    {
+      unsigned long long base = 0;
+      if (tid == 0) base = atomicAdd(&P.ctrl->q_head, (unsigned long long)P.n_workers);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      for (uint32_t k = tid; k < P.n_workers; k += 32) {
+        unsigned long long pos = base + k;
+        ptx::st_release_u64(&P.ring[pos & P.ring_mask], ((pos + 1) << 32) | TASK_EXIT);
+      }
+    }
+    if (tid == 0) {
+      P.ctrl->n_dispatch = seq; P.ctrl->n_ticks = n_ticks; P.ctrl->n_log = n_log;
+      P.ctrl->sched_wait_ns = wait_ns; P.ctrl->wall_first_ns = wall0;
+      P.ctrl->wall_last_ns = ptx::globaltimer();
+      P.ctrl->log_overflow = ((P.flags & SALUS_FLAG_LOG) && n_log > P.log_cap) ? 1u : 0u;
+    }
+  }
+};
+
+}  // namespace salus

@@ -1,0 +1,235 @@
+"""Thin ctypes binding of libsalus.so (include/salus.h).
+
+Argument marshalling only: every step of the hot path (admission, lane
+assignment, page allocation, dispatch, iteration execution) runs inside the
+persistent CUDA kernel.  PyTorch is used for device memory (arena, meta) and
+the stream.  If the library is missing this module raises — there is no CPU
+fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Dict, Iterable, List, Optional
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libsalus.so")
+
+FIFO, SRTF, PACK, FAIR = 0, 1, 2, 3
+TRAIN, INFER = 0, 1
+FLAG_LOG, FLAG_NULL_WORK, FLAG_CHECK = 1, 2, 4
+DUMP_OUTPUTS, DUMP_WEIGHTS = 1, 2
+WEIGHTS = 0xFFFFFFFF
+
+ERRORS = {-1: "E_INVAL", -2: "E_DUPLICATE", -3: "E_UNSCHEDULABLE", -4: "E_STATE",
+          -5: "E_CAPACITY", -6: "E_CUDA", -7: "E_STUCK", -8: "E_TIMEOUT"}
+
+
+class SalusError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"{ERRORS.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Config(C.Structure):
+    _fields_ = [("device", C.c_int32), ("policy", C.c_uint32), ("arena", C.c_void_p),
+                ("arena_bytes", C.c_uint64), ("stream", C.c_void_p), ("capacity_bytes", C.c_uint64),
+                ("page_bytes", C.c_uint32), ("max_lanes", C.c_uint32), ("max_jobs", C.c_uint32),
+                ("flags", C.c_uint32), ("switch_ticks", C.c_uint64), ("log_capacity", C.c_uint64),
+                ("dump_bytes", C.c_uint64), ("n_workers", C.c_uint32), ("timeout_ms", C.c_uint32)]
+
+
+class JobDesc(C.Structure):
+    _fields_ = [("job_id", C.c_uint32), ("kind", C.c_uint32), ("arrival_tick", C.c_int64),
+                ("persistent_bytes", C.c_uint64), ("ephemeral_bytes", C.c_uint64),
+                ("n_iters", C.c_uint32), ("n_layers", C.c_uint32), ("iter_ticks", C.c_uint64),
+                ("dims", C.c_uint32 * 9), ("batch", C.c_uint32), ("lr", C.c_float),
+                ("dump", C.c_uint32), ("seed", C.c_uint64), ("request_ticks", C.POINTER(C.c_int64))]
+
+
+class JobStat(C.Structure):
+    _fields_ = [("job_id", C.c_uint32), ("first_lane", C.c_uint32), ("admit_tick", C.c_int64),
+                ("first_start_tick", C.c_int64), ("completion_tick", C.c_int64),
+                ("completion_seq", C.c_uint64), ("wall_start_ns", C.c_uint64), ("wall_end_ns", C.c_uint64)]
+
+
+class RunStats(C.Structure):
+    _fields_ = [("n_dispatch", C.c_uint64), ("n_ticks", C.c_uint64), ("n_log", C.c_uint64),
+                ("n_tasks", C.c_uint64), ("kernel_ns", C.c_uint64), ("wall_first_ns", C.c_uint64),
+                ("wall_last_ns", C.c_uint64), ("sched_wait_ns", C.c_uint64), ("status", C.c_int32),
+                ("n_workers", C.c_uint32)]
+
+
+WALL_DTYPE = np.dtype([("seq", "<u8"), ("lane", "<u4"), ("job", "<u4"), ("start_ns", "<u8"),
+                       ("end_ns", "<u8")])
+LOG_DTYPE = np.dtype([("tick", "<i8"), ("kind", "<u4"), ("lane", "<u4"), ("job", "<u4"),
+                      ("a", "<u4"), ("b", "<u8")])
+
+EXPORTS = ["salus_open", "salus_job_footprint", "salus_submit_job", "salus_meta_bytes",
+           "salus_prepare", "salus_run", "salus_read_run_stats", "salus_read_log",
+           "salus_read_wall", "salus_read_layers", "salus_last_error", "salus_close"]
+
+_lib = None
+
+
+def lib():
+    """Load libsalus.so (fails loudly if it was not built)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} missing: run `python -m paper_1902_04610_b200.build` "
+                               "(there is no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        P = C.c_void_p
+        L.salus_open.argtypes = [C.POINTER(Config), C.POINTER(P)]
+        L.salus_job_footprint.argtypes = [C.POINTER(JobDesc), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]
+        L.salus_submit_job.argtypes = [P, C.POINTER(JobDesc)]
+        L.salus_meta_bytes.argtypes = [P, C.POINTER(C.c_uint64)]
+        L.salus_prepare.argtypes = [P, P, C.c_uint64]
+        L.salus_run.argtypes = [P, C.POINTER(JobStat), C.c_uint64, C.POINTER(C.c_uint64)]
+        L.salus_read_run_stats.argtypes = [P, C.POINTER(RunStats)]
+        L.salus_read_log.argtypes = [P, P, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.salus_read_wall.argtypes = [P, P, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.salus_read_layers.argtypes = [P, C.c_uint32, C.c_uint32, C.POINTER(C.c_float), C.c_uint64,
+                                        C.POINTER(C.c_uint64)]
+        L.salus_last_error.argtypes = [P]
+        L.salus_last_error.restype = C.c_char_p
+        L.salus_close.argtypes = [P]
+        for name in EXPORTS:
+            if name != "salus_last_error":
+                getattr(L, name).restype = C.c_int
+        _lib = L
+    return _lib
+
+
+def job_desc(job, dump: int = 0):
+    """Marshal a workloads.Job-like object into a salus_job; returns (desc, keepalive)."""
+    d = JobDesc()
+    d.job_id = job.job_id
+    d.kind = job.kind
+    d.arrival_tick = job.arrival_tick
+    d.persistent_bytes = job.persistent_bytes
+    d.ephemeral_bytes = job.ephemeral_bytes
+    d.n_iters = job.n_iters
+    d.n_layers = len(job.dims) - 1
+    d.iter_ticks = job.iter_ticks
+    for i, v in enumerate(job.dims):
+        d.dims[i] = v
+    d.batch = job.batch
+    d.lr = job.lr
+    d.dump = dump
+    d.seed = job.seed & (2**64 - 1)
+    keep = None
+    if job.kind == INFER:
+        keep = (C.c_int64 * len(job.request_ticks))(*job.request_ticks)
+        d.request_ticks = C.cast(keep, C.POINTER(C.c_int64))
+    return d, keep
+
+
+def footprint(job):
+    d, _ = job_desc(job)
+    p, e = C.c_uint64(), C.c_uint64()
+    rc = lib().salus_job_footprint(C.byref(d), C.byref(p), C.byref(e))
+    if rc:
+        raise SalusError(rc, "footprint")
+    return p.value, e.value
+
+
+class Context:
+    """One Salus instance on one GPU: open + submit + prepare (salus.h)."""
+
+    def __init__(self, jobs: Iterable, capacity_bytes: int, policy: int, *, device: int = 0,
+                 max_lanes: int = 0, switch_ticks: int = 0, log: bool = True, null_work: bool = False,
+                 check: bool = False, dump: Optional[Dict[int, int]] = None, n_workers: int = 0,
+                 timeout_ms: int = 0, page_bytes: int = 65536):
+        import torch
+        self._torch = torch
+        self.L = lib()
+        self.jobs = list(jobs)
+        self.device = device
+        G = page_bytes
+        Cp = capacity_bytes // G
+        self.arena = torch.empty(Cp * G, dtype=torch.uint8, device=f"cuda:{device}")
+        self.stream = torch.cuda.current_stream(device)
+        cfg = Config()
+        cfg.device = device
+        cfg.policy = policy
+        cfg.arena = self.arena.data_ptr()
+        cfg.arena_bytes = Cp * G
+        cfg.stream = self.stream.cuda_stream
+        cfg.capacity_bytes = capacity_bytes
+        cfg.page_bytes = page_bytes
+        cfg.max_lanes = max_lanes
+        cfg.max_jobs = max(1, len(self.jobs))
+        cfg.flags = (FLAG_LOG if log else 0) | (FLAG_NULL_WORK if null_work else 0) | (FLAG_CHECK if check else 0)
+        cfg.switch_ticks = switch_ticks
+        cfg.n_workers = n_workers
+        cfg.timeout_ms = timeout_ms
+        self.flags = cfg.flags
+        self.ctx = C.c_void_p()
+        self._check(self.L.salus_open(C.byref(cfg), C.byref(self.ctx)), "open")
+        dump = dump or {}
+        for j in self.jobs:
+            d, keep = job_desc(j, dump.get(j.job_id, 0))
+            self._check(self.L.salus_submit_job(self.ctx, C.byref(d)), f"submit {j.job_id}")
+        mb = C.c_uint64()
+        self._check(self.L.salus_meta_bytes(self.ctx, C.byref(mb)), "meta_bytes")
+        self.meta = torch.empty(max(256, mb.value), dtype=torch.uint8, device=f"cuda:{device}")
+        self._check(self.L.salus_prepare(self.ctx, C.c_void_p(self.meta.data_ptr()), mb.value), "prepare")
+
+    def _check(self, rc, what):
+        if rc != 0:
+            msg = self.L.salus_last_error(self.ctx) if getattr(self, "ctx", None) else b""
+            raise SalusError(rc, f"{what}: {(msg or b'').decode()}")
+
+    def run(self) -> Dict[int, dict]:
+        """One salus_run; returns {job_id: stat dict}."""
+        n = len(self.jobs)
+        arr = (JobStat * n)()
+        cnt = C.c_uint64()
+        self._check(self.L.salus_run(self.ctx, arr, n, C.byref(cnt)), "run")
+        out = {}
+        for s in arr[:cnt.value]:
+            out[s.job_id] = {k: getattr(s, k) for k, _ in JobStat._fields_}
+        return out
+
+    def run_stats(self) -> dict:
+        rs = RunStats()
+        self._check(self.L.salus_read_run_stats(self.ctx, C.byref(rs)), "run_stats")
+        return {k: getattr(rs, k) for k, _ in RunStats._fields_}
+
+    def log_bytes(self) -> bytes:
+        n = C.c_uint64()
+        self._check(self.L.salus_read_log(self.ctx, None, 0, C.byref(n)), "log size")
+        buf = C.create_string_buffer(max(1, n.value))
+        self._check(self.L.salus_read_log(self.ctx, buf, n.value, C.byref(n)), "log")
+        return buf.raw[:n.value]
+
+    def wall(self) -> np.ndarray:
+        n = C.c_uint64()
+        self._check(self.L.salus_read_wall(self.ctx, None, 0, C.byref(n)), "wall size")
+        out = np.zeros(n.value, dtype=WALL_DTYPE)
+        self._check(self.L.salus_read_wall(self.ctx, C.c_void_p(out.ctypes.data), n.value, C.byref(n)), "wall")
+        return out
+
+    def layers(self, job_id: int, iteration: int) -> np.ndarray:
+        n = C.c_uint64()
+        self._check(self.L.salus_read_layers(self.ctx, job_id, iteration, None, 0, C.byref(n)), "layers size")
+        out = np.zeros(n.value, dtype=np.float32)
+        self._check(self.L.salus_read_layers(self.ctx, job_id, iteration,
+                                             out.ctypes.data_as(C.POINTER(C.c_float)), n.value, C.byref(n)),
+                    "layers")
+        return out
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self.L.salus_close(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

@@ -1,0 +1,90 @@
+"""GPU numerics parity: the tcgen05 GEMM tiles + fused epilogues of each
+dispatched iteration against the oracle's fp64 layer math.  Tolerance: the
+north star's 2e-2 max relative error for bf16 operands with fp32
+accumulation, read per tensor as max|g - r| / max|r| (A24).  Training jobs
+also compare the final-minus-initial weights (so small updates are not
+hidden under the large initial weights)."""
+import numpy as np
+import pytest
+
+from oracle import layers as OL
+from oracle import scheduler as OS
+from workloads import TRAIN, INFER, c1_trace, make_job, tiny_math_trace
+
+from gpu_helpers import assert_schedule_parity, normwise_rel, run_gpu
+
+pytestmark = pytest.mark.gpu
+TOL = 2e-2
+
+
+def _check_math(ctx, jobs, iters=None):
+    """Outputs against the fp64 definition (north-star tolerance); outputs and
+    weight updates against the oracle with the kernel's bf16 storage points
+    (reading A31: the ReLU mask is decided in the kernel's precision)."""
+    from paper_1902_04610_b200 import salus as S
+    worst = 0.0
+    for j in jobs:
+        outs64, _ = OL.run_job(j)
+        outs, W = OL.run_job(j, store=OL.bf16)
+        L = len(j.dims) - 1
+        for k in range(j.n_iters) if iters is None else iters:
+            g = ctx.layers(j.job_id, k).reshape(j.batch, j.dims[-1])
+            rel = max(normwise_rel(g, outs64[k]), normwise_rel(g, outs[k]))
+            worst = max(worst, rel)
+            assert rel <= TOL, (j.job_id, k, rel)
+        if j.kind == TRAIN:
+            W0 = OL.init_weights(j)
+            flat = ctx.layers(j.job_id, S.WEIGHTS)
+            off = 0
+            for l in range(L):
+                n = j.dims[l] * j.dims[l + 1]
+                Wg = flat[off:off + n].reshape(j.dims[l], j.dims[l + 1])
+                off += n
+                assert normwise_rel(Wg, W[l]) <= TOL, (j.job_id, l)
+                rel = normwise_rel(Wg - W0[l], W[l] - W0[l])
+                worst = max(worst, rel)
+                assert rel <= TOL, (j.job_id, "dW", l, rel)
+    return worst
+
+
+@pytest.mark.parametrize("kind", [TRAIN, INFER])
+@pytest.mark.parametrize("dims,batch", [((128, 256, 128), 128), ((256, 256, 256), 200),
+                                        ((384, 128, 256, 128), 100), ((200, 256, 72), 300)])
+def test_tiny_jobs(kind, dims, batch):
+    from paper_1902_04610_b200 import salus as S
+    jobs, cap = tiny_math_trace(kind, n_jobs=2, dims=dims, batch=batch, n_iters=3, lr=5e-2)
+    dump = {j.job_id: S.DUMP_OUTPUTS | (S.DUMP_WEIGHTS if kind == TRAIN else 0) for j in jobs}
+    ctx, ref, stats = assert_schedule_parity(jobs, cap, OS.PACK, null_work=False, dump=dump)
+    try:
+        _check_math(ctx, jobs)
+    finally:
+        ctx.close()
+
+
+@pytest.mark.parametrize("policy", [OS.FIFO, OS.SRTF])
+def test_c1_real_work(policy):
+    """BASELINE configs[0] end to end: schedule parity with real iterations
+    executing, plus layer parity of every iteration of both jobs."""
+    from paper_1902_04610_b200 import salus as S
+    jobs, cap = c1_trace()
+    dump = {j.job_id: S.DUMP_OUTPUTS | S.DUMP_WEIGHTS for j in jobs}
+    ctx, ref, stats = assert_schedule_parity(jobs, cap, policy, null_work=False, dump=dump)
+    try:
+        _check_math(ctx, jobs)
+        wall = ctx.wall()
+        assert len(wall) == 20 and np.all(wall["end_ns"] > wall["start_ns"])
+    finally:
+        ctx.close()
+
+
+def test_deep_and_wide_layers():
+    """8 layers, N tiles of 128 and 256, K up to 1024, ragged batch."""
+    from paper_1902_04610_b200 import salus as S
+    jobs = [make_job(0, TRAIN, 0, (256, 384, 512, 128, 1024, 256, 640, 128, 128), 136, 2, lr=1e-2, seed=3),
+            make_job(1, INFER, 0, (1024, 2048, 256), 7, 2, seed=4, request_ticks=(0, 5))]
+    dump = {0: S.DUMP_OUTPUTS | S.DUMP_WEIGHTS, 1: S.DUMP_OUTPUTS}
+    ctx, ref, stats = assert_schedule_parity(jobs, 1 << 30, OS.PACK, null_work=False, dump=dump)
+    try:
+        _check_math(ctx, jobs)
+    finally:
+        ctx.close()

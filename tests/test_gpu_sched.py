@@ -1,0 +1,56 @@
+"""GPU schedule parity: the device-resident scheduler (CTA 0 of the
+persistent kernel) must reproduce the oracle's canonical log byte for byte
+on every config and policy (north star: bit-exact schedules)."""
+import numpy as np
+import pytest
+
+from oracle import scheduler as OS
+from workloads import (c1_trace, c1_tie_trace, c2_trace, c3_trace, c4_trace, c5_trace,
+                       random_sched_trace)
+
+from gpu_helpers import assert_schedule_parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("policy", [OS.FIFO, OS.SRTF, OS.PACK, OS.FAIR])
+def test_c1(policy):
+    jobs, cap = c1_trace()
+    ctx, ref, stats = assert_schedule_parity(jobs, cap, policy)
+    ctx.close()
+    jobs, cap = c1_tie_trace()
+    assert_schedule_parity(jobs, cap, policy)[0].close()
+
+
+@pytest.mark.parametrize("policy", [OS.FIFO, OS.PACK])
+def test_c2_sweep(policy):
+    jobs, cap = c2_trace("a")
+    assert_schedule_parity(jobs, cap, policy)[0].close()
+
+
+@pytest.mark.parametrize("policy,max_lanes", [(OS.PACK, 0), (OS.FAIR, 8), (OS.FAIR, 1), (OS.SRTF, 4)])
+def test_c3_inference(policy, max_lanes):
+    jobs, cap = c3_trace()
+    assert_schedule_parity(jobs, cap, policy, max_lanes=max_lanes)[0].close()
+
+
+@pytest.mark.parametrize("policy", [OS.FIFO, OS.SRTF, OS.PACK, OS.FAIR])
+def test_c4_mixed(policy):
+    jobs, cap = c4_trace()
+    assert_schedule_parity(jobs, cap, policy, switch_ticks=1000)[0].close()
+
+
+def test_c5_2000_jobs_pack():
+    jobs, cap = c5_trace()
+    assert_schedule_parity(jobs, cap, OS.PACK)[0].close()
+
+
+@pytest.mark.parametrize("policy", [OS.FIFO, OS.SRTF, OS.PACK, OS.FAIR])
+def test_random_traces(policy):
+    rng = np.random.default_rng(1000 + policy)
+    for trial in range(12):
+        jobs, cap = random_sched_trace(rng, int(rng.integers(1, 40)), cap_pages=int(rng.integers(8, 120)),
+                                       infer_frac=0.3)
+        ml = int(rng.integers(1, 9)) if policy != OS.FIFO else 0
+        assert_schedule_parity(jobs, cap, policy, max_lanes=ml,
+                               switch_ticks=int(rng.integers(0, 3)), check=True)[0].close()

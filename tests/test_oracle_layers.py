@@ -108,3 +108,33 @@ def test_inference_is_forward_of_init_weights():
     outs, W = LY.run_job(job)
     X1, _ = LY.inputs(job, 1)
     assert np.array_equal(outs[1], LY.forward(LY.init_weights(job), X1)[-1])
+
+
+def test_bf16_storage_mode_rounds_exactly_the_stored_tensors():
+    """Reading A31: store=bf16 rounds W copies, A_l (l>=1) and G_l to bf16;
+    Z_L and the master weights stay fp64."""
+    job = _tiny_job((16, 12, 8, 4), 6, lr=0.1)
+    W = LY.init_weights(job)
+    X, T = LY.inputs(job, 0)
+    A = LY.forward(W, X, LY.bf16)
+    for a in A[1:-1]:
+        assert np.array_equal(LY.bf16(a), a)
+    assert not np.array_equal(LY.bf16(A[-1]), A[-1])         # Z_L unrounded
+    # same structure as the fp64 definition: with identity rounding equal
+    A64 = LY.forward(W, X)
+    assert all(np.allclose(a, b, rtol=2e-2, atol=1e-2) for a, b in zip(A, A64))
+    _, dW16 = LY.gradients(W, X, T, LY.bf16)
+    _, dW64 = LY.gradients(W, X, T)
+    for a, b in zip(dW16, dW64):
+        assert np.max(np.abs(a - b)) <= 0.2 * np.max(np.abs(b))
+
+
+def test_bf16_storage_equals_fp64_when_everything_is_representable():
+    """One layer: X, W are bf16-exact, so forward and dW differ only by the
+    bf16 rounding of G_L."""
+    job = _tiny_job((8, 4), 5, lr=0.0)
+    W = LY.init_weights(job)
+    X, T = LY.inputs(job, 0)
+    assert np.array_equal(LY.forward(W, X, LY.bf16)[-1], LY.forward(W, X)[-1])
+    _, d16 = LY.gradients(W, X, T, LY.bf16)
+    assert np.array_equal(d16[0], X.T @ LY.bf16((X @ W[0] - T) / 5))

@@ -322,7 +322,7 @@ def tiny_math_trace(kind: int = TRAIN, n_jobs: int = 2, dims=(128, 256, 128), ba
     """Small jobs for GEMM parity: several tiles and a ragged batch tail."""
     jobs = []
     for j in range(n_jobs):
-        req = tuple(range(0, 10 * n_iters, 10)) if kind == INFER else ()
+        req = tuple(range(100 * j, 100 * j + 10 * n_iters, 10)) if kind == INFER else ()
         jobs.append(make_job(j, kind, 100 * j, dims, batch, n_iters, lr=lr, seed=77 + j,
                              request_ticks=req))
     return jobs, GIB
