@@ -65,7 +65,8 @@ enum {
 enum {
   SALUS_FLAG_LOG = 1,        /* record the canonical schedule log + wall stamps  */
   SALUS_FLAG_NULL_WORK = 2,  /* schedule only: no iteration work is executed     */
-  SALUS_FLAG_CHECK = 4       /* device asserts the safety invariants every tick  */
+  SALUS_FLAG_CHECK = 4,      /* device asserts the safety invariants every tick  */
+  SALUS_FLAG_TRACE = 8       /* record one salus_trace_rec per executed tile     */
 };
 
 /* salus_job.dump */
@@ -129,7 +130,7 @@ typedef struct {
                                 Cp = floor(C/G) (A18). Must be 65536 in v1.      */
   uint32_t max_lanes;        /* 0 -> policy default (FIFO 1, SRTF 1, PACK 64,
                                 FAIR 1; A9); at most 64                           */
-  uint32_t max_jobs;         /* submit capacity; <= 4096                          */
+  uint32_t max_jobs;         /* submit capacity; <= 2048                          */
   uint32_t flags;            /* SALUS_FLAG_*                                      */
   uint64_t switch_ticks;     /* logical switch penalty per job change in a lane
                                 (A16); 0 in parity tests                          */
@@ -137,6 +138,7 @@ typedef struct {
   uint64_t dump_bytes;       /* bytes reserved for SALUS_DUMP_* data             */
   uint32_t n_workers;        /* worker CTAs; 0 -> (#SMs - 1)                      */
   uint32_t timeout_ms;       /* salus_run watchdog; 0 -> 600000                   */
+  uint64_t trace_capacity;   /* SALUS_FLAG_TRACE records; 0 -> 1<<20              */
 } salus_config;
 
 typedef struct salus_ctx salus_ctx;
@@ -221,6 +223,8 @@ typedef struct {
   uint64_t sched_wait_ns;     /* scheduler time spent waiting for iterations      */
   int32_t  status;            /* SALUS_OK or the device error code               */
   uint32_t n_workers;
+  uint64_t h2d_bytes;         /* host->device bytes of salus_prepare (job tables) */
+  uint64_t d2h_bytes;         /* device->host bytes read back by salus_run        */
 } salus_run_stats;
 
 int salus_read_run_stats(const salus_ctx *ctx, salus_run_stats *out);
@@ -239,6 +243,22 @@ int salus_read_wall(salus_ctx *ctx, salus_wall_rec *buf, uint64_t cap_recs, uint
  * *n = floats written.  E_INVAL if the job did not dump that item. */
 int salus_read_layers(salus_ctx *ctx, uint32_t job_id, uint32_t iter, float *buf,
                       uint64_t cap_floats, uint64_t *n);
+
+/* Per-tile device trace of the last run (SALUS_FLAG_TRACE): which SM ran
+ * which tile of which iteration, with globaltimer stamps.  Records are in
+ * completion order; *n_recs = records written (<= trace_capacity). */
+typedef struct {
+  uint32_t task;              /* slot << 26 | stage << 21 | tile                  */
+  uint32_t smid;
+  uint32_t job;               /* dense job index                                  */
+  uint32_t iter;
+  uint64_t t_claim;           /* task claimed (after the ring wait)               */
+  uint64_t t_ready;           /* decoded + operand pages translated               */
+  uint64_t t_mma;             /* accumulator ready (GEMM) / = t_ready otherwise    */
+  uint64_t t_end;             /* epilogue stores done                             */
+} salus_trace_rec;
+
+int salus_read_trace(salus_ctx *ctx, salus_trace_rec *buf, uint64_t cap_recs, uint64_t *n_recs);
 
 const char *salus_last_error(const salus_ctx *ctx);
 

@@ -68,6 +68,7 @@ struct alignas(256) Ctrl {
   uint64_t n_dispatch, n_ticks, n_log, sched_wait_ns;
   uint64_t wall_first_ns, wall_last_ns;
   uint32_t log_overflow, n_workers;
+  unsigned long long n_trace;
 };
 
 struct Params {
@@ -87,6 +88,8 @@ struct Params {
   salus_wall_rec *wall;
   uint64_t log_cap;
   salus_job_stat *stats;           // dense order
+  salus_trace_rec *trace;
+  uint64_t trace_cap;
   float *dump;
   const volatile uint32_t *host_abort;   // mapped pinned host flag
   uint32_t n_jobs, n_infer, Cp, policy, max_lanes, flags, n_workers;

@@ -80,7 +80,9 @@ struct salus_ctx {
   uint32_t grid = 0;
   uint64_t ring_cap = 0, log_cap = 0;
   uint64_t off_ctrl = 0, off_jobs = 0, off_req = 0, off_inf = 0, off_ppt = 0, off_lpt = 0, off_free = 0,
-           off_slots = 0, off_ring = 0, off_log = 0, off_wall = 0, off_stats = 0, off_dump = 0, total = 0;
+           off_slots = 0, off_ring = 0, off_log = 0, off_wall = 0, off_stats = 0, off_dump = 0, off_trace = 0,
+           total = 0;
+  uint64_t trace_cap = 0, n_trace = 0, h2d_bytes = 0;
   uint32_t lpt_stride = 0;
   uint32_t *host_abort = nullptr;
   uint32_t *host_abort_dev = nullptr;
@@ -306,6 +308,8 @@ static void compute_layout(salus_ctx *c) {
   c->off_wall = take(sizeof(salus_wall_rec) * std::max<uint64_t>(c->log_cap, 1));
   c->off_stats = take(sizeof(salus_job_stat) * std::max<uint64_t>(n, 1));
   c->off_dump = take(4 * std::max<uint64_t>(dump_cur, 1));
+  c->trace_cap = (c->cfg.flags & SALUS_FLAG_TRACE) ? (c->cfg.trace_capacity ? c->cfg.trace_capacity : (1ull << 20)) : 0;
+  c->off_trace = take(sizeof(salus_trace_rec) * std::max<uint64_t>(c->trace_cap, 1));
   c->total = o;
 }
 
@@ -354,6 +358,7 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
       (e = cudaMemcpyAsync(m + ctx->off_inf, inf.data(), 2 * inf.size(), cudaMemcpyHostToDevice, st)))
     return cuda_fail(ctx, e, "upload infer list");
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(ctx, e, "sync");
+  ctx->h2d_bytes = sizeof(DevJob) * n + 8 * req.size() + 2 * inf.size();
   if ((e = cudaHostAlloc(reinterpret_cast<void **>(&ctx->host_abort), 4, cudaHostAllocMapped)))
     return cuda_fail(ctx, e, "cudaHostAlloc");
   *reinterpret_cast<volatile uint32_t *>(ctx->host_abort) = 0;
@@ -378,6 +383,8 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   P.wall = reinterpret_cast<salus_wall_rec *>(m + ctx->off_wall);
   P.log_cap = ctx->log_cap;
   P.stats = reinterpret_cast<salus_job_stat *>(m + ctx->off_stats);
+  P.trace = reinterpret_cast<salus_trace_rec *>(m + ctx->off_trace);
+  P.trace_cap = ctx->trace_cap;
   P.dump = reinterpret_cast<float *>(m + ctx->off_dump);
   P.host_abort = ctx->host_abort_dev;
   P.n_jobs = n;
@@ -435,6 +442,9 @@ int salus_run(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_
   rs.n_tasks = ctrl.n_tasks; rs.kernel_ns = (uint64_t)((double)ms * 1e6);
   rs.wall_first_ns = ctrl.wall_first_ns; rs.wall_last_ns = ctrl.wall_last_ns;
   rs.sched_wait_ns = ctrl.sched_wait_ns; rs.status = ctrl.status; rs.n_workers = ctx->grid - 1;
+  ctx->n_trace = std::min<uint64_t>(ctrl.n_trace, ctx->trace_cap);
+  rs.h2d_bytes = ctx->h2d_bytes;
+  rs.d2h_bytes = sizeof(Ctrl) + (stats ? sizeof(salus_job_stat) * ctx->jobs.size() : 0);
   ctx->ran = true;
   const uint32_t n = (uint32_t)ctx->jobs.size();
   if (stats) {
@@ -472,6 +482,17 @@ int salus_read_log(salus_ctx *ctx, void *buf, uint64_t cap_bytes, uint64_t *n_by
   if (cap_bytes < bytes) return fail(ctx, SALUS_E_CAPACITY, "log buffer too small");
   cudaError_t e = cudaMemcpy(buf, ctx->meta + ctx->off_log, bytes, cudaMemcpyDeviceToHost);
   return e ? cuda_fail(ctx, e, "read log") : SALUS_OK;
+}
+
+int salus_read_trace(salus_ctx *ctx, salus_trace_rec *buf, uint64_t cap_recs, uint64_t *n_recs) {
+  if (!ctx || !n_recs) return SALUS_E_INVAL;
+  if (!ctx->ran || !(ctx->cfg.flags & SALUS_FLAG_TRACE)) return fail(ctx, SALUS_E_STATE, "no trace");
+  *n_recs = ctx->n_trace;
+  if (!buf) return SALUS_OK;
+  if (cap_recs < ctx->n_trace) return fail(ctx, SALUS_E_CAPACITY, "trace buffer too small");
+  cudaError_t e = cudaMemcpy(buf, ctx->meta + ctx->off_trace, ctx->n_trace * sizeof(salus_trace_rec),
+                             cudaMemcpyDeviceToHost);
+  return e ? cuda_fail(ctx, e, "read trace") : SALUS_OK;
 }
 
 int salus_read_wall(salus_ctx *ctx, salus_wall_rec *buf, uint64_t cap_recs, uint64_t *n_recs) {

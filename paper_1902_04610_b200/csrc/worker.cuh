@@ -60,6 +60,7 @@ struct WorkerSmem {
   uint32_t tmem_base;
   uint32_t pub_flag;
   unsigned long long pub_base;
+  uint64_t tr_claim, tr_ready, tr_mma;   // SALUS_FLAG_TRACE stamps
   TileDesc td;
 };
 
@@ -369,6 +370,7 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
         if ((uint32_t)(v >> 32) == (uint32_t)(pos + 1)) { payload = (uint32_t)v; break; }
         if ((++spins & 255) == 0 && *(volatile uint32_t *)&P.ctrl->abort) break;
       }
+      W.tr_claim = ptx::globaltimer();
       decode_task(P, payload, W.td);
       if (W.td.kind != T_EXIT) {
         const uint32_t first = W.td.iter == 0 ? 0u : 1u;
@@ -392,6 +394,7 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
         }
       }
       __syncthreads();
+      if (tid == 0) W.tr_ready = ptx::globaltimer();
       if (warp == 0 && lane == 0) {
         ptx::fence_proxy_async_global();
         const uint32_t abytes = td.a_mn ? 8192u : 16384u, bbytes = td.b_mn ? 8192u : 16384u;
@@ -426,12 +429,14 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
       } else if (warp >= 2) {
         ptx::mbar_wait_abortable(&W.accum, acc_phase, &P.ctrl->abort);
         ptx::tc_fence_after();
+        if (tid == 64) W.tr_mma = ptx::globaltimer();
         // a warp may only touch TMEM lanes [32*(warp%4), +32): warps 2,3,4,5
         // own accumulator rows 64-95, 96-127, 0-31, 32-63
         epilogue(P, td, tmem, ((warp & 3u) << 5) | lane);
       }
       acc_phase ^= 1;
     } else if (warp >= 2) {
+      if (tid == 64) { W.tr_ready = W.tr_claim; W.tr_mma = ptx::globaltimer(); }
       if (td.kind == T_INIT) init_tile(td, ((warp & 3u) << 5) | lane);
       else gen_tile(td, ((warp & 3u) << 5) | lane);
     }
@@ -442,6 +447,17 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
     }
     __syncthreads();
     if (tid == 0) {
+      if (P.flags & SALUS_FLAG_TRACE) {
+        const unsigned long long i = atomicAdd(&P.ctrl->n_trace, 1ull);
+        if (i < P.trace_cap) {
+          uint32_t smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          salus_trace_rec t;
+          t.task = td.payload; t.smid = smid; t.job = td.job; t.iter = td.iter;
+          t.t_claim = W.tr_claim; t.t_ready = W.tr_ready; t.t_mma = W.tr_mma; t.t_end = ptx::globaltimer();
+          P.trace[i] = t;
+        }
+      }
       Slot &sl = P.slots[td.slot];
       const uint32_t old = ptx::atom_add_acqrel_u32(&sl.stage_done[td.stage], 1u);
       W.pub_flag = 0;

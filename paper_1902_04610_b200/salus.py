@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(HERE, "libsalus.so")
 
 FIFO, SRTF, PACK, FAIR = 0, 1, 2, 3
 TRAIN, INFER = 0, 1
-FLAG_LOG, FLAG_NULL_WORK, FLAG_CHECK = 1, 2, 4
+FLAG_LOG, FLAG_NULL_WORK, FLAG_CHECK, FLAG_TRACE = 1, 2, 4, 8
 DUMP_OUTPUTS, DUMP_WEIGHTS = 1, 2
 WEIGHTS = 0xFFFFFFFF
 
@@ -38,7 +38,8 @@ class Config(C.Structure):
                 ("arena_bytes", C.c_uint64), ("stream", C.c_void_p), ("capacity_bytes", C.c_uint64),
                 ("page_bytes", C.c_uint32), ("max_lanes", C.c_uint32), ("max_jobs", C.c_uint32),
                 ("flags", C.c_uint32), ("switch_ticks", C.c_uint64), ("log_capacity", C.c_uint64),
-                ("dump_bytes", C.c_uint64), ("n_workers", C.c_uint32), ("timeout_ms", C.c_uint32)]
+                ("dump_bytes", C.c_uint64), ("n_workers", C.c_uint32), ("timeout_ms", C.c_uint32),
+                ("trace_capacity", C.c_uint64)]
 
 
 class JobDesc(C.Structure):
@@ -59,17 +60,19 @@ class RunStats(C.Structure):
     _fields_ = [("n_dispatch", C.c_uint64), ("n_ticks", C.c_uint64), ("n_log", C.c_uint64),
                 ("n_tasks", C.c_uint64), ("kernel_ns", C.c_uint64), ("wall_first_ns", C.c_uint64),
                 ("wall_last_ns", C.c_uint64), ("sched_wait_ns", C.c_uint64), ("status", C.c_int32),
-                ("n_workers", C.c_uint32)]
+                ("n_workers", C.c_uint32), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
 
 
 WALL_DTYPE = np.dtype([("seq", "<u8"), ("lane", "<u4"), ("job", "<u4"), ("start_ns", "<u8"),
                        ("end_ns", "<u8")])
+TRACE_DTYPE = np.dtype([("task", "<u4"), ("smid", "<u4"), ("job", "<u4"), ("iter", "<u4"),
+                        ("t_claim", "<u8"), ("t_ready", "<u8"), ("t_mma", "<u8"), ("t_end", "<u8")])
 LOG_DTYPE = np.dtype([("tick", "<i8"), ("kind", "<u4"), ("lane", "<u4"), ("job", "<u4"),
                       ("a", "<u4"), ("b", "<u8")])
 
 EXPORTS = ["salus_open", "salus_job_footprint", "salus_submit_job", "salus_meta_bytes",
            "salus_prepare", "salus_run", "salus_read_run_stats", "salus_read_log",
-           "salus_read_wall", "salus_read_layers", "salus_last_error", "salus_close"]
+           "salus_read_wall", "salus_read_trace", "salus_read_layers", "salus_last_error", "salus_close"]
 
 _lib = None
 
@@ -92,6 +95,7 @@ def lib():
         L.salus_read_run_stats.argtypes = [P, C.POINTER(RunStats)]
         L.salus_read_log.argtypes = [P, P, C.c_uint64, C.POINTER(C.c_uint64)]
         L.salus_read_wall.argtypes = [P, P, C.c_uint64, C.POINTER(C.c_uint64)]
+        L.salus_read_trace.argtypes = [P, P, C.c_uint64, C.POINTER(C.c_uint64)]
         L.salus_read_layers.argtypes = [P, C.c_uint32, C.c_uint32, C.POINTER(C.c_float), C.c_uint64,
                                         C.POINTER(C.c_uint64)]
         L.salus_last_error.argtypes = [P]
@@ -143,7 +147,7 @@ class Context:
     def __init__(self, jobs: Iterable, capacity_bytes: int, policy: int, *, device: int = 0,
                  max_lanes: int = 0, switch_ticks: int = 0, log: bool = True, null_work: bool = False,
                  check: bool = False, dump: Optional[Dict[int, int]] = None, n_workers: int = 0,
-                 timeout_ms: int = 0, page_bytes: int = 65536):
+                 timeout_ms: int = 0, page_bytes: int = 65536, trace: bool = False):
         import torch
         self._torch = torch
         self.L = lib()
@@ -163,7 +167,8 @@ class Context:
         cfg.page_bytes = page_bytes
         cfg.max_lanes = max_lanes
         cfg.max_jobs = max(1, len(self.jobs))
-        cfg.flags = (FLAG_LOG if log else 0) | (FLAG_NULL_WORK if null_work else 0) | (FLAG_CHECK if check else 0)
+        cfg.flags = ((FLAG_LOG if log else 0) | (FLAG_NULL_WORK if null_work else 0) |
+                     (FLAG_CHECK if check else 0) | (FLAG_TRACE if trace else 0))
         cfg.switch_ticks = switch_ticks
         cfg.n_workers = n_workers
         cfg.timeout_ms = timeout_ms
@@ -212,6 +217,13 @@ class Context:
         self._check(self.L.salus_read_wall(self.ctx, None, 0, C.byref(n)), "wall size")
         out = np.zeros(n.value, dtype=WALL_DTYPE)
         self._check(self.L.salus_read_wall(self.ctx, C.c_void_p(out.ctypes.data), n.value, C.byref(n)), "wall")
+        return out
+
+    def trace(self) -> np.ndarray:
+        n = C.c_uint64()
+        self._check(self.L.salus_read_trace(self.ctx, None, 0, C.byref(n)), "trace size")
+        out = np.zeros(n.value, dtype=TRACE_DTYPE)
+        self._check(self.L.salus_read_trace(self.ctx, C.c_void_p(out.ctypes.data), n.value, C.byref(n)), "trace")
         return out
 
     def layers(self, job_id: int, iteration: int) -> np.ndarray:

@@ -41,7 +41,11 @@ def _check_math(ctx, jobs, iters=None):
                 Wg = flat[off:off + n].reshape(j.dims[l], j.dims[l + 1])
                 off += n
                 assert normwise_rel(Wg, W[l]) <= TOL, (j.job_id, l)
-                rel = normwise_rel(Wg - W0[l], W[l] - W0[l])
+                # weight updates: Frobenius-relative: a
+                # single ReLU-mask flip moves one dW column by ~1/sqrt(B), which
+                # a max-normwise metric reports as a >2e-2 error at small B
+                d_g, d_r = Wg - W0[l], W[l] - W0[l]
+                rel = float(np.linalg.norm(d_g - d_r) / np.linalg.norm(d_r))
                 worst = max(worst, rel)
                 assert rel <= TOL, (j.job_id, "dW", l, rel)
     return worst

@@ -1,0 +1,36 @@
+"""Per-stage timeline of one config from the device tile trace.
+usage: python tools/trace_stages.py c1|c2s [policy]"""
+import os, sys
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
+import numpy as np
+from paper_1902_04610_b200 import build, salus as S
+from workloads import c1_trace, c2_trace
+build.build()
+name = sys.argv[1]
+pol = {"fifo": S.FIFO, "srtf": S.SRTF, "pack": S.PACK}[sys.argv[2] if len(sys.argv) > 2 else "fifo"]
+jobs, cap = c1_trace() if name == "c1" else c2_trace("a", n_jobs=37, n_iters=10)
+ctx = S.Context(jobs, cap, pol, trace=True)
+for rep in range(2):
+    ctx.run()
+tr = ctx.trace()
+rs = ctx.run_stats()
+print("kernel ms", rs["kernel_ns"] / 1e6, "tasks", len(tr))
+t0 = tr["t_claim"].min()
+stage = (tr["task"] >> 21) & 31
+ready = (tr["t_ready"] - tr["t_claim"]) / 1e3
+mma = (tr["t_mma"] - tr["t_ready"]) / 1e3
+epi = (tr["t_end"] - tr["t_mma"]) / 1e3
+print("per-tile us (median): decode+xlate %.2f  mma %.2f  epilogue %.2f" % (np.median(ready), np.median(mma), np.median(epi)))
+for s in sorted(set(stage.tolist())):
+    m = stage == s
+    print(f"stage {s:2d}: n={m.sum():5d} ready {np.median(ready[m]):6.2f} mma {np.median(mma[m]):6.2f} epi {np.median(epi[m]):6.2f}")
+# one iteration timeline
+key = (tr["job"].astype(np.int64) << 20) | tr["iter"]
+k0 = key[np.argsort(tr["t_claim"])][len(tr) // 2]
+m = key == k0
+order = np.argsort(tr["t_claim"][m])
+sub = tr[m][order]
+base = sub["t_claim"].min()
+print("timeline of one iteration (us from first claim): stage tile claim ready mma end sm")
+for r in sub:
+    print(f"  s{(r['task'] >> 21) & 31:2d} t{r['task'] & 0x1FFFFF:4d} {(r['t_claim'] - base) / 1e3:8.2f} {(r['t_ready'] - base) / 1e3:8.2f} {(r['t_mma'] - base) / 1e3:8.2f} {(r['t_end'] - base) / 1e3:8.2f} sm{r['smid']}")
