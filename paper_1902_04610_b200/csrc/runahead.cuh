@@ -1,0 +1,62 @@
+// runahead.cuh — per-slot dispatch rings for run-ahead execution (SURVEY
+// §8(c)-A30 mode 2).
+//
+// The schedule is decided purely in logical ticks by the scheduler warp,
+// which appends each DISPATCH to its lane slot's ring of RQ records.  A slot
+// executes its records strictly in order ("iteration execution is serialised
+// within a lane"): whoever holds the slot's `running` token —
+// the scheduler after an append to an idle slot, or the worker thread that
+// completes an iteration's last tile — takes the next record and starts it.
+// The handoff is a Dekker-style store/fence/load on (q_tail, running), so an
+// append racing with the last completion is never lost.
+#pragma once
+#include "salus_dev.h"
+#include "ptx.cuh"
+
+namespace salus {
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// Caller holds `running`.  Takes the next record (true) or releases the token
+// (false), re-checking for an append that raced with the release.
+__device__ __forceinline__ bool take_next(Slot &sl, DispRec *rec) {
+  for (;;) {
+    const uint32_t h = *(volatile uint32_t *)&sl.q_head;
+    uint32_t t = ld_acquire_u32(&sl.q_tail);
+    if (h != t) {
+      const volatile DispRec *vr = &sl.recs[h % RQ];
+      rec->job = vr->job; rec->iter = vr->iter; rec->seq = vr->seq; rec->lane_id = vr->lane_id; rec->pad = 0;
+      st_release_u32(&sl.q_head, h + 1);
+      return true;
+    }
+    st_release_u32(&sl.running, 0u);
+    __threadfence();                                  // store running -> load q_tail (SC)
+    t = ld_acquire_u32(&sl.q_tail);
+    if (h == t) return false;
+    if (atomicCAS(&sl.running, 0u, 1u) != 0u) return false;   // the appender took it
+  }
+}
+
+// Single thread: make `rec` the slot's in-flight iteration.  Returns the first
+// stage (INIT before a job's first iteration, else GEN); the caller enqueues
+// that stage's tiles after this returns (the fence orders these writes first).
+__device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec) {
+  sl.job = rec.job;
+  sl.iter = rec.iter;
+  sl.seq = rec.seq;
+  sl.lane_id = rec.lane_id;
+  sl.start_ns = ~0ull;
+  sl.end_ns = 0;
+  for (uint32_t k = 0; k < MAX_STAGES + 2; k++) sl.stage_done[k] = 0;
+  __threadfence();
+  return rec.iter == 0 ? 0u : 1u;
+}
+
+}  // namespace salus

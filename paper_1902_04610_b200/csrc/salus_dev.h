@@ -45,16 +45,33 @@ struct DevJob {
   uint32_t stage_tiles[MAX_STAGES];       // tiles per stage
 };
 
-// One physical lane slot: the dispatch record the scheduler writes and the
-// per-stage completion counters the worker CTAs update.  256-B aligned.
+// Run-ahead execution (A30 mode 2): the scheduler appends dispatch records to
+// a per-slot ring; the thread that completes an iteration starts the slot's
+// next record itself, so a lane never waits for the scheduler.
+constexpr uint32_t RQ = 32;            // records queued per slot (run-ahead depth)
+
+struct DispRec {
+  uint32_t job, iter;                  // dense job index, iteration index
+  uint64_t seq;                        // global dispatch seq
+  uint32_t lane_id, pad;               // logical lane id (for the wall log)
+};
+
+// One physical lane slot.  256-B aligned.
 struct alignas(256) Slot {
+  // the in-flight iteration (written by whoever started it)
   uint32_t job;             // dense job index of the in-flight iteration
   uint32_t iter;            // iteration index k
   uint64_t seq;             // global dispatch seq
   uint64_t start_ns;        // min globaltimer over first-stage tiles (atomicMin)
   uint64_t end_ns;          // globaltimer when the last stage completed
-  uint64_t done_seq;        // seq + 1 once the iteration is physically complete
+  uint64_t done_seq;        // seq + 1 of the last physically completed iteration (monotonic)
+  uint32_t lane_id;
   uint32_t stage_done[MAX_STAGES + 2];
+  // dispatch ring
+  uint32_t q_tail;          // records appended (scheduler; release)
+  uint32_t q_head;          // records started (only the holder of `running`)
+  uint32_t running;         // 1 while an iteration is in flight or being started
+  DispRec recs[RQ];
 };
 
 // Control block at the start of meta.
@@ -81,6 +98,9 @@ struct Params {
   uint32_t *lpt;                   // lane page tables: MAX_LANES x lpt_stride
   uint32_t lpt_stride;
   uint32_t *free_stack;            // Cp entries
+  uint8_t *fence_slot;             // per page: slot of its last user (A30 mode 2 fences)
+  uint64_t *fence_seq;             // per page: last user's final seq + 1 (0 = none)
+  unsigned long long *pend_fence;  // [target slot][source slot]: seq + 1 to wait for
   Slot *slots;                     // MAX_LANES
   unsigned long long *ring;        // task ring (seq << 32 | payload)
   uint32_t ring_mask;
@@ -108,8 +128,9 @@ __host__ __device__ inline uint32_t last_stage(uint32_t kind, uint32_t L) {
   return kind == SALUS_TRAIN ? 2 * L + 1 : L + 1;
 }
 
-__host__ __device__ inline uint32_t ntile_for(uint32_t dpad) {   // GEMM N tile
-  return (dpad % 256 == 0) ? 256 : 128;
-}
+// GEMM N tile for an output width (padded to 128): 256 when it divides, else
+// 128.  Wide tiles halve operand re-reads; the epilogue streams its input
+// (fp32 master weights / ReLU mask) through two 32 KiB smem chunk buffers.
+__host__ __device__ inline uint32_t ntile_for(uint32_t dpad) { return (dpad % 256 == 0) ? 256 : 128; }
 
 }  // namespace salus

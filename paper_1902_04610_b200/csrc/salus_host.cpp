@@ -80,7 +80,7 @@ struct salus_ctx {
   uint32_t grid = 0;
   uint64_t ring_cap = 0, log_cap = 0;
   uint64_t off_ctrl = 0, off_jobs = 0, off_req = 0, off_inf = 0, off_ppt = 0, off_lpt = 0, off_free = 0,
-           off_slots = 0, off_ring = 0, off_log = 0, off_wall = 0, off_stats = 0, off_dump = 0, off_trace = 0,
+           off_slots = 0, off_ring = 0, off_fslot = 0, off_fseq = 0, off_pend = 0, off_log = 0, off_wall = 0, off_stats = 0, off_dump = 0, off_trace = 0,
            total = 0;
   uint64_t trace_cap = 0, n_trace = 0, h2d_bytes = 0;
   uint32_t lpt_stride = 0;
@@ -302,6 +302,9 @@ static void compute_layout(salus_ctx *c) {
   c->off_ppt = take(4 * std::max<uint64_t>(ppt_total, 1));
   c->off_lpt = take(4ull * MAX_LANES * c->lpt_stride);
   c->off_free = take(4ull * c->Cp);
+  c->off_fslot = take(1ull * c->Cp);
+  c->off_fseq = take(8ull * c->Cp);
+  c->off_pend = take(8ull * MAX_LANES * MAX_LANES);
   c->off_slots = take(sizeof(Slot) * MAX_LANES);
   c->off_ring = take(8 * c->ring_cap);
   c->off_log = take(sizeof(salus_log_rec) * std::max<uint64_t>(c->log_cap, 1));
@@ -376,6 +379,9 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   P.lpt = reinterpret_cast<uint32_t *>(m + ctx->off_lpt);
   P.lpt_stride = ctx->lpt_stride;
   P.free_stack = reinterpret_cast<uint32_t *>(m + ctx->off_free);
+  P.fence_slot = m + ctx->off_fslot;
+  P.fence_seq = reinterpret_cast<uint64_t *>(m + ctx->off_fseq);
+  P.pend_fence = reinterpret_cast<unsigned long long *>(m + ctx->off_pend);
   P.slots = reinterpret_cast<Slot *>(m + ctx->off_slots);
   P.ring = reinterpret_cast<unsigned long long *>(m + ctx->off_ring);
   P.ring_mask = (uint32_t)(ctx->ring_cap - 1);
@@ -409,7 +415,9 @@ int salus_run(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_
   uint8_t *m = ctx->meta;
   if ((e = cudaMemsetAsync(m + ctx->off_ctrl, 0, sizeof(Ctrl), st)) ||
       (e = cudaMemsetAsync(m + ctx->off_slots, 0, sizeof(Slot) * MAX_LANES, st)) ||
-      (e = cudaMemsetAsync(m + ctx->off_ring, 0, 8 * ctx->ring_cap, st)))
+      (e = cudaMemsetAsync(m + ctx->off_ring, 0, 8 * ctx->ring_cap, st)) ||
+      (e = cudaMemsetAsync(m + ctx->off_fseq, 0, 8ull * ctx->Cp, st)) ||
+      (e = cudaMemsetAsync(m + ctx->off_pend, 0, 8ull * MAX_LANES * MAX_LANES, st)))
     return cuda_fail(ctx, e, "reset");
   *reinterpret_cast<volatile uint32_t *>(ctx->host_abort) = 0;
   if ((e = cudaEventRecord(ctx->ev0, st))) return cuda_fail(ctx, e, "event");

@@ -10,12 +10,14 @@
 // the 32 threads (ballot / shuffle reductions); shared-memory writes of
 // scalar state are done by thread 0 followed by __syncwarp().
 //
-// Coupled execution (A30 mode 1): tick t is processed only after every
-// iteration whose logical end is <= t has physically completed, so memory
-// freed at t is physically free when it is re-handed out at t.
+// Run-ahead execution (A30 mode 2): decisions use logical ticks only, so the
+// scheduler never waits for an iteration to finish; it appends each dispatch
+// to its lane slot's ring (runahead.cuh) and moves on.  It blocks only for
+// ring backpressure and for page-reuse fences (see pop_pages).
 #pragma once
 #include "salus_dev.h"
 #include "ptx.cuh"
+#include "runahead.cuh"
 
 namespace salus {
 
@@ -39,6 +41,9 @@ struct SchedShared {
   uint16_t Q[MAX_JOBS];
   uint16_t adm[MAX_JOBS];                   // admitted, unfinished
   uint8_t st[MAX_JOBS], jslot[MAX_JOBS], kind[MAX_JOBS];
+  // run-ahead: records appended per physical slot, last appended seq + 1
+  uint32_t sq_tail[MAX_LANES];
+  uint64_t last_app[MAX_LANES];
 };
 
 __device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
@@ -78,8 +83,11 @@ struct Sched {
   uint64_t slot_free = ~0ull;
   int64_t next_arrival = IDLE_T;
   bool dirty = false;
+  bool physical = true;                      // false in SALUS_FLAG_NULL_WORK
+  uint64_t pend_mask = 0;                    // target slots with page-reuse fences
 
-  __device__ Sched(const Params &p_, SchedShared &s_) : P(p_), S(s_), tid(threadIdx.x & 31) {}
+  __device__ Sched(const Params &p_, SchedShared &s_)
+      : P(p_), S(s_), tid(threadIdx.x & 31), physical(!(p_.flags & SALUS_FLAG_NULL_WORK)) {}
 
   __device__ void fail(int32_t code, uint32_t info) {
     if (tid == 0 && err == 0) {
@@ -103,14 +111,39 @@ struct Sched {
   // ------------------------------------------------------------ page pool
   // A18: the arena is a pool of 64 KiB pages; a lane / persistent region is a
   // page list, so "auto defragmentation" never moves data.
-  __device__ void pop_pages(uint32_t *dst, uint32_t k) {
+  //
+  // Run-ahead (A30 mode 2) makes page reuse the one physical hazard: a page
+  // freed at logical tick t may still be in use by its previous owner's
+  // queued iterations.  Every freed page therefore carries a fence (slot,
+  // seq+1 of that owner's final iteration); popping it for a different
+  // target slot records the fence, and the target's next record is appended
+  // only after the fence iteration has physically completed.
+  __device__ void pop_pages(uint32_t *dst, uint32_t k, uint32_t target) {
     if (k > free_top) { fail(SALUS_E_CAPACITY, 1); return; }
-    for (uint32_t i = tid; i < k; i += 32) dst[i] = P.free_stack[free_top - k + i];
+    bool any = false;
+    for (uint32_t i = tid; i < k; i += 32) {
+      const uint32_t pg = P.free_stack[free_top - k + i];
+      dst[i] = pg;
+      if (physical) {
+        const uint64_t fs = P.fence_seq[pg];
+        const uint32_t src = P.fence_slot[pg];
+        if (fs && src != target) {
+          atomicMax(&P.pend_fence[target * MAX_LANES + src], (unsigned long long)fs);
+          any = true;
+        }
+        P.fence_seq[pg] = 0;
+      }
+    }
+    if (__any_sync(0xffffffffu, any)) pend_mask |= 1ull << target;
     free_top -= k;
     __syncwarp();
   }
-  __device__ void push_pages(const uint32_t *src, uint32_t k) {
-    for (uint32_t i = tid; i < k; i += 32) P.free_stack[free_top + i] = src[i];
+  __device__ void push_pages(const uint32_t *src, uint32_t k, uint32_t fslot, uint64_t fseq) {
+    for (uint32_t i = tid; i < k; i += 32) {
+      const uint32_t pg = src[i];
+      P.free_stack[free_top + i] = pg;
+      if (physical) { P.fence_slot[pg] = (uint8_t)fslot; P.fence_seq[pg] = fseq + 1; }
+    }
     free_top += k;
     __syncwarp();
   }
@@ -170,12 +203,13 @@ struct Sched {
 
   __device__ bool host_abort() const { return P.host_abort && ptx::ld_volatile_u32(P.host_abort) != 0; }
 
-  // Spin until the iteration `sq` in `slot` is physically complete (A30 mode 1)
-  __device__ void wait_slot(uint32_t slot, uint64_t sq) {
+  // Spin until `slot` has physically completed the iteration with seq + 1 ==
+  // want (done_seq is monotonic per slot).
+  __device__ void wait_slot(uint32_t slot, uint64_t want) {
     uint64_t t0 = ptx::globaltimer();
     uint32_t ok = 0, spins = 0;
     while (true) {
-      if (tid == 0) ok = ptx::ld_acquire_u64(&P.slots[slot].done_seq) == sq + 1;
+      if (tid == 0) ok = ptx::ld_acquire_u64(&P.slots[slot].done_seq) >= want;
       ok = __shfl_sync(0xffffffffu, ok, 0);
       if (ok) break;
       if ((++spins & 1023) == 0) {
@@ -203,6 +237,7 @@ struct Sched {
       st.completion_tick = -1; st.completion_seq = ~0ull; st.wall_start_ns = 0; st.wall_end_ns = 0;
     }
     for (uint32_t i = tid; i < P.Cp; i += 32) P.free_stack[i] = P.Cp - 1 - i;
+    for (uint32_t i = tid; i < MAX_LANES; i += 32) { S.sq_tail[i] = 0; S.last_app[i] = 0; }
     free_top = P.Cp;
     max_lanes = P.max_lanes;
     next_arrival = N ? P.jobs[0].arrival : IDLE_T;
@@ -247,25 +282,8 @@ struct Sched {
     for (uint32_t i = 0; i < nl;) {
       if (S.lane_busy[i] != t) { i++; continue; }
       const uint32_t slot = S.lane_slot[i];
-      if (!(P.flags & SALUS_FLAG_NULL_WORK)) {
-        wait_slot(slot, S.lane_seq[i]);
-        if (err) return;
-        if ((P.flags & SALUS_FLAG_LOG) && tid == 0 && S.lane_seq[i] < P.log_cap) {
-          salus_wall_rec w;
-          w.seq = S.lane_seq[i]; w.lane = S.lane_id[i]; w.job = S.id[S.lane_cur[i]];
-          w.start_ns = P.slots[slot].start_ns; w.end_ns = P.slots[slot].end_ns;
-          P.wall[S.lane_seq[i]] = w;
-        }
-      }
       const uint32_t j = S.lane_cur[i];
-      if (tid == 0) {
-        S.done[j] += 1; S.svc[j] += S.c[j]; S.lane_busy[i] = IDLE_T;
-        if (!(P.flags & SALUS_FLAG_NULL_WORK)) {
-          salus_job_stat &st = P.stats[j];
-          if (st.wall_start_ns == 0) st.wall_start_ns = P.slots[slot].start_ns;
-          st.wall_end_ns = P.slots[slot].end_ns;
-        }
-      }
+      if (tid == 0) { S.done[j] += 1; S.svc[j] += S.c[j]; S.lane_busy[i] = IDLE_T; }
       __syncwarp();
       if (S.done[j] == S.n[j]) {
         if (tid == 0) {
@@ -276,7 +294,7 @@ struct Sched {
         __syncwarp();
         remove_adm(j);
         emit(SALUS_REC_JOB_FINISH, S.lane_id[i], S.id[j], S.n[j], P.stats[j].completion_seq);
-        push_pages(job_table(j), S.ap[j]);
+        push_pages(job_table(j), S.ap[j], slot, P.stats[j].completion_seq);
         // residents left in this lane: count, max e, max actual e
         uint32_t cnt = 0, maxe = 0, maxae = 0;
         for (uint32_t a = tid; a < an; a += 32) {
@@ -288,7 +306,7 @@ struct Sched {
         maxae = warp_max_u32(maxae);
         if (cnt == 0) {                           // ref(lane) == 0: delete lane
           emit(SALUS_REC_LANE_CLOSE, S.lane_id[i], S.id[j], 0, 0);
-          push_pages(lane_table(slot), S.lane_back[i]);
+          push_pages(lane_table(slot), S.lane_back[i], slot, S.lane_seq[i]);
           sumL -= S.lane_L[i];
           slot_free |= (1ull << slot);
           remove_lane(i);
@@ -300,7 +318,7 @@ struct Sched {
           if (tid == 0) S.lane_L[i] = maxe;
         }
         if (maxae < S.lane_back[i]) {
-          push_pages(lane_table(slot) + maxae, S.lane_back[i] - maxae);
+          push_pages(lane_table(slot) + maxae, S.lane_back[i] - maxae, slot, S.lane_seq[i]);
           if (tid == 0) S.lane_back[i] = maxae;
         }
         __syncwarp();
@@ -426,10 +444,13 @@ struct Sched {
     // physical backing: the lane grows to the max actual E of its residents,
     // the job's persistent tensors get their own pages (Observation 2)
     if (S.ae[j] > S.lane_back[li]) {
-      pop_pages(lane_table(slot) + S.lane_back[li], S.ae[j] - S.lane_back[li]);
+      // the slot's page table is about to be rewritten: iterations already
+      // queued on this slot (run-ahead) translate through it, so drain them
+      if (physical && S.last_app[slot]) wait_slot(slot, S.last_app[slot]);
+      pop_pages(lane_table(slot) + S.lane_back[li], S.ae[j] - S.lane_back[li], slot);
       if (tid == 0) S.lane_back[li] = S.ae[j];
     }
-    pop_pages(job_table(j), S.ap[j]);
+    pop_pages(job_table(j), S.ap[j], slot);
     if (P.policy == SALUS_FAIR) {                        // A12: virtual-time start
       const int64_t m = min_svc_in(slot, NONE32, false);
       if (tid == 0) S.svc[j] = (m == IDLE_T) ? 0 : m;
@@ -473,16 +494,78 @@ struct Sched {
     }
   }
 
-  __device__ void dispatch_physical(uint32_t slot, uint32_t j) {
-    Slot &sl = P.slots[slot];
-    if (tid == 0) {
-      sl.job = j; sl.iter = S.done[j]; sl.seq = seq; sl.start_ns = ~0ull; sl.end_ns = 0;
+  // Page-reuse fences of `slot` (pop_pages): wait until every source slot has
+  // physically completed the recorded iteration, then clear them.
+  __device__ void wait_fences(uint32_t slot) {
+    if (!((pend_mask >> slot) & 1ull)) return;
+    for (uint32_t q = 0; q < MAX_LANES; q++) {
+      unsigned long long *pf = &P.pend_fence[slot * MAX_LANES + q];
+      const uint64_t want = *(volatile unsigned long long *)pf;
+      if (want) {
+        wait_slot(q, want);
+        if (err) return;
+        if (tid == 0) *pf = 0;
+      }
     }
-    for (uint32_t k = tid; k < MAX_STAGES + 2; k += 32) sl.stage_done[k] = 0;
-    __threadfence();
     __syncwarp();
-    const uint32_t first = S.done[j] == 0 ? 0u : 1u;    // INIT only before the first iteration
-    enqueue(slot, first, P.jobs[j].stage_tiles[first]);
+    pend_mask &= ~(1ull << slot);
+  }
+
+  // Append the dispatch to the slot's ring (A30 mode 2); if the slot is idle,
+  // take the `running` token and start it here, else the worker finishing
+  // the slot's current iteration will.
+  __device__ void append(uint32_t slot, uint32_t lane_id, uint32_t j) {
+    wait_fences(slot);
+    if (err) return;
+    Slot &sl = P.slots[slot];
+    const uint32_t tl = S.sq_tail[slot];
+    {                                                      // backpressure: RQ in flight
+      uint64_t t0 = 0;
+      uint32_t full = 1, spins = 0;
+      while (true) {
+        if (tid == 0) full = tl - ld_acquire_u32(&sl.q_head) >= RQ;
+        full = __shfl_sync(0xffffffffu, full, 0);
+        if (!full) break;
+        if (t0 == 0) t0 = ptx::globaltimer();
+        if ((++spins & 1023) == 0) {
+          uint32_t bad = 0;
+          if (tid == 0) bad = host_abort() || (ptx::globaltimer() - t0 > P.timeout_ns) ||
+                              *(volatile uint32_t *)&P.ctrl->abort;
+          if (__shfl_sync(0xffffffffu, bad, 0)) { fail(host_abort() ? SALUS_E_TIMEOUT : SALUS_E_STUCK, 6); return; }
+        }
+      }
+      if (t0) wait_ns += ptx::globaltimer() - t0;
+    }
+    uint32_t won = 0;
+    if (tid == 0) {
+      volatile DispRec *vr = &sl.recs[tl % RQ];
+      vr->job = j; vr->iter = S.done[j]; vr->seq = seq; vr->lane_id = lane_id; vr->pad = 0;
+      st_release_u32(&sl.q_tail, tl + 1);
+      __threadfence();                                     // store q_tail -> CAS running (SC)
+      won = atomicCAS(&sl.running, 0u, 1u) == 0u;
+      S.sq_tail[slot] = tl + 1;
+      S.last_app[slot] = seq + 1;
+    }
+    __syncwarp();
+    won = __shfl_sync(0xffffffffu, won, 0);
+    if (!won) return;
+    uint32_t got = 0, first = 0, jj = 0;
+    if (tid == 0) {
+      DispRec r;
+      got = take_next(sl, &r);
+      if (got) { first = begin_iteration(sl, r); jj = r.job; }
+    }
+    got = __shfl_sync(0xffffffffu, got, 0);
+    if (!got) return;
+    first = __shfl_sync(0xffffffffu, first, 0);
+    jj = __shfl_sync(0xffffffffu, jj, 0);
+    enqueue(slot, first, P.jobs[jj].stage_tiles[first]);
+  }
+
+  // End of the schedule: wait for every slot to drain its ring.
+  __device__ void drain() {
+    for (uint32_t s = 0; s < MAX_LANES && !err; s++)
+      if (S.last_app[s]) wait_slot(s, S.last_app[s]);
   }
 
   // P4: every idle lane dispatches its next iteration
@@ -518,7 +601,7 @@ struct Sched {
       }
       __syncwarp();
       emit(SALUS_REC_DISPATCH, S.lane_id[i], S.id[j], S.done[j], seq);
-      if (!(P.flags & SALUS_FLAG_NULL_WORK)) dispatch_physical(slot, j);
+      if (physical) append(slot, S.lane_id[i], j);
       seq++;
     }
   }
@@ -548,6 +631,7 @@ struct Sched {
         if (__shfl_sync(0xffffffffu, bad, 0)) fail(SALUS_E_TIMEOUT, 5);
       }
     }
+    if (physical && !err) drain();
     // release the workers
     {
       unsigned long long base = 0;

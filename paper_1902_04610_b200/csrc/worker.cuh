@@ -1,35 +1,58 @@
-// worker.cuh — worker CTAs of the persistent kernel.  Each worker loops:
-// claim a tile task from the device task ring, execute it, and, if it was the
-// last tile of its stage, publish the next stage of that iteration (or mark
-// the iteration complete for the scheduler).  No host round-trip and no
-// context teardown between iterations or jobs: TMEM and barriers are set up
-// once per kernel, and a "job switch" is just a task with a different slot.
+// worker.cuh — worker CTAs of the persistent kernel.
 //
-// GEMM tiles (the only tensor-core work, north star): M = 128 rows, N = 128
-// or 256, K in chunks of 64 bf16.  Operands are bf16 tensors stored in HBM as
-// 128-byte-swizzled column panels, so every K-chunk
-// of an operand is one or a few contiguous 8/16 KiB blocks moved by the bulk
-// async copy engine (cp.async.bulk, TMA unit) into a 4-stage mbarrier ring;
-// one thread issues tcgen05.mma (kind::f16, fp32 accumulate in TMEM); four
-// epilogue warps drain TMEM with tcgen05.ld and apply the fused epilogue.
+// Each worker CTA is a warp-specialized, persistent tile engine (9 warps):
+//   warp 0     decoder: claims tile tasks from the device task ring up to
+//              NDESC tiles ahead, decodes them (stage -> GEMM / epilogue kind,
+//              tensors, coordinates) and translates the epilogue's page
+//              addresses, lanes in parallel.
+//   warp 1     operand loader (1 thread): issues every K-chunk of the A/B
+//              operands as bulk async copies (cp.async.bulk, TMA unit) into a
+//              3-stage mbarrier ring, translating pages on the fly.
+//   warp 2     MMA (1 thread): tcgen05.mma kind::f16 (bf16 in, fp32 accumulate)
+//              into one of two TMEM accumulators of 256 columns (double
+//              buffered: the epilogue of tile i overlaps the MMA of tile i+1).
+//   warp 3     epilogue-input loader (1 thread): streams the tile's epilogue
+//              input (fp32 master weights of a dW tile, ReLU mask of a dX
+//              tile) in 32 KiB chunks through two smem buffers.
+//   warps 4-7  epilogue: drain TMEM (tcgen05.ld), fused epilogue, stores.
+//   warp 8     completion: gpu-scope fence, stage accounting, publication of
+//              the next stage / start of the slot's next iteration (run-ahead)
+//              -- off the epilogue's critical path.
+// No host round-trip and no context teardown between iterations or jobs: a
+// "job switch" is just a task whose slot points at a different job.
+//
+// Tiles are M = 128 x N (N = 256 when it divides the output width, else 128),
+// K in chunks of 64 bf16.  Operands are bf16 tensors stored as 128-byte-
+// swizzled 64-column panels, so a K-chunk is one 16 KiB block
+// per 128 rows (K-major) or one 8 KiB block per 64 columns (MN-major).
 #pragma once
 #include <cuda_bf16.h>
 #include "salus_dev.h"
 #include "ptx.cuh"
 #include "datagen.cuh"
+#include "runahead.cuh"
 
 namespace salus {
 
-constexpr uint32_t PIPE = 4;
+constexpr uint32_t PIPE = 3;
 constexpr uint32_t STAGE_A_BYTES = 16384;             // 128 x 64 bf16
-constexpr uint32_t STAGE_B_BYTES = 32768;             // 256 x 64 bf16
+constexpr uint32_t STAGE_B_BYTES = 32768;             // <= 256 x 64 bf16
 constexpr uint32_t STAGE_BYTES = STAGE_A_BYTES + STAGE_B_BYTES;
-constexpr uint32_t MAX_COPIES = 1024;
-constexpr uint32_t WORKER_THREADS = 192;              // w0 producer, w1 MMA, w2-5 epilogue
-constexpr uint32_t TMEM_COLS = 256;
+constexpr uint32_t ECH_BYTES = 32768;                 // epilogue-input chunk
+constexpr uint32_t NDESC = 4;                         // decoder lookahead (tiles)
+constexpr uint32_t EPI_WARPS = 4;
+constexpr uint32_t EPI_THREADS = 32 * EPI_WARPS;
+constexpr uint32_t EPI_WARP0 = 4;
+constexpr uint32_t DONE_WARP = EPI_WARP0 + EPI_WARPS;          // completion warp
+constexpr uint32_t WORKER_THREADS = 32 * (DONE_WARP + 1);
+constexpr uint32_t ACC_COLS = 256;
+constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;          // all of TMEM: 2 accumulators
 
 enum : uint32_t { T_EXIT = 0, T_INIT = 1, T_GEN = 2, T_GEMM = 3 };
 enum : uint32_t { EPI_RELU = 0, EPI_OUT = 1, EPI_LOSS = 2, EPI_DX = 3, EPI_SGD = 4 };
+// translated pointers of a tile: bf16 output panels, Wb panels (SGD/INIT),
+// fp32 master pages, epilogue-input panels (DX mask)
+enum : uint32_t { PTR_OUT = 0, PTR_AUX = 4, PTR_W32 = 8, PTR_EPI = 10, NPTR = 14 };
 
 struct OpDesc {
   const uint32_t *table;   // page table of the operand's space
@@ -37,36 +60,47 @@ struct OpDesc {
 };
 
 struct TileDesc {
-  uint32_t kind, payload, slot, stage, job, iter, ntiles, next_ntiles, is_last;
-  uint64_t seq;
+  uint32_t kind, payload, slot, stage, job, iter, ntiles, next_ntiles, is_last, first_stage;
+  uint64_t seq, t_claim, t_ready, t_mma, t_end;   // trace stamps
   // GEMM
-  uint32_t N, nk, idesc, epi, layer, a_mn, b_mn, ncopy_a, ncopy_b, bytes_chunk;
+  uint32_t N, nk, idesc, epi, layer, ncopy_a, ncopy_b, abytes, bbytes;
+  uint32_t n_ech;          // epilogue-input chunks (0 = none)
   OpDesc a, b;
-  // epilogue / elementwise addressing (row block base pointers, translated)
-  uint8_t *out[4];         // output panels (bf16)
-  uint8_t *aux[4];         // EPI_DX: mask panels; SGD/INIT: Wb panels
-  uint8_t *w32[2];         // SGD/INIT: W32 pages
-  uint32_t m0, n0;         // tile origin in logical (row, col) of the output
-  uint32_t rows_valid, cols_valid, ld_logical;   // batch / d for masking & indexing
-  uint64_t key;            // datagen key (T for LOSS, W for INIT, X for GEN)
+  uint8_t *ptr[NPTR];
+  const uint32_t *xt_table[NPTR];
+  uint32_t xt_off[NPTR];
+  uint32_t xt_mask;
+  uint32_t m0, n0;
+  uint32_t rows_valid, cols_valid, ld_logical;
+  uint64_t key;
   float scale, lr;
-  int64_t dump_off;        // float offset, -1 = no dump
+  int64_t dump_off;
 };
 
 struct WorkerSmem {
   uint8_t stage[PIPE][STAGE_BYTES];   // 1024-aligned (first member)
-  uint64_t src[MAX_COPIES];           // translated global addresses of copies
-  uint64_t full[PIPE], empty[PIPE], accum;
+  uint8_t epi_in[2][ECH_BYTES];       // 1024-aligned
+  TileDesc desc[NDESC];
+  uint64_t full[PIPE], empty[PIPE];
+  uint64_t desc_full[NDESC], desc_empty[NDESC];
+  uint64_t acc_full[2], acc_empty[2];
+  uint64_t epi_full[2], epi_empty[2];
+  uint64_t epi_done[NDESC];           // epilogue -> completion warp
   uint32_t tmem_base;
-  uint32_t pub_flag;
-  unsigned long long pub_base;
-  uint64_t tr_claim, tr_ready, tr_mma;   // SALUS_FLAG_TRACE stamps
-  TileDesc td;
+  alignas(16) uint32_t job_cache[128]; // decoder scratch: the task's DevJob (<= 512 B)
 };
+
+static_assert(sizeof(DevJob) <= 512, "DevJob must fit the decoder cache");
 
 __device__ __forceinline__ uint8_t *xlate(const Params &P, const uint32_t *table, uint32_t off) {
   const uint32_t page = table[off >> PAGE_SHIFT];
   return P.arena + ((uint64_t)page << PAGE_SHIFT) + (off & (PAGE_BYTES - 1));
+}
+
+__device__ __forceinline__ void defer(TileDesc &td, uint32_t which, const uint32_t *table, uint32_t off) {
+  td.xt_table[which] = table;
+  td.xt_off[which] = off;
+  td.xt_mask |= 1u << which;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -74,33 +108,40 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   return *reinterpret_cast<uint32_t *>(&h);
 }
 
-// 8 consecutive columns (one 16-byte chunk) of row r in a swizzled panel block
-__device__ __forceinline__ uint4 *panel_chunk(uint8_t *panel_rowblock, uint32_t r, uint32_t chunk) {
-  return reinterpret_cast<uint4 *>(panel_rowblock + r * 128u + (((chunk ^ (r & 7u)) & 7u) << 4));
+// 16-byte chunk (8 columns) `chunk` of row r inside a swizzled panel row block
+__device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t chunk) {
+  return r * 128u + (((chunk ^ (r & 7u)) & 7u) << 4);
+}
+
+__device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // ---------------------------------------------------------------------------
-// Decode a task into a TileDesc (thread 0).  Stage numbering: 0 INIT,
-// 1 GEN, 2..L+1 F_1..F_L, L+2.. B_L..B_1 (salus_dev.h).
+// Decode (lane 0 of the decoder warp, from the smem copy of the DevJob).
+// Stage numbering: 0 INIT, 1 GEN, 2..L+1 F_1..F_L, L+2.. B_L..B_1.
+// Page translations are only recorded here (defer) and resolved by the
+// decoder warp's lanes in parallel.
 // ---------------------------------------------------------------------------
-__device__ void decode_task(const Params &P, uint32_t payload, TileDesc &td) {
+__device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, const Slot &sl,
+                            TileDesc &td) {
   td.payload = payload;
-  if (payload == TASK_EXIT) { td.kind = T_EXIT; return; }
   const uint32_t slot = payload >> 26, stage = (payload >> 21) & 31u, tile = payload & ((1u << 21) - 1);
-  const Slot &sl = P.slots[slot];
-  const uint32_t j = sl.job, k = sl.iter;
-  const DevJob &J = P.jobs[j];
+  const uint32_t k = sl.iter;
   const uint32_t L = J.n_layers, bp = J.bpad;
-  td.slot = slot; td.stage = stage; td.job = j; td.iter = k; td.seq = sl.seq;
+  td.slot = slot; td.stage = stage; td.job = sl.job; td.iter = k; td.seq = sl.seq;
   td.ntiles = J.stage_tiles[stage];
-  const uint32_t ls = last_stage(J.kind, L);
-  td.is_last = stage == ls;
+  td.is_last = stage == last_stage(J.kind, L);
   td.next_ntiles = td.is_last ? 0 : J.stage_tiles[stage + 1];
+  td.first_stage = k == 0 ? 0u : 1u;
   td.dump_off = -1;
+  td.n_ech = 0;
+  td.xt_mask = 0;
+  td.ptr[PTR_W32] = nullptr;
   const uint32_t *lt = P.lpt + (uint64_t)slot * P.lpt_stride;   // lane (ephemeral) space
   const uint32_t *jt = P.ppt + J.pt_off;                        // job (persistent) space
 
-  if (stage == 0) {                                   // INIT weights
+  if (stage == 0) {                                   // INIT weights (128 x 128 blocks)
     td.kind = T_INIT;
     uint32_t t = tile, l = 1;
     for (; l <= L; l++) {
@@ -112,33 +153,32 @@ __device__ void decode_task(const Params &P, uint32_t payload, TileDesc &td) {
     td.layer = l; td.m0 = jb * 128; td.n0 = ib * 128;
     td.rows_valid = J.dims[l]; td.cols_valid = J.dims[l - 1];
     // inference jobs keep only the bf16 copy (2 B/param): no fp32 master
-    td.w32[0] = J.kind == SALUS_TRAIN
-                    ? xlate(P, jt, J.w32_off[l - 1] + (jb * (J.dpad[l - 1] / 4) + 32 * ib) * 2048u)
-                    : nullptr;
+    if (J.kind == SALUS_TRAIN)
+      defer(td, PTR_W32, jt, J.w32_off[l - 1] + (jb * (J.dpad[l - 1] / 4) + 32 * ib) * 2048u);
     for (uint32_t q = 0; q < 2; q++)
-      td.aux[q] = xlate(P, jt, J.wb_off[l - 1][0] + (2 * ib + q) * J.dpad[l] * 128u + jb * 16384u);
+      defer(td, PTR_AUX + q, jt, J.wb_off[l - 1][0] + (2 * ib + q) * J.dpad[l] * 128u + jb * 16384u);
     td.key = gen_key(J.seed, J.job_id, GEN_W, l, 0);
     td.scale = gen_wscale(J.dims[l - 1]);
     return;
   }
-  if (stage == 1) {                                   // GEN input batch X
+  if (stage == 1) {                                   // GEN input batch X (128 x 128 blocks)
     td.kind = T_GEN;
     const uint32_t ncb = J.dpad[0] / 128, mb = tile / ncb, cb = tile % ncb;
     td.m0 = mb * 128; td.n0 = cb * 128;
     td.rows_valid = J.batch; td.cols_valid = J.dims[0];
     for (uint32_t q = 0; q < 2; q++)
-      td.out[q] = xlate(P, lt, J.act_off[0] + (2 * cb + q) * bp * 128u + mb * 16384u);
+      defer(td, PTR_OUT + q, lt, J.act_off[0] + (2 * cb + q) * bp * 128u + mb * 16384u);
     td.key = gen_key(J.seed, J.job_id, GEN_X, 0, k);
     return;
   }
   td.kind = T_GEMM;
   if (stage <= L + 1) {                               // forward F_l
-    const uint32_t l = stage - 1, NT = ntile_for(J.dpad[l]), ntn = J.dpad[l] / NT;
+    const uint32_t l = stage - 1, N = ntile_for(J.dpad[l]), ntn = J.dpad[l] / N;
     const uint32_t mb = tile / ntn, nb = tile % ntn;
-    td.layer = l; td.N = NT; td.nk = J.dpad[l - 1] / 64;
+    td.layer = l; td.N = N; td.nk = J.dpad[l - 1] / 64;
     td.a = OpDesc{lt, J.act_off[l - 1], bp, mb * 128, 0};
-    td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * NT, 0};
-    td.m0 = mb * 128; td.n0 = nb * NT;
+    td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * N, 0};
+    td.m0 = mb * 128; td.n0 = nb * N;
     td.rows_valid = J.batch; td.cols_valid = J.dims[l]; td.ld_logical = J.dims[l];
     uint32_t out_off;
     if (l < L) { td.epi = EPI_RELU; out_off = J.act_off[l]; }
@@ -148,25 +188,28 @@ __device__ void decode_task(const Params &P, uint32_t payload, TileDesc &td) {
     } else { td.epi = EPI_OUT; out_off = J.act_off[L]; }
     if (l == L && (J.dump & SALUS_DUMP_OUTPUTS))
       td.dump_off = (int64_t)(J.dump_out_off + (uint64_t)k * J.batch * J.dims[L]);
-    for (uint32_t q = 0; q < NT / 64; q++)
-      td.out[q] = xlate(P, lt, out_off + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
+    for (uint32_t q = 0; q < N / 64; q++)
+      defer(td, PTR_OUT + q, lt, out_off + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
   } else {                                            // backward B_l
-    const uint32_t l = L - (stage - (L + 2)), NT = ntile_for(J.dpad[l - 1]);
-    const uint32_t ntn = J.dpad[l - 1] / NT, nW = (J.dpad[l] / 128) * ntn;
+    const uint32_t l = L - (stage - (L + 2));
+    const uint32_t N = ntile_for(J.dpad[l - 1]), ntn = J.dpad[l - 1] / N, nW = (J.dpad[l] / 128) * ntn;
     const uint32_t gin = J.g_off[(L - l) & 1], gout = J.g_off[(L - l + 1) & 1];
-    td.layer = l; td.N = NT;
+    td.layer = l; td.N = N;
     if (tile < nW) {                                  // dW_l^T = G_l^T A_{l-1}; SGD
       const uint32_t mb = tile / ntn, nb = tile % ntn;
       td.epi = EPI_SGD; td.nk = bp / 64;
       td.a = OpDesc{lt, gin, bp, mb * 128, 1};
-      td.b = OpDesc{lt, J.act_off[l - 1], bp, nb * NT, 1};
-      td.m0 = mb * 128; td.n0 = nb * NT;
+      td.b = OpDesc{lt, J.act_off[l - 1], bp, nb * N, 1};
+      td.m0 = mb * 128; td.n0 = nb * N;
       td.rows_valid = J.dims[l]; td.cols_valid = J.dims[l - 1]; td.ld_logical = J.dims[l];
       td.lr = J.lr;
-      const uint32_t w32 = J.w32_off[l - 1] + (mb * (J.dpad[l - 1] / 4) + nb * NT / 4) * 2048u;
-      for (uint32_t q = 0; q < NT / 128; q++) td.w32[q] = xlate(P, jt, w32 + q * 65536u);
-      for (uint32_t q = 0; q < NT / 64; q++)
-        td.aux[q] = xlate(P, jt, J.wb_off[l - 1][(k + 1) & 1] + (td.n0 / 64 + q) * J.dpad[l] * 128u + mb * 16384u);
+      // the 128 x N fp32 master tile is N/128 contiguous 64 KiB pages
+      // (j-blocked layout), streamed to the epilogue in 64-column chunks
+      const uint32_t w32 = J.w32_off[l - 1] + (mb * (J.dpad[l - 1] / 4) + nb * N / 4) * 2048u;
+      for (uint32_t q = 0; q < N / 128; q++) defer(td, PTR_W32 + q, jt, w32 + q * 65536u);
+      td.n_ech = N / 64;
+      for (uint32_t q = 0; q < N / 64; q++)
+        defer(td, PTR_AUX + q, jt, J.wb_off[l - 1][(k + 1) & 1] + (td.n0 / 64 + q) * J.dpad[l] * 128u + mb * 16384u);
       if ((J.dump & SALUS_DUMP_WEIGHTS) && k + 1 == J.n_iters) {
         uint64_t base = J.dump_w_off;
         for (uint32_t q = 1; q < l; q++) base += (uint64_t)J.dims[q - 1] * J.dims[q];
@@ -176,19 +219,21 @@ __device__ void decode_task(const Params &P, uint32_t payload, TileDesc &td) {
       const uint32_t u = tile - nW, mb = u / ntn, nb = u % ntn;
       td.epi = EPI_DX; td.nk = J.dpad[l] / 64;
       td.a = OpDesc{lt, gin, bp, mb * 128, 0};
-      td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * NT, 1};
-      td.m0 = mb * 128; td.n0 = nb * NT;
+      td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * N, 1};
+      td.m0 = mb * 128; td.n0 = nb * N;
       td.rows_valid = J.batch; td.cols_valid = J.dims[l - 1];
-      for (uint32_t q = 0; q < NT / 64; q++) {
-        td.out[q] = xlate(P, lt, gout + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
-        td.aux[q] = xlate(P, lt, J.act_off[l - 1] + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
+      for (uint32_t q = 0; q < N / 64; q++) {
+        defer(td, PTR_OUT + q, lt, gout + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
+        defer(td, PTR_EPI + q, lt, J.act_off[l - 1] + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
       }
+      td.n_ech = N / 128;                             // 2 mask panels (32 KiB) per chunk
     }
   }
-  td.a_mn = td.a.mn; td.b_mn = td.b.mn;
+  // A is always M = 128 rows; B is N rows (K-major) or N/64 panels (MN-major)
   td.ncopy_a = td.a.mn ? 2 : 1;
+  td.abytes = td.a.mn ? 8192u : 16384u;
   td.ncopy_b = td.b.mn ? td.N / 64 : td.N / 128;
-  td.bytes_chunk = STAGE_A_BYTES + td.N * 128u;
+  td.bbytes = td.b.mn ? 8192u : 16384u;
   td.idesc = ptx::idesc_bf16(128, td.N, td.a.mn, td.b.mn);
 }
 
@@ -199,39 +244,48 @@ __device__ __forceinline__ uint32_t copy_off(const OpDesc &o, uint32_t kc, uint3
 }
 
 // ---------------------------------------------------------------------------
-// Epilogues: thread r of the 4 epilogue warps owns accumulator row r
-// (TMEM lane r); columns are drained 32 at a time.
+// Epilogue over accumulator column blocks [cc0, cc1) (32 columns each):
+// thread r of the 4 epilogue warps owns accumulator row r (TMEM lane r, warp
+// % 4 = lane quarter).  `buf` is the smem epilogue-input chunk holding the
+// W32 columns [32*cc0, +64) (SGD) or the mask columns [32*cc0, +128) (DX).
 // ---------------------------------------------------------------------------
-__device__ void epilogue(const Params &P, const TileDesc &td, uint32_t tmem, uint32_t r) {
+struct EpiView {   // register copy of the descriptor fields the epilogue uses
+  uint32_t m0, n0, rows_valid, cols_valid, ld_logical, epi;
+  float lr;
+  uint64_t key;
+  int64_t dump_off;
+};
+
+__device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiView &td, uint32_t tacc,
+                              uint32_t r, uint32_t cc0, uint32_t cc1, const uint8_t *buf) {
   const uint32_t qw = r >> 5;
   const uint32_t row = td.m0 + r;
   const bool row_ok = row < td.rows_valid;
   float *dump = td.dump_off >= 0 ? P.dump + td.dump_off : nullptr;
-  for (uint32_t cc = 0; cc < td.N / 32; cc++) {
+#pragma unroll 1
+  for (uint32_t cc = cc0; cc < cc1; cc++) {
     uint32_t raw[32];
-    ptx::tmem_ld32(tmem + ((qw * 32u) << 16) + cc * 32u, raw);
+    ptx::tmem_ld32(tacc + ((qw * 32u) << 16) + cc * 32u, raw);
     ptx::tmem_ld_wait();
     float v[32];
 #pragma unroll
     for (int x = 0; x < 32; x++) v[x] = __uint_as_float(raw[x]);
     const uint32_t col0 = td.n0 + cc * 32;
-    uint8_t *ob = td.out[cc >> 1];
-    const uint32_t ch0 = (cc & 1) * 4;
+    const uint32_t pan = cc >> 1, ch0 = (cc & 1) * 4;
     if (td.epi == EPI_SGD) {
       // rows are j (d_l), columns i (d_{l-1}): W32[j][i] -= lr * dW^T[j][i]
-      uint8_t *wp = td.w32[cc >> 2];
 #pragma unroll
       for (int g = 0; g < 8; g++) {
-        float4 *a = reinterpret_cast<float4 *>(wp + (((cc * 8 + g) & 31u) * 2048u) + r * 16u);
-        float4 w = *a;
+        const uint32_t grp = cc * 8 + g;                    // float4 column group in the tile
+        float4 w = *reinterpret_cast<const float4 *>(buf + ((cc - cc0) * 8 + g) * 2048u + r * 16u);
         w.x = fmaf(-td.lr, v[4 * g + 0], w.x);
         w.y = fmaf(-td.lr, v[4 * g + 1], w.y);
         w.z = fmaf(-td.lr, v[4 * g + 2], w.z);
         w.w = fmaf(-td.lr, v[4 * g + 3], w.w);
-        *a = w;
+        *reinterpret_cast<float4 *>(tds.ptr[PTR_W32 + (grp >> 5)] + (grp & 31u) * 2048u + r * 16u) = w;
         v[4 * g + 0] = w.x; v[4 * g + 1] = w.y; v[4 * g + 2] = w.z; v[4 * g + 3] = w.w;
       }
-      uint8_t *wb = td.aux[cc >> 1];
+      uint8_t *aux = tds.ptr[PTR_AUX + pan];
 #pragma unroll
       for (int q = 0; q < 4; q++) {
         uint4 u;
@@ -239,7 +293,7 @@ __device__ void epilogue(const Params &P, const TileDesc &td, uint32_t tmem, uin
         u.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
         u.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
         u.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-        *panel_chunk(wb, r, ch0 + q) = u;
+        *reinterpret_cast<uint4 *>(aux + swz(r, ch0 + q)) = u;
       }
       if (dump && row_ok) {                     // W[i][j], logical d_{l-1} x d_l
         for (int x = 0; x < 32; x++)
@@ -248,16 +302,16 @@ __device__ void epilogue(const Params &P, const TileDesc &td, uint32_t tmem, uin
       continue;
     }
     if (td.epi == EPI_DX) {
-      uint8_t *mb = td.aux[cc >> 1];
+      const uint8_t *mp = buf + ((cc - cc0) >> 1) * 16384u;
 #pragma unroll
       for (int q = 0; q < 4; q++) {
-        const uint4 m = *panel_chunk(mb, r, ch0 + q);
+        const uint4 m = *reinterpret_cast<const uint4 *>(mp + swz(r, ch0 + q));
         const uint32_t w[4] = {m.x, m.y, m.z, m.w};
 #pragma unroll
-        for (int h = 0; h < 4; h++) {
-          const uint32_t lo = w[h] & 0xFFFFu, hi = w[h] >> 16;
-          if (!((lo & 0x8000u) == 0 && (lo & 0x7FFFu) != 0)) v[8 * q + 2 * h] = 0.f;
-          if (!((hi & 0x8000u) == 0 && (hi & 0x7FFFu) != 0)) v[8 * q + 2 * h + 1] = 0.f;
+        for (int hh = 0; hh < 4; hh++) {
+          const uint32_t lo = w[hh] & 0xFFFFu, hi = w[hh] >> 16;
+          if (!((lo & 0x8000u) == 0 && (lo & 0x7FFFu) != 0)) v[8 * q + 2 * hh] = 0.f;
+          if (!((hi & 0x8000u) == 0 && (hi & 0x7FFFu) != 0)) v[8 * q + 2 * hh + 1] = 0.f;
         }
       }
     } else {
@@ -272,19 +326,19 @@ __device__ void epilogue(const Params &P, const TileDesc &td, uint32_t tmem, uin
 #pragma unroll
         for (int x = 0; x < 32; x++) v[x] = row_ok ? v[x] : 0.f;
       } else {  // EPI_LOSS: G_L = (A_L - T) / B  (MSE)
-        const float fb = (float)td.rows_valid;
-#pragma unroll 4
+        // branch-free so the 32 independent hash chains interleave (ILP)
+        const float inv_b = 1.0f / (float)td.rows_valid;
+        const uint64_t key = td.key, base = (uint64_t)row * td.ld_logical + col0;
+        const int ncol = row_ok ? (int)td.cols_valid - (int)col0 : 0;
+#pragma unroll
         for (int x = 0; x < 32; x++) {
-          const uint32_t col = col0 + x;
-          if (row_ok && col < td.cols_valid) {
-            const float tv = gen_value(td.key, (uint64_t)row * td.ld_logical + col, 1.0f);
-            v[x] = __fdiv_rn(v[x] - tv, fb);
-          } else {
-            v[x] = 0.f;
-          }
+          const float tv = gen_value(key, base + x, 1.0f);
+          const float gl = (v[x] - tv) * inv_b;
+          v[x] = x < ncol ? gl : 0.f;
         }
       }
     }
+    uint8_t *out = tds.ptr[PTR_OUT + pan];
 #pragma unroll
     for (int q = 0; q < 4; q++) {
       uint4 u;
@@ -292,49 +346,324 @@ __device__ void epilogue(const Params &P, const TileDesc &td, uint32_t tmem, uin
       u.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
       u.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
       u.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-      *panel_chunk(ob, r, ch0 + q) = u;
+      *reinterpret_cast<uint4 *>(out + swz(r, ch0 + q)) = u;
     }
   }
 }
 
 // INIT: W_l block (rows j = m0 + r of W^T storage, 128 columns i)
 __device__ void init_tile(const TileDesc &td, uint32_t r) {
-  const uint32_t j = td.m0 + r;
+  // descriptor fields in registers: global stores below may alias smem for
+  // the compiler, which would otherwise reload them after every store
+  const uint32_t j = td.m0 + r, n0 = td.n0, rows = td.rows_valid, cols = td.cols_valid;
+  const uint64_t key = td.key;
+  const float scale = td.scale;
+  uint8_t *const w32 = td.ptr[PTR_W32];
+  uint8_t *const aux0 = td.ptr[PTR_AUX], *const aux1 = td.ptr[PTR_AUX + 1];
+  const int ncol = j < rows ? (int)cols - (int)n0 : 0;
+#pragma unroll 2
   for (uint32_t cg = 0; cg < 128; cg += 8) {
     float v[8];
 #pragma unroll
     for (int x = 0; x < 8; x++) {
-      const uint32_t i = td.n0 + cg + x;
-      v[x] = (j < td.rows_valid && i < td.cols_valid)
-                 ? gen_value(td.key, (uint64_t)i * td.rows_valid + j, td.scale) : 0.f;
+      const uint32_t i = n0 + cg + x;
+      const float g = gen_value(key, (uint64_t)i * rows + j, scale);
+      v[x] = (int)(cg + x) < ncol ? g : 0.f;
     }
     // W32 j-blocked layout: ((j/128)*(dp_in/4) + i/4)*2048 + (j%128)*16 + (i%4)*4
-    if (td.w32[0]) {
-      *reinterpret_cast<float4 *>(td.w32[0] + ((cg / 4) * 2048u) + r * 16u) = make_float4(v[0], v[1], v[2], v[3]);
-      *reinterpret_cast<float4 *>(td.w32[0] + ((cg / 4 + 1) * 2048u) + r * 16u) = make_float4(v[4], v[5], v[6], v[7]);
+    if (w32) {
+      *reinterpret_cast<float4 *>(w32 + (cg / 4) * 2048u + r * 16u) = make_float4(v[0], v[1], v[2], v[3]);
+      *reinterpret_cast<float4 *>(w32 + (cg / 4 + 1) * 2048u + r * 16u) = make_float4(v[4], v[5], v[6], v[7]);
     }
     uint4 u;
     u.x = pack_bf16x2(v[0], v[1]); u.y = pack_bf16x2(v[2], v[3]);
     u.z = pack_bf16x2(v[4], v[5]); u.w = pack_bf16x2(v[6], v[7]);
-    *panel_chunk(td.aux[cg / 64], r, (cg % 64) / 8) = u;
+    *reinterpret_cast<uint4 *>((cg < 64 ? aux0 : aux1) + swz(r, (cg % 64) / 8)) = u;
   }
 }
 
 // GEN: X block (rows m = m0 + r, 128 columns)
 __device__ void gen_tile(const TileDesc &td, uint32_t r) {
-  const uint32_t m = td.m0 + r;
+  const uint32_t m = td.m0 + r, n0 = td.n0, cols = td.cols_valid;
+  const uint64_t key = td.key, base = (uint64_t)m * cols + n0;
+  uint8_t *const out0 = td.ptr[PTR_OUT], *const out1 = td.ptr[PTR_OUT + 1];
+  const int ncol = m < td.rows_valid ? (int)cols - (int)n0 : 0;
+#pragma unroll 2
   for (uint32_t cg = 0; cg < 128; cg += 8) {
     float v[8];
 #pragma unroll
     for (int x = 0; x < 8; x++) {
-      const uint32_t c = td.n0 + cg + x;
-      v[x] = (m < td.rows_valid && c < td.cols_valid)
-                 ? gen_value(td.key, (uint64_t)m * td.cols_valid + c, 1.0f) : 0.f;
+      const float g = gen_value(key, base + cg + x, 1.0f);
+      v[x] = (int)(cg + x) < ncol ? g : 0.f;
     }
     uint4 u;
     u.x = pack_bf16x2(v[0], v[1]); u.y = pack_bf16x2(v[2], v[3]);
     u.z = pack_bf16x2(v[4], v[5]); u.w = pack_bf16x2(v[6], v[7]);
-    *panel_chunk(td.out[cg / 64], r, (cg % 64) / 8) = u;
+    *reinterpret_cast<uint4 *>((cg < 64 ? out0 : out1) + swz(r, (cg % 64) / 8)) = u;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Roles
+// ---------------------------------------------------------------------------
+__device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
+  uint32_t d = 0, d_phase = 0;
+  for (;;) {
+    ptx::mbar_wait_abortable(&W.desc_empty[d], d_phase ^ 1, &P.ctrl->abort);
+    TileDesc &td = W.desc[d];
+    uint32_t payload = TASK_EXIT;
+    uint64_t t_claim = 0;
+    if (lane == 0) {
+      const unsigned long long pos = atomicAdd(&P.ctrl->q_tail, 1ull);
+      uint32_t spins = 0;
+      for (;;) {
+        const unsigned long long v = ptx::ld_acquire_u64(&P.ring[pos & P.ring_mask]);
+        if ((uint32_t)(v >> 32) == (uint32_t)(pos + 1)) { payload = (uint32_t)v; break; }
+        if ((++spins & 255) == 0 && *(volatile uint32_t *)&P.ctrl->abort) break;
+      }
+      t_claim = ptx::globaltimer();
+    }
+    payload = __shfl_sync(0xffffffffu, payload, 0);
+    __syncwarp();   // lane 0's acquire orders the other lanes' reads below
+    if (payload == TASK_EXIT) {
+      if (lane == 0) {
+        td.kind = T_EXIT;
+        td.payload = TASK_EXIT;
+        ptx::mbar_arrive(&W.desc_full[d]);
+      }
+      break;
+    }
+    const Slot &sl = P.slots[payload >> 26];
+    const uint32_t j = *(volatile const uint32_t *)&sl.job;
+    const uint32_t *src = reinterpret_cast<const uint32_t *>(P.jobs + j);
+    for (uint32_t x = lane; x < sizeof(DevJob) / 4; x += 32) W.job_cache[x] = src[x];
+    __syncwarp();
+    if (lane == 0) {
+      decode_task(P, payload, *reinterpret_cast<const DevJob *>(W.job_cache), sl, td);
+      td.t_claim = t_claim;
+    }
+    __syncwarp();
+    if (lane < NPTR && ((td.xt_mask >> lane) & 1u)) td.ptr[lane] = xlate(P, td.xt_table[lane], td.xt_off[lane]);
+    __syncwarp();
+    if (lane == 0) {
+      if (td.stage == td.first_stage)
+        atomicMin((unsigned long long *)&P.slots[td.slot].start_ns, (unsigned long long)ptx::globaltimer());
+      ptx::fence_proxy_async_global();
+      ptx::mbar_arrive(&W.desc_full[d]);
+    }
+    __syncwarp();
+    if (++d == NDESC) { d = 0; d_phase ^= 1; }
+  }
+}
+
+__device__ void operand_loader(const Params &P, WorkerSmem &W) {
+  uint32_t d = 0, d_phase = 0, s = 0, s_phase = 0;
+  for (;;) {
+    ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
+    const TileDesc &td = W.desc[d];
+    if (td.kind == T_EXIT) break;
+    if (td.kind == T_GEMM) {
+      const OpDesc a = td.a, b = td.b;
+      const uint32_t nk = td.nk, nca = td.ncopy_a, ncb = td.ncopy_b, ab = td.abytes, bb = td.bbytes;
+      const uint32_t tx = nca * ab + ncb * bb;
+      for (uint32_t kc = 0; kc < nk; kc++) {
+        ptx::mbar_wait_abortable(&W.empty[s], s_phase ^ 1, &P.ctrl->abort);
+        ptx::mbar_arrive_expect_tx(&W.full[s], tx);
+        uint8_t *sa = W.stage[s], *sb = W.stage[s] + STAGE_A_BYTES;
+        for (uint32_t q = 0; q < nca; q++)
+          ptx::bulk_g2s(sa + q * ab, xlate(P, a.table, copy_off(a, kc, q)), ab, &W.full[s]);
+        for (uint32_t q = 0; q < ncb; q++)
+          ptx::bulk_g2s(sb + q * bb, xlate(P, b.table, copy_off(b, kc, q)), bb, &W.full[s]);
+        if (++s == PIPE) { s = 0; s_phase ^= 1; }
+      }
+    }
+    ptx::mbar_arrive(&W.desc_empty[d]);
+    if (++d == NDESC) { d = 0; d_phase ^= 1; }
+  }
+}
+
+// Streams a tile's epilogue input in 32 KiB chunks: SGD chunk c = W32 columns
+// [64c, 64c+64) (half of a 64 KiB page); DX chunk c = mask panels 2c, 2c+1.
+__device__ void epi_loader(const Params &P, WorkerSmem &W) {
+  uint32_t d = 0, d_phase = 0, e = 0, e_phase = 0;
+  for (;;) {
+    ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
+    const TileDesc &td = W.desc[d];
+    if (td.kind == T_EXIT) break;
+    if (td.kind == T_GEMM) {
+      const uint32_t n = td.n_ech;
+      const bool sgd = td.epi == EPI_SGD;
+      for (uint32_t c = 0; c < n; c++) {
+        ptx::mbar_wait_abortable(&W.epi_empty[e], e_phase ^ 1, &P.ctrl->abort);
+        ptx::mbar_arrive_expect_tx(&W.epi_full[e], ECH_BYTES);
+        if (sgd) {
+          ptx::bulk_g2s(W.epi_in[e], td.ptr[PTR_W32 + (c >> 1)] + (c & 1) * 32768u, ECH_BYTES, &W.epi_full[e]);
+        } else {
+          ptx::bulk_g2s(W.epi_in[e], td.ptr[PTR_EPI + 2 * c], 16384u, &W.epi_full[e]);
+          ptx::bulk_g2s(W.epi_in[e] + 16384u, td.ptr[PTR_EPI + 2 * c + 1], 16384u, &W.epi_full[e]);
+        }
+        if (++e == 2) { e = 0; e_phase ^= 1; }
+      }
+    }
+    ptx::mbar_arrive(&W.desc_empty[d]);
+    if (++d == NDESC) { d = 0; d_phase ^= 1; }
+  }
+}
+
+__device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
+  uint32_t d = 0, d_phase = 0, s = 0, s_phase = 0, b = 0, b_phase = 0;
+  for (;;) {
+    ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
+    const TileDesc &td = W.desc[d];
+    if (td.kind == T_EXIT) break;
+    if (td.kind == T_GEMM) {
+      ptx::mbar_wait_abortable(&W.acc_empty[b], b_phase ^ 1, &P.ctrl->abort);
+      ptx::tc_fence_after();
+      const uint32_t tacc = tmem + b * ACC_COLS, idesc = td.idesc, nk = td.nk;
+      const uint32_t a_lbo = td.a.mn ? 8192u : 16u, b_lbo = td.b.mn ? 8192u : 16u;
+      const uint32_t a_step = td.a.mn ? 2048u : 32u, b_step = td.b.mn ? 2048u : 32u;
+      for (uint32_t kc = 0; kc < nk; kc++) {
+        ptx::mbar_wait_abortable(&W.full[s], s_phase, &P.ctrl->abort);
+        ptx::tc_fence_after();
+        const uint32_t sa = ptx::smem_u32(W.stage[s]), sb = sa + STAGE_A_BYTES;
+#pragma unroll
+        for (uint32_t ks = 0; ks < 4; ks++) {
+          const uint64_t ad = ptx::smem_desc_sw128(sa + ks * a_step, a_lbo, 1024);
+          const uint64_t bd = ptx::smem_desc_sw128(sb + ks * b_step, b_lbo, 1024);
+          ptx::mma_bf16(tacc, ad, bd, idesc, (kc | ks) != 0);
+        }
+        ptx::mma_commit(&W.empty[s]);
+        if (++s == PIPE) { s = 0; s_phase ^= 1; }
+      }
+      ptx::mma_commit(&W.acc_full[b]);
+      if (++b == 2) { b = 0; b_phase ^= 1; }
+    }
+    ptx::mbar_arrive(&W.desc_empty[d]);
+    if (++d == NDESC) { d = 0; d_phase ^= 1; }
+  }
+}
+
+__device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, uint32_t tid,
+                               unsigned long long &my_tasks) {
+  const uint32_t warp = tid >> 5, lane = tid & 31;
+  const uint32_t r = ((warp & 3u) << 5) | lane;   // TMEM lane quarter = warp % 4
+  const uint32_t et = tid - 32 * EPI_WARP0;       // 0..EPI_THREADS-1
+  uint32_t d = 0, d_phase = 0, b = 0, b_phase = 0, e = 0, e_phase = 0;
+  for (;;) {
+    ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
+    const TileDesc &td = W.desc[d];
+    if (td.kind == T_EXIT) break;
+    my_tasks++;
+    const uint64_t t_ready = ptx::globaltimer();
+    uint64_t t_mma = t_ready;
+    if (td.kind == T_GEMM) {
+      const EpiView ev = {td.m0, td.n0, td.rows_valid, td.cols_valid, td.ld_logical, td.epi, td.lr, td.key,
+                          td.dump_off};
+      const uint32_t ncc = td.N / 32, n = td.n_ech;
+      ptx::mbar_wait_abortable(&W.acc_full[b], b_phase, &P.ctrl->abort);
+      ptx::tc_fence_after();
+      t_mma = ptx::globaltimer();
+      const uint32_t tacc = tmem + b * ACC_COLS;
+      if (n == 0) {
+        epilogue_cols(P, td, ev, tacc, r, 0, ncc, nullptr);
+      } else {
+        const uint32_t per = ncc / n;                 // column blocks per input chunk
+        for (uint32_t c = 0; c < n; c++) {
+          ptx::mbar_wait_abortable(&W.epi_full[e], e_phase, &P.ctrl->abort);
+          epilogue_cols(P, td, ev, tacc, r, c * per, (c + 1) * per, W.epi_in[e]);
+          named_bar(1, EPI_THREADS);                  // every thread is done with this chunk
+          if (et == 0) ptx::mbar_arrive(&W.epi_empty[e]);
+          if (++e == 2) { e = 0; e_phase ^= 1; }
+        }
+      }
+      ptx::tc_fence_before();
+      named_bar(1, EPI_THREADS);
+      if (et == 0) ptx::mbar_arrive(&W.acc_empty[b]);
+      if (++b == 2) { b = 0; b_phase ^= 1; }
+    } else if (td.kind == T_INIT) {
+      init_tile(td, r);
+    } else {
+      gen_tile(td, r);
+    }
+    // hand the tile to the completion warp: all epilogue stores are issued
+    // before the CTA barrier; the completion thread's gpu-scope fence after
+    // the mbarrier handoff is cumulative over them (the grid-sync pattern)
+    ptx::fence_proxy_async_global();
+    named_bar(1, EPI_THREADS);
+    if (et == 0) {
+      W.desc[d].t_ready = t_ready; W.desc[d].t_mma = t_mma; W.desc[d].t_end = ptx::globaltimer();
+      ptx::mbar_arrive(&W.epi_done[d]);
+    }
+    if (++d == NDESC) { d = 0; d_phase ^= 1; }
+  }
+}
+
+// Completion warp: per tile, in order — fence, stage counter, and publication
+// of the next stage's tiles or (last stage) the slot's next iteration.
+__device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
+  uint32_t d = 0, d_phase = 0;
+  for (;;) {
+    ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
+    const TileDesc &td = W.desc[d];
+    if (td.kind == T_EXIT) break;
+    ptx::mbar_wait_abortable(&W.epi_done[d], d_phase, &P.ctrl->abort);
+    uint32_t pub = 0, ps = 0, pst = 0, pn = 0;
+    unsigned long long pb = 0;
+    if (lane == 0) {
+      __threadfence();
+      if (P.flags & SALUS_FLAG_TRACE) {
+        const unsigned long long i = atomicAdd(&P.ctrl->n_trace, 1ull);
+        if (i < P.trace_cap) {
+          uint32_t smid;
+          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+          salus_trace_rec t;
+          t.task = td.payload; t.smid = smid; t.job = td.job; t.iter = td.iter;
+          t.t_claim = td.t_claim; t.t_ready = td.t_ready; t.t_mma = td.t_mma; t.t_end = td.t_end;
+          P.trace[i] = t;
+        }
+      }
+      Slot &sl = P.slots[td.slot];
+      const uint32_t old = ptx::atom_add_acqrel_u32(&sl.stage_done[td.stage], 1u);
+      if (old + 1 == td.ntiles) {
+        if (td.is_last) {                      // the iteration is physically complete
+          const uint64_t end = ptx::globaltimer(), start = sl.start_ns;
+          sl.end_ns = end;
+          const DevJob &J = P.jobs[td.job];
+          if ((P.flags & SALUS_FLAG_LOG) && td.seq < P.log_cap) {
+            salus_wall_rec w;
+            w.seq = td.seq; w.lane = sl.lane_id; w.job = J.job_id; w.start_ns = start; w.end_ns = end;
+            P.wall[td.seq] = w;
+          }
+          if (td.iter == 0) P.stats[td.job].wall_start_ns = start;
+          if (td.iter + 1 == J.n_iters) P.stats[td.job].wall_end_ns = end;
+          ptx::st_release_u64(&sl.done_seq, td.seq + 1);
+          // run-ahead: start the slot's next queued iteration right here
+          DispRec rec;
+          if (take_next(sl, &rec)) {
+            pst = begin_iteration(sl, rec);
+            pub = 1; ps = td.slot; pn = P.jobs[rec.job].stage_tiles[pst];
+            pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)pn);
+          }
+        } else {
+          pub = 1; ps = td.slot; pst = td.stage + 1; pn = td.next_ntiles;
+          pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)pn);
+        }
+      }
+    }
+    pub = __shfl_sync(0xffffffffu, pub, 0);
+    if (pub) {                                 // publish the next tiles (32 lanes)
+      ps = __shfl_sync(0xffffffffu, ps, 0);
+      pst = __shfl_sync(0xffffffffu, pst, 0);
+      pn = __shfl_sync(0xffffffffu, pn, 0);
+      pb = __shfl_sync(0xffffffffu, pb, 0);
+      for (uint32_t x = lane; x < pn; x += 32) {
+        const unsigned long long pos = pb + x;
+        ptx::st_release_u64(&P.ring[pos & P.ring_mask], ((pos + 1) << 32) | task_pack(ps, pst, x));
+      }
+    }
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&W.desc_empty[d]);
+    if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
 }
 
@@ -345,7 +674,17 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
 
   if (tid == 0) {
     for (uint32_t s = 0; s < PIPE; s++) { ptx::mbar_init(&W.full[s], 1); ptx::mbar_init(&W.empty[s], 1); }
-    ptx::mbar_init(&W.accum, 1);
+    // a descriptor is released by its 4 consumers: operand loader, epilogue-
+    // input loader, MMA thread, completion warp (after the epilogue is done)
+    for (uint32_t d = 0; d < NDESC; d++) {
+      ptx::mbar_init(&W.desc_full[d], 1);
+      ptx::mbar_init(&W.desc_empty[d], 4);
+      ptx::mbar_init(&W.epi_done[d], 1);
+    }
+    for (uint32_t b = 0; b < 2; b++) {
+      ptx::mbar_init(&W.acc_full[b], 1); ptx::mbar_init(&W.acc_empty[b], 1);
+      ptx::mbar_init(&W.epi_full[b], 1); ptx::mbar_init(&W.epi_empty[b], 1);
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 2) { ptx::tmem_alloc(&W.tmem_base, TMEM_COLS); ptx::tmem_relinquish(); }
@@ -353,136 +692,24 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = W.tmem_base;
-
-  uint32_t p_stage = 0, p_phase = 0;     // producer ring position (warp 0 lane 0)
-  uint32_t m_stage = 0, m_phase = 0;     // MMA ring position (warp 1 lane 0)
-  uint32_t acc_phase = 0;
   unsigned long long my_tasks = 0;
 
-  for (;;) {
-    __syncthreads();
-    if (tid == 0) {
-      const unsigned long long pos = atomicAdd(&P.ctrl->q_tail, 1ull);
-      uint32_t payload = TASK_EXIT;
-      uint32_t spins = 0;
-      for (;;) {
-        const unsigned long long v = ptx::ld_acquire_u64(&P.ring[pos & P.ring_mask]);
-        if ((uint32_t)(v >> 32) == (uint32_t)(pos + 1)) { payload = (uint32_t)v; break; }
-        if ((++spins & 255) == 0 && *(volatile uint32_t *)&P.ctrl->abort) break;
-      }
-      W.tr_claim = ptx::globaltimer();
-      decode_task(P, payload, W.td);
-      if (W.td.kind != T_EXIT) {
-        const uint32_t first = W.td.iter == 0 ? 0u : 1u;
-        if (W.td.stage == first) atomicMin((unsigned long long *)&P.slots[W.td.slot].start_ns,
-                                           (unsigned long long)ptx::globaltimer());
-      }
+  if (warp == 0) {
+    decoder_warp(P, W, lane);
+  } else if (warp < EPI_WARP0) {
+    if (lane == 0) {
+      if (warp == 1) operand_loader(P, W);
+      else if (warp == 2) mma_thread(P, W, tmem);
+      else epi_loader(P, W);
     }
-    __syncthreads();
-    const TileDesc &td = W.td;
-    if (td.kind == T_EXIT) break;
-    my_tasks++;
-
-    if (td.kind == T_GEMM) {
-      const uint32_t nc = td.ncopy_a + td.ncopy_b, total = td.nk * nc;
-      if (warp == 0) {
-        for (uint32_t x = lane; x < total; x += 32) {
-          const uint32_t kc = x / nc, q = x % nc;
-          const OpDesc &o = q < td.ncopy_a ? td.a : td.b;
-          const uint32_t qq = q < td.ncopy_a ? q : q - td.ncopy_a;
-          W.src[x] = reinterpret_cast<uint64_t>(xlate(P, o.table, copy_off(o, kc, qq)));
-        }
-      }
-      __syncthreads();
-      if (tid == 0) W.tr_ready = ptx::globaltimer();
-      if (warp == 0 && lane == 0) {
-        ptx::fence_proxy_async_global();
-        const uint32_t abytes = td.a_mn ? 8192u : 16384u, bbytes = td.b_mn ? 8192u : 16384u;
-        for (uint32_t kc = 0; kc < td.nk; kc++) {
-          ptx::mbar_wait_abortable(&W.empty[p_stage], p_phase ^ 1, &P.ctrl->abort);
-          ptx::mbar_arrive_expect_tx(&W.full[p_stage], td.bytes_chunk);
-          uint8_t *sa = W.stage[p_stage], *sb = W.stage[p_stage] + STAGE_A_BYTES;
-          for (uint32_t q = 0; q < td.ncopy_a; q++)
-            ptx::bulk_g2s(sa + q * abytes, reinterpret_cast<void *>(W.src[kc * nc + q]), abytes, &W.full[p_stage]);
-          for (uint32_t q = 0; q < td.ncopy_b; q++)
-            ptx::bulk_g2s(sb + q * bbytes, reinterpret_cast<void *>(W.src[kc * nc + td.ncopy_a + q]), bbytes,
-                          &W.full[p_stage]);
-          if (++p_stage == PIPE) { p_stage = 0; p_phase ^= 1; }
-        }
-      } else if (warp == 1 && lane == 0) {
-        const uint32_t a_lbo = td.a_mn ? 8192u : 16u, b_lbo = td.b_mn ? 8192u : 16u;
-        const uint32_t a_step = td.a_mn ? 2048u : 32u, b_step = td.b_mn ? 2048u : 32u;
-        for (uint32_t kc = 0; kc < td.nk; kc++) {
-          ptx::mbar_wait_abortable(&W.full[m_stage], m_phase, &P.ctrl->abort);
-          ptx::tc_fence_after();
-          const uint32_t sa = ptx::smem_u32(W.stage[m_stage]), sb = sa + STAGE_A_BYTES;
-#pragma unroll
-          for (uint32_t ks = 0; ks < 4; ks++) {
-            const uint64_t ad = ptx::smem_desc_sw128(sa + ks * a_step, a_lbo, 1024);
-            const uint64_t bd = ptx::smem_desc_sw128(sb + ks * b_step, b_lbo, 1024);
-            ptx::mma_bf16(tmem, ad, bd, td.idesc, (kc | ks) != 0);
-          }
-          ptx::mma_commit(&W.empty[m_stage]);
-          if (++m_stage == PIPE) { m_stage = 0; m_phase ^= 1; }
-        }
-        ptx::mma_commit(&W.accum);
-      } else if (warp >= 2) {
-        ptx::mbar_wait_abortable(&W.accum, acc_phase, &P.ctrl->abort);
-        ptx::tc_fence_after();
-        if (tid == 64) W.tr_mma = ptx::globaltimer();
-        // a warp may only touch TMEM lanes [32*(warp%4), +32): warps 2,3,4,5
-        // own accumulator rows 64-95, 96-127, 0-31, 32-63
-        epilogue(P, td, tmem, ((warp & 3u) << 5) | lane);
-      }
-      acc_phase ^= 1;
-    } else if (warp >= 2) {
-      if (tid == 64) { W.tr_ready = W.tr_claim; W.tr_mma = ptx::globaltimer(); }
-      if (td.kind == T_INIT) init_tile(td, ((warp & 3u) << 5) | lane);
-      else gen_tile(td, ((warp & 3u) << 5) | lane);
-    }
-    if (warp >= 2) {
-      __threadfence();
-      ptx::fence_proxy_async_global();
-      ptx::tc_fence_before();
-    }
-    __syncthreads();
-    if (tid == 0) {
-      if (P.flags & SALUS_FLAG_TRACE) {
-        const unsigned long long i = atomicAdd(&P.ctrl->n_trace, 1ull);
-        if (i < P.trace_cap) {
-          uint32_t smid;
-          asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
-          salus_trace_rec t;
-          t.task = td.payload; t.smid = smid; t.job = td.job; t.iter = td.iter;
-          t.t_claim = W.tr_claim; t.t_ready = W.tr_ready; t.t_mma = W.tr_mma; t.t_end = ptx::globaltimer();
-          P.trace[i] = t;
-        }
-      }
-      Slot &sl = P.slots[td.slot];
-      const uint32_t old = ptx::atom_add_acqrel_u32(&sl.stage_done[td.stage], 1u);
-      W.pub_flag = 0;
-      if (old + 1 == td.ntiles) {
-        if (td.is_last) {
-          sl.end_ns = ptx::globaltimer();
-          ptx::st_release_u64(&sl.done_seq, td.seq + 1);
-        } else {
-          W.pub_flag = 1;
-          W.pub_base = atomicAdd(&P.ctrl->q_head, (unsigned long long)td.next_ntiles);
-        }
-      }
-    }
-    __syncthreads();
-    if (W.pub_flag) {                          // publish the next stage's tiles
-      const unsigned long long b0 = W.pub_base;
-      for (uint32_t x = tid; x < td.next_ntiles; x += WORKER_THREADS) {
-        const unsigned long long pos = b0 + x;
-        ptx::st_release_u64(&P.ring[pos & P.ring_mask],
-                            ((pos + 1) << 32) | task_pack(td.slot, td.stage + 1, x));
-      }
-    }
+    __syncwarp();
+  } else if (warp < DONE_WARP) {
+    epilogue_warps(P, W, tmem, tid, my_tasks);
+  } else {
+    completion_warp(P, W, lane);
   }
-  if (tid == 0) atomicAdd(&P.ctrl->n_tasks, my_tasks);
   __syncthreads();
+  if (tid == 32 * EPI_WARP0) atomicAdd(&P.ctrl->n_tasks, my_tasks);
   if (warp == 2) ptx::tmem_dealloc(tmem, TMEM_COLS);
 }
 

@@ -15,7 +15,7 @@ from typing import Dict, Iterable, List, Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libsalus.so")
+LIB_PATH = os.environ.get("SALUS_LIB", os.path.join(HERE, "libsalus.so"))
 
 FIFO, SRTF, PACK, FAIR = 0, 1, 2, 3
 TRAIN, INFER = 0, 1

@@ -34,3 +34,19 @@ base = sub["t_claim"].min()
 print("timeline of one iteration (us from first claim): stage tile claim ready mma end sm")
 for r in sub:
     print(f"  s{(r['task'] >> 21) & 31:2d} t{r['task'] & 0x1FFFFF:4d} {(r['t_claim'] - base) / 1e3:8.2f} {(r['t_ready'] - base) / 1e3:8.2f} {(r['t_mma'] - base) / 1e3:8.2f} {(r['t_end'] - base) / 1e3:8.2f} sm{r['smid']}")
+# SM busy fraction: per SM, union of [t_ready, t_end] intervals / kernel span
+span = (tr["t_end"].max() - tr["t_claim"].min())
+busy = 0
+for sm in np.unique(tr["smid"]):
+    m = tr["smid"] == sm
+    iv = sorted(zip(tr["t_ready"][m].tolist(), tr["t_end"][m].tolist()))
+    cur_s, cur_e, tot = None, None, 0
+    for s_, e_ in iv:
+        if cur_e is None or s_ > cur_e:
+            if cur_e is not None: tot += cur_e - cur_s
+            cur_s, cur_e = s_, e_
+        else:
+            cur_e = max(cur_e, e_)
+    tot += cur_e - cur_s
+    busy += tot
+print(f"SM busy fraction (epilogue-side, union of tile intervals): {busy / (span * len(np.unique(tr['smid']))):.3f} over {span / 1e6:.2f} ms")
