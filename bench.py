@@ -30,7 +30,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from workloads import (TRAIN, algorithmic_bytes, algorithmic_flops, c2_trace,  # noqa: E402
-                       partition)
+                       c3_trace, partition)
 
 METRIC = "aggregate iters/s at 1-8 B200; job-switch µs; avg JCT vs FIFO baseline"
 UNIT = "iters/s"
@@ -117,6 +117,35 @@ class ClockSampler:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
         return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
                 "samples": len(sm)}
+
+
+def switch_latency(S, device):
+    """North-star secondary metric: iteration-boundary switch latency with
+    42 packed inference models (C3: 14 architectures x 3 instances, FAIR over
+    8 time-shared lanes).  From the device wall stamps of one run: for
+    consecutive iterations of a lane, start(next) - end(prev), split into job
+    switches and same-job continuations."""
+    jobs, cap = c3_trace()
+    ctx = S.Context(jobs, cap, S.FAIR, device=device, max_lanes=8, log=True)
+    ctx.run()
+    rs = ctx.run_stats()
+    w = ctx.wall()
+    ctx.close()
+    w = w[np.argsort(w["seq"])]
+    sw, gap, last = [], [], {}
+    for r in w:
+        ln = int(r["lane"])
+        if ln in last:
+            prev = last[ln]
+            d = (int(r["start_ns"]) - int(prev["end_ns"])) / 1e3
+            (gap if prev["job"] == r["job"] else sw).append(d)
+        last[ln] = r
+    return {"config": "C3: 42 inference models (14 archs x 3), FAIR, 8 lanes, 16 GiB",
+            "models_coresident": len(jobs), "requests": int(rs["n_dispatch"]),
+            "requests_per_s": rs["n_dispatch"] / (rs["kernel_ns"] / 1e9),
+            "switch_us": {"n": len(sw), "p50": float(np.median(sw)) if sw else None,
+                          "p99": float(np.percentile(sw, 99)) if sw else None},
+            "same_job_gap_us": {"n": len(gap), "p50": float(np.median(gap)) if gap else None}}
 
 
 def cpu_baseline(jobs, cap, budget_s=12.0):
@@ -321,6 +350,10 @@ def main():
             "stats_allgathered": int(all_stats.shape[0]),
             "sched_wait_frac": rs0["sched_wait_ns"] / max(1, rs0["kernel_ns"]),
         }
+        try:
+            line["c3_switch"] = switch_latency(S, local)
+        except Exception as exc:  # noqa: BLE001
+            line["c3_switch"] = {"error": str(exc)[:200]}
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(jobs, cap)
         print(json.dumps(line), flush=True)
