@@ -45,8 +45,9 @@ def dist_env():
 
 
 def workload(world, rank):
+    from paper_1902_04610_b200 import multigpu as MG
     jobs, cap = c2_trace("a", n_jobs=N_JOBS * world, n_iters=N_ITERS)
-    return partition(jobs, world, rank), cap
+    return MG.partition_jobs(jobs, world, rank), cap
 
 
 def work_per_iter(job):
@@ -268,14 +269,11 @@ def main():
     value = total_iters / (ms_max / 1000.0)
 
     # NCCL all_gather of per-GPU completion statistics
-    rec = torch.tensor([[s["job_id"], s["completion_tick"], s["completion_seq"], s["first_lane"]]
-                        for s in stats.values()], dtype=torch.int64, device=f"cuda:{local}")
-    gathered = [torch.empty_like(rec) for _ in range(world)]
-    if world > 1:
-        dist.all_gather(gathered, rec)
-    else:
-        gathered = [rec]
-    all_stats = torch.cat(gathered).cpu().numpy()
+    from paper_1902_04610_b200 import multigpu as MG
+    torch.cuda.synchronize()
+    ta = time.perf_counter()
+    all_stats = MG.gather_stats(stats, rank, world, device=f"cuda:{local}")
+    allgather_us = (time.perf_counter() - ta) * 1e6
 
     # e2e: the same metric through the C ABI from host buffers (open + submit
     # + prepare [H2D job tables] + run + stats readback [D2H]) every step
@@ -347,7 +345,7 @@ def main():
             "jct": {"avg_fifo_ticks": fifo["avg_jct"], "avg_pack_ticks": pack["avg_jct"],
                     "fifo_over_pack": fifo["avg_jct"] / pack["avg_jct"],
                     "makespan_fifo_over_pack": fifo["makespan"] / pack["makespan"]},
-            "stats_allgathered": int(all_stats.shape[0]),
+            "stats_allgathered": len(all_stats), "allgather_us": allgather_us,
             "sched_wait_frac": rs0["sched_wait_ns"] / max(1, rs0["kernel_ns"]),
         }
         try:

@@ -1,0 +1,53 @@
+"""Multi-GPU plumbing: one independent Salus instance per GPU.
+
+Jobs are independent units, so the path shards with no data-path
+collective: the k-th job in (arrival, id) order goes to GPU k mod G
+(`workloads.partition`).  The only collective is one all_gather of fixed-size
+per-GPU completion records after the run (NCCL over NVLink on the GPU box,
+gloo in the CPU tests).  Host logic only — marshalling, no method arithmetic.
+"""
+from __future__ import annotations
+
+from typing import Dict, Iterable
+
+import numpy as np
+
+# one int64 record per job: job_id, first_lane, admit, first_start, completion, completion_seq, rank
+REC_FIELDS = ("job_id", "first_lane", "admit_tick", "first_start_tick", "completion_tick",
+              "completion_seq", "rank")
+
+
+def pack_stats(stats: Dict[int, dict], rank: int, n_pad: int):
+    """{job_id: stat dict} -> int64 array [n_pad, 7], padded with job_id -1."""
+    out = np.full((n_pad, len(REC_FIELDS)), -1, dtype=np.int64)
+    for i, jid in enumerate(sorted(stats)):
+        s = stats[jid]
+        out[i] = (s["job_id"], s["first_lane"], s["admit_tick"], s["first_start_tick"],
+                  s["completion_tick"], np.int64(np.uint64(s["completion_seq"]).astype(np.int64)), rank)
+    return out
+
+
+def gather_stats(stats: Dict[int, dict], rank: int, world: int, device=None) -> Dict[int, dict]:
+    """All-gather every rank's per-job records; returns the merged dict."""
+    import torch
+    import torch.distributed as dist
+    n = torch.tensor([len(stats)], dtype=torch.int64, device=device)
+    if world > 1:
+        dist.all_reduce(n, op=dist.ReduceOp.MAX)
+    rec = torch.from_numpy(pack_stats(stats, rank, int(n.item()))).to(device)
+    parts = [torch.empty_like(rec) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(parts, rec)
+    else:
+        parts = [rec]
+    merged = {}
+    for row in torch.cat(parts).cpu().numpy():
+        if row[0] < 0:
+            continue
+        merged[int(row[0])] = dict(zip(REC_FIELDS, (int(x) for x in row)))
+    return merged
+
+
+def partition_jobs(jobs: Iterable, world: int, rank: int):
+    from workloads import partition
+    return partition(list(jobs), world, rank)
