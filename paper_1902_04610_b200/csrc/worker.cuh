@@ -113,6 +113,39 @@ __device__ __forceinline__ uint32_t swz(uint32_t r, uint32_t chunk) {
   return r * 128u + (((chunk ^ (r & 7u)) & 7u) << 4);
 }
 
+__device__ __forceinline__ uint4 shfl_xor_u4(uint4 v, int m) {
+  v.x = __shfl_xor_sync(0xffffffffu, v.x, m);
+  v.y = __shfl_xor_sync(0xffffffffu, v.y, m);
+  v.z = __shfl_xor_sync(0xffffffffu, v.z, m);
+  v.w = __shfl_xor_sync(0xffffffffu, v.w, m);
+  return v;
+}
+
+// Store 32 bf16 columns (4 x 16-byte chunks, chunk index ch0..ch0+3) of the
+// warp's 32 rows into a swizzled panel row block.  A 4x4 transpose of the
+// chunks inside each group of 4 lanes (two shfl_xor stages) lets every store
+// instruction write 8 rows x 64 contiguous bytes (the swizzle keeps a
+// row-half's 4 chunks inside one 64-byte half) instead of 32 rows x 16 bytes.
+// `r` = this lane's row in the tile (warp-uniform quarter base + lane).
+__device__ __forceinline__ void store_bf16_rows(uint8_t *panel, uint4 (&u)[4], uint32_t r, uint32_t ch0) {
+  const uint32_t lane = r & 31u, base = r & ~31u;
+  const bool b0 = lane & 1u, b1 = lane & 2u;
+#pragma unroll
+  for (int p = 0; p < 4; p += 2) {                 // stage 1: pairs (xor 1)
+    const uint4 recv = shfl_xor_u4(b0 ? u[p] : u[p + 1], 1);
+    if (b0) u[p] = recv; else u[p + 1] = recv;
+  }
+#pragma unroll
+  for (int p = 0; p < 2; p++) {                    // stage 2: pairs of pairs (xor 2)
+    const uint4 recv = shfl_xor_u4(b1 ? u[p] : u[p + 2], 2);
+    if (b1) u[p] = recv; else u[p + 2] = recv;
+  }
+  // lane now holds chunk c = lane & 3 of rows 4*(lane>>2) + k, k = 0..3
+  const uint32_t c = ch0 + (lane & 3u), g = base + 4u * (lane >> 2);
+#pragma unroll
+  for (int k = 0; k < 4; k++) *reinterpret_cast<uint4 *>(panel + swz(g + k, c)) = u[k];
+}
+
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
@@ -285,15 +318,16 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
         *reinterpret_cast<float4 *>(tds.ptr[PTR_W32 + (grp >> 5)] + (grp & 31u) * 2048u + r * 16u) = w;
         v[4 * g + 0] = w.x; v[4 * g + 1] = w.y; v[4 * g + 2] = w.z; v[4 * g + 3] = w.w;
       }
-      uint8_t *aux = tds.ptr[PTR_AUX + pan];
+      {
+        uint4 u[4];
 #pragma unroll
-      for (int q = 0; q < 4; q++) {
-        uint4 u;
-        u.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-        u.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-        u.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-        u.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-        *reinterpret_cast<uint4 *>(aux + swz(r, ch0 + q)) = u;
+        for (int q = 0; q < 4; q++) {
+          u[q].x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+          u[q].y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+          u[q].z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+          u[q].w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
+        }
+        store_bf16_rows(tds.ptr[PTR_AUX + pan], u, r, ch0);
       }
       if (dump && row_ok) {                     // W[i][j], logical d_{l-1} x d_l
         for (int x = 0; x < 32; x++)
@@ -338,16 +372,15 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
         }
       }
     }
-    uint8_t *out = tds.ptr[PTR_OUT + pan];
+    uint4 u[4];
 #pragma unroll
     for (int q = 0; q < 4; q++) {
-      uint4 u;
-      u.x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
-      u.y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
-      u.z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
-      u.w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
-      *reinterpret_cast<uint4 *>(out + swz(r, ch0 + q)) = u;
+      u[q].x = pack_bf16x2(v[8 * q + 0], v[8 * q + 1]);
+      u[q].y = pack_bf16x2(v[8 * q + 2], v[8 * q + 3]);
+      u[q].z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
+      u[q].w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
     }
+    store_bf16_rows(tds.ptr[PTR_OUT + pan], u, r, ch0);
   }
 }
 
