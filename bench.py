@@ -149,6 +149,63 @@ def switch_latency(S, device):
             "same_job_gap_us": {"n": len(gap), "p50": float(np.median(gap)) if gap else None}}
 
 
+def overhead_vs_standalone(S, device, dims=(1024, 1024, 1024, 1024), batch=256, iters=100):
+    """SURVEY NEXT-1 (the analogue of PAPER.md fig:exp5-17): the
+    per-iteration time of ONE job running alone inside Salus (device wall
+    stamps) vs the same training step issued standalone through PyTorch /
+    cuBLAS (bf16 GEMMs, fp32 master SGD) and replayed from a CUDA graph.
+    A comparison baseline only -- never the product path."""
+    import torch
+    from workloads import make_job
+    job = make_job(0, TRAIN, 0, dims, batch, iters, lr=1e-3, seed=1)
+    ctx = S.Context([job], 1 << 30, S.PACK, device=device, log=True)
+    ctx.run()
+    w = ctx.wall()
+    ctx.close()
+    salus_us = float(np.median((w["end_ns"][1:] - w["start_ns"][1:]) / 1e3))
+    dev = f"cuda:{device}"
+    L = len(dims) - 1
+    W32 = [torch.randn(dims[l], dims[l + 1], device=dev) * dims[l] ** -0.5 for l in range(L)]
+    Wb = [w_.to(torch.bfloat16) for w_ in W32]
+    X = torch.randn(batch, dims[0], device=dev).to(torch.bfloat16)
+    T = torch.randn(batch, dims[-1], device=dev)
+
+    def step():
+        A = [X]
+        for l in range(L):
+            Z = A[-1] @ Wb[l]
+            A.append(torch.relu(Z) if l < L - 1 else Z)
+        G = ((A[-1].float() - T) / batch).to(torch.bfloat16)
+        for l in range(L - 1, -1, -1):
+            dW = (A[l].t() @ G).float()
+            if l > 0:
+                G = (G @ Wb[l].t()) * (A[l] > 0)
+            W32[l].sub_(1e-3 * dW)
+            Wb[l].copy_(W32[l])
+
+    s = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(s):
+        for _ in range(3):
+            step()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        step()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(s):
+        for _ in range(5):
+            g.replay()
+        e0.record(s)
+        for _ in range(iters):
+            g.replay()
+        e1.record(s)
+    torch.cuda.synchronize()
+    torch_us = e0.elapsed_time(e1) * 1e3 / iters
+    return {"shape": f"MLP {list(dims)} B={batch}, one job alone", "salus_iter_us": salus_us,
+            "standalone_torch_graph_iter_us": torch_us, "ratio": salus_us / torch_us}
+
+
 def cpu_baseline(jobs, cap, budget_s=12.0):
     """The oracle as it stands, on this host's cores, on a bounded sample of
     the same workload: the full schedule simulation plus as many fp64
@@ -348,6 +405,10 @@ def main():
             "stats_allgathered": len(all_stats), "allgather_us": allgather_us,
             "sched_wait_frac": rs0["sched_wait_ns"] / max(1, rs0["kernel_ns"]),
         }
+        try:
+            line["overhead_vs_standalone"] = overhead_vs_standalone(S, local)
+        except Exception as exc:  # noqa: BLE001
+            line["overhead_vs_standalone"] = {"error": str(exc)[:200]}
         try:
             line["c3_switch"] = switch_latency(S, local)
         except Exception as exc:  # noqa: BLE001

@@ -121,3 +121,63 @@ def test_deep_and_wide_layers():
         _check_math(ctx, jobs)
     finally:
         ctx.close()
+
+
+def test_c3_inference_real_work_sampled():
+    """C3 (42 inference models, PACK, real work): schedule parity, and the
+    outputs of a sample of models (small MLPs with b = 1..16 and an
+    im2col/1x1-conv chain) at their first and last request."""
+    from paper_1902_04610_b200 import salus as S
+    from workloads import c3_trace
+    jobs, cap = c3_trace()
+    pick = [j for j in jobs if j.dims[-1] * j.batch <= 1024 * 256][:4] + \
+           [j for j in jobs if j.batch >= 1024][:1]
+    dump = {j.job_id: S.DUMP_OUTPUTS for j in pick}
+    ctx, ref, stats = assert_schedule_parity(jobs, cap, OS.PACK, null_work=False, dump=dump)
+    try:
+        for j in pick:
+            W0 = OL.init_weights(j)
+            for k in (0, j.n_iters - 1):
+                X, _ = OL.inputs(j, k)
+                r64 = OL.forward(W0, X)[-1]
+                r16 = OL.forward(W0, X, OL.bf16)[-1]
+                g = ctx.layers(j.job_id, k).reshape(j.batch, j.dims[-1])
+                assert normwise_rel(g, r64) <= TOL, (j.job_id, k)
+                # vs the bf16-storage oracle: each layer may round a few
+                # boundary elements one bf16 ulp (2^-8) differently (fp32 vs
+                # fp64 sums); over up to 4 layers that stays well below 5e-3
+                assert normwise_rel(g, r16) <= 5e-3, (j.job_id, k)
+    finally:
+        ctx.close()
+
+
+def test_c4_real_work_sampled():
+    """C4 (100-job mixed trace, SRTF, real work at full size): schedule
+    parity; full weight trajectories of the small jobs compared to the oracle."""
+    from paper_1902_04610_b200 import salus as S
+    from workloads import c4_trace
+    jobs, cap = c4_trace()
+    small = sorted((j for j in jobs if j.dims[0] <= 512 and j.n_iters <= 60),
+                   key=lambda j: j.n_iters)[:2]
+    assert small
+    dump = {j.job_id: S.DUMP_OUTPUTS | S.DUMP_WEIGHTS for j in small}
+    ctx, ref, stats = assert_schedule_parity(jobs, cap, OS.SRTF, null_work=False, dump=dump,
+                                             timeout_ms=300000)
+    try:
+        _check_math(ctx, small)
+    finally:
+        ctx.close()
+
+
+def test_max_sizes():
+    """Widest layer the ABI accepts (8192 -> K = 8192, 128 K-chunks) and a
+    ragged 8-layer-deep job, in one arena."""
+    from paper_1902_04610_b200 import salus as S
+    jobs = [make_job(0, TRAIN, 0, (8192, 256), 136, 2, lr=1e-2, seed=5),
+            make_job(1, INFER, 0, (256, 8192, 128), 3, 2, seed=6, request_ticks=(0, 1))]
+    dump = {0: S.DUMP_OUTPUTS | S.DUMP_WEIGHTS, 1: S.DUMP_OUTPUTS}
+    ctx, ref, stats = assert_schedule_parity(jobs, 4 << 30, OS.PACK, null_work=False, dump=dump)
+    try:
+        _check_math(ctx, jobs)
+    finally:
+        ctx.close()
