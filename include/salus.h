@@ -136,7 +136,7 @@ typedef struct {
                                 (A16); 0 in parity tests                          */
   uint64_t log_capacity;     /* records reserved for the log and for wall stamps */
   uint64_t dump_bytes;       /* bytes reserved for SALUS_DUMP_* data             */
-  uint32_t n_workers;        /* worker CTAs; 0 -> (#SMs - 1)                      */
+  uint32_t n_workers;        /* worker CTA pairs; 0 -> (#SMs / 2 - 1)              */
   uint32_t timeout_ms;       /* salus_run watchdog; 0 -> 600000                   */
   uint64_t trace_capacity;   /* SALUS_FLAG_TRACE records; 0 -> 1<<20              */
 } salus_config;
@@ -217,12 +217,12 @@ typedef struct {
   uint64_t n_dispatch;        /* iterations executed                              */
   uint64_t n_ticks;           /* scheduler ticks processed                        */
   uint64_t n_log;             /* log records written                              */
-  uint64_t n_tasks;           /* tile tasks executed by workers                   */
+  uint64_t n_tasks;           /* 128-row tiles executed by workers (per CTA half) */
   uint64_t kernel_ns;         /* CUDA-event time of the persistent kernel         */
   uint64_t wall_first_ns, wall_last_ns;   /* globaltimer at kernel start / end   */
   uint64_t sched_wait_ns;     /* scheduler time spent waiting for iterations      */
   int32_t  status;            /* SALUS_OK or the device error code               */
-  uint32_t n_workers;
+  uint32_t n_workers;         /* worker CTA pairs                                 */
   uint64_t h2d_bytes;         /* host->device bytes of salus_prepare (job tables) */
   uint64_t d2h_bytes;         /* device->host bytes read back by salus_run        */
 } salus_run_stats;

@@ -8,7 +8,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsalus.so")
 SOURCES = ["salus_kernel.cu", "salus_host.cpp"]
-HEADERS = ["salus_dev.h", "ptx.cuh", "datagen.cuh", "scheduler.cuh", "worker.cuh"]
+HEADERS = ["salus_dev.h", "ptx.cuh", "datagen.cuh", "scheduler.cuh", "worker.cuh", "runahead.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
@@ -33,6 +33,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
     return LIB
+
+
+def build_variant(out: str, defines) -> str:
+    """Experiment builds (compile-time ablations) into a separate .so."""
+    os.makedirs(os.path.dirname(os.path.abspath(out)), exist_ok=True)
+    cmd = [NVCC] + FLAGS + ["-D" + d for d in defines] + ["-o", os.path.abspath(out)] + SOURCES
+    r = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(r.stdout + r.stderr)
+        raise RuntimeError("nvcc failed building " + out)
+    return out
 
 
 if __name__ == "__main__":

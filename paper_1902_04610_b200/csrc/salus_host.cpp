@@ -263,16 +263,18 @@ static void compute_layout(salus_ctx *c) {
       D.g_off[0] = (uint32_t)off; off += 2 * bp * mx;
       D.g_off[1] = (uint32_t)off; off += 2 * bp * mx;
     }
-    // stage tiles
+    // stage tasks: pair tasks (a CTA pair computes 2 blocks / a 256-row super-tile)
+    auto pairs = [](uint32_t n) { return (n + 1) / 2; };
     uint32_t ti = 0;
     for (uint32_t l = 1; l <= L; l++) ti += (D.dpad[l] / 128) * (D.dpad[l - 1] / 128);
-    D.stage_tiles[0] = ti;
-    D.stage_tiles[1] = (D.bpad / 128) * (D.dpad[0] / 128);
-    for (uint32_t l = 1; l <= L; l++) D.stage_tiles[1 + l] = (D.bpad / 128) * (D.dpad[l] / ntile_for(D.dpad[l]));
+    D.stage_tiles[0] = pairs(ti);
+    D.stage_tiles[1] = pairs((D.bpad / 128) * (D.dpad[0] / 128));
+    for (uint32_t l = 1; l <= L; l++) D.stage_tiles[1 + l] = pairs(D.bpad / 128) * (D.dpad[l] / ntile_for(D.dpad[l]));
     if (j.kind == SALUS_TRAIN) {
       for (uint32_t l = L; l >= 1; l--) {
         const uint32_t s = L + 2 + (L - l), nt = ntile_for(D.dpad[l - 1]);
-        D.stage_tiles[s] = (D.dpad[l] / 128) * (D.dpad[l - 1] / nt) + (l > 1 ? (D.bpad / 128) * (D.dpad[l - 1] / nt) : 0);
+        D.stage_tiles[s] = pairs(D.dpad[l] / 128) * (D.dpad[l - 1] / nt) +
+                           (l > 1 ? pairs(D.bpad / 128) * (D.dpad[l - 1] / nt) : 0);
       }
     }
     D.n_stages = last_stage(j.kind, L) + 1;
@@ -335,8 +337,9 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   int grid = 0;
   int rc = max_coresident_grid(ctx->cfg.device, &grid);
   if (rc) return cuda_fail(ctx, (cudaError_t)rc, "occupancy");
-  if (grid < 2) return fail(ctx, SALUS_E_CUDA, "persistent kernel does not fit one CTA per SM");
-  if (ctx->cfg.n_workers && (int)ctx->cfg.n_workers + 1 < grid) grid = (int)ctx->cfg.n_workers + 1;
+  if (grid < 4) return fail(ctx, SALUS_E_CUDA, "persistent kernel does not fit two CTA pairs");
+  // n_workers counts worker CTA pairs; pair 0 is the scheduler's cluster
+  if (ctx->cfg.n_workers && 2 * ((int)ctx->cfg.n_workers + 1) < grid) grid = 2 * ((int)ctx->cfg.n_workers + 1);
   ctx->grid = (uint32_t)grid;
   ctx->meta = static_cast<uint8_t *>(meta);
   ctx->meta_bytes = meta_bytes;
@@ -399,7 +402,7 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   P.policy = ctx->cfg.policy;
   P.max_lanes = ctx->cfg.max_lanes;
   P.flags = ctx->cfg.flags;
-  P.n_workers = ctx->grid - 1;
+  P.n_workers = ctx->grid / 2 - 1;
   P.switch_ticks = (int64_t)ctx->cfg.switch_ticks;
   P.timeout_ns = (uint64_t)ctx->cfg.timeout_ms * 1000000ull;
   ctx->state = 1;
@@ -449,7 +452,7 @@ int salus_run(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_
   rs.n_dispatch = ctrl.n_dispatch; rs.n_ticks = ctrl.n_ticks; rs.n_log = std::min<uint64_t>(ctrl.n_log, ctx->log_cap);
   rs.n_tasks = ctrl.n_tasks; rs.kernel_ns = (uint64_t)((double)ms * 1e6);
   rs.wall_first_ns = ctrl.wall_first_ns; rs.wall_last_ns = ctrl.wall_last_ns;
-  rs.sched_wait_ns = ctrl.sched_wait_ns; rs.status = ctrl.status; rs.n_workers = ctx->grid - 1;
+  rs.sched_wait_ns = ctrl.sched_wait_ns; rs.status = ctrl.status; rs.n_workers = ctx->grid / 2 - 1;
   ctx->n_trace = std::min<uint64_t>(ctrl.n_trace, ctx->trace_cap);
   rs.h2d_bytes = ctx->h2d_bytes;
   rs.d2h_bytes = sizeof(Ctrl) + (stats ? sizeof(salus_job_stat) * ctx->jobs.size() : 0);

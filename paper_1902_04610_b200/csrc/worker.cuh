@@ -1,28 +1,37 @@
 // worker.cuh — worker CTAs of the persistent kernel.
 //
-// Each worker CTA is a warp-specialized, persistent tile engine (9 warps):
-//   warp 0     decoder: claims tile tasks from the device task ring up to
-//              NDESC tiles ahead, decodes them (stage -> GEMM / epilogue kind,
-//              tensors, coordinates) and translates the epilogue's page
-//              addresses, lanes in parallel.
+// Workers run as CTA pairs (a cluster of 2 on one TPC): every task is a
+// 256 x N super-tile computed by one tcgen05.mma.cta_group::2 issued by the
+// pair's leader (cluster rank 0).  CTA h holds rows [128h, 128h+128) of A
+// and columns [h N/2, h N/2 + N/2) of B in its shared memory and receives
+// its 128 accumulator rows in its own TMEM, so each SM loads half of the
+// shared B operand.  Both CTAs run the same roles on the same
+// task sequence; the leader claims tasks and mails the payload to its peer.
+// Each worker CTA is a warp-specialized, persistent tile engine (13 warps):
+//   warp 0     decoder: (leader) claims tasks from the device task ring up
+//              to NDESC ahead and mails them to the peer; (both) decodes its
+//              half (stage -> GEMM / epilogue kind, tensors, coordinates) and
+//              translates the epilogue's page addresses, lanes in parallel.
 //   warp 1     operand loader (1 thread): issues every K-chunk of the A/B
 //              operands as bulk async copies (cp.async.bulk, TMA unit) into a
-//              3-stage mbarrier ring, translating pages on the fly.
-//   warp 2     MMA (1 thread): tcgen05.mma kind::f16 (bf16 in, fp32 accumulate)
-//              into one of two TMEM accumulators of 256 columns (double
-//              buffered: the epilogue of tile i overlaps the MMA of tile i+1).
+//              5-stage mbarrier ring (page-table reads two chunks ahead).
+//   warp 2     leader: MMA (1 thread): tcgen05.mma.cta_group::2 kind::f16
+//              (bf16 in, fp32 accumulate) into one of two TMEM accumulators
+//              of 256 columns in both CTAs (double buffered: the epilogue of
+//              tile i overlaps the MMA of tile i+1).  peer: forwards each
+//              landed K-chunk of its smem to the leader's pair_full barrier.
 //   warp 3     epilogue-input loader (1 thread): streams the tile's epilogue
 //              input (fp32 master weights of a dW tile, ReLU mask of a dX
 //              tile) in 32 KiB chunks through two smem buffers.
-//   warps 4-7  epilogue: drain TMEM (tcgen05.ld), fused epilogue, stores.
-//   warp 8     completion: gpu-scope fence, stage accounting, publication of
+//   warps 4-11 epilogue: drain TMEM (tcgen05.ld), fused epilogue, stores.
+//   warp 12    completion: gpu-scope fence, stage accounting, publication of
 //              the next stage / start of the slot's next iteration (run-ahead)
 //              -- off the epilogue's critical path.
 // No host round-trip and no context teardown between iterations or jobs: a
 // "job switch" is just a task whose slot points at a different job.
 //
-// Tiles are M = 128 x N (N = 256 when it divides the output width, else 128),
-// K in chunks of 64 bf16.  Operands are bf16 tensors stored as 128-byte-
+// Per CTA a tile is M = 128 x N (N = 256 when it divides the output width,
+// else 128), K in chunks of 64 bf16.  Operands are bf16 tensors stored as 128-byte-
 // swizzled 64-column panels, so a K-chunk is one 16 KiB block
 // per 128 rows (K-major) or one 8 KiB block per 64 columns (MN-major).
 #pragma once
@@ -34,19 +43,36 @@
 
 namespace salus {
 
-constexpr uint32_t PIPE = 3;
-constexpr uint32_t STAGE_A_BYTES = 16384;             // 128 x 64 bf16
-constexpr uint32_t STAGE_B_BYTES = 32768;             // <= 256 x 64 bf16
+#ifndef SALUS_PIPE
+#define SALUS_PIPE 5
+#endif
+constexpr uint32_t PIPE = SALUS_PIPE;                 // operand stages in flight
+constexpr uint32_t STAGE_A_BYTES = 16384;             // 128 x 64 bf16 (this CTA's rows)
+constexpr uint32_t STAGE_B_BYTES = 16384;             // <= 128 x 64 bf16 (this CTA's half of N)
 constexpr uint32_t STAGE_BYTES = STAGE_A_BYTES + STAGE_B_BYTES;
 constexpr uint32_t ECH_BYTES = 32768;                 // epilogue-input chunk
-constexpr uint32_t NDESC = 4;                         // decoder lookahead (tiles)
-constexpr uint32_t EPI_WARPS = 4;
+#ifndef SALUS_NDESC
+#define SALUS_NDESC 4
+#endif
+constexpr uint32_t NDESC = SALUS_NDESC;               // decoder lookahead (tiles)
+#ifndef SALUS_EPI_WARPS
+#define SALUS_EPI_WARPS 8
+#endif
+// 4 or 8 epilogue warps: warp w reads TMEM lane quarter w % 4; with 8, the
+// two warps of a quarter split the columns (two warps per SM sub-partition
+// hide each other's TMEM / smem / store latencies)
+constexpr uint32_t EPI_WARPS = SALUS_EPI_WARPS;
+constexpr uint32_t EPI_HALVES = EPI_WARPS / 4;
+static_assert(EPI_WARPS == 4 || EPI_WARPS == 8, "epilogue warps: 4 or 8");
 constexpr uint32_t EPI_THREADS = 32 * EPI_WARPS;
 constexpr uint32_t EPI_WARP0 = 4;
 constexpr uint32_t DONE_WARP = EPI_WARP0 + EPI_WARPS;          // completion warp
 constexpr uint32_t WORKER_THREADS = 32 * (DONE_WARP + 1);
 constexpr uint32_t ACC_COLS = 256;
 constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;          // all of TMEM: 2 accumulators
+#ifndef SALUS_SGD_BULK
+#define SALUS_SGD_BULK 1   // SGD epilogue writes W32 back in smem, one bulk store per chunk
+#endif
 
 enum : uint32_t { T_EXIT = 0, T_INIT = 1, T_GEN = 2, T_GEMM = 3 };
 enum : uint32_t { EPI_RELU = 0, EPI_OUT = 1, EPI_LOSS = 2, EPI_DX = 3, EPI_SGD = 4 };
@@ -61,6 +87,7 @@ struct OpDesc {
 
 struct TileDesc {
   uint32_t kind, payload, slot, stage, job, iter, ntiles, next_ntiles, is_last, first_stage;
+  uint32_t valid;          // this CTA's half exists (odd block counts leave the peer's empty)
   uint64_t seq, t_claim, t_ready, t_mma, t_end;   // trace stamps
   // GEMM
   uint32_t N, nk, idesc, epi, layer, ncopy_a, ncopy_b, abytes, bbytes;
@@ -86,6 +113,9 @@ struct WorkerSmem {
   uint64_t acc_full[2], acc_empty[2];
   uint64_t epi_full[2], epi_empty[2];
   uint64_t epi_done[NDESC];           // epilogue -> completion warp
+  uint64_t pair_full[PIPE];           // leader: the peer's K-chunk has landed
+  uint64_t mail_full[NDESC];          // peer: the leader mailed task d
+  struct { uint32_t payload, pad; uint64_t t_claim; } mail[NDESC];
   uint32_t tmem_base;
   alignas(16) uint32_t job_cache[128]; // decoder scratch: the task's DevJob (<= 512 B)
 };
@@ -156,8 +186,10 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
 // Page translations are only recorded here (defer) and resolved by the
 // decoder warp's lanes in parallel.
 // ---------------------------------------------------------------------------
+// A task is a pair task: CTA h takes block 2t + h of INIT / GEN, and M block
+// 2 mp + h of a GEMM super-tile (the N block is shared).
 __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, const Slot &sl,
-                            TileDesc &td) {
+                            TileDesc &td, uint32_t h) {
   td.payload = payload;
   const uint32_t slot = payload >> 26, stage = (payload >> 21) & 31u, tile = payload & ((1u << 21) - 1);
   const uint32_t k = sl.iter;
@@ -170,18 +202,20 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   td.dump_off = -1;
   td.n_ech = 0;
   td.xt_mask = 0;
+  td.valid = 1;
   td.ptr[PTR_W32] = nullptr;
   const uint32_t *lt = P.lpt + (uint64_t)slot * P.lpt_stride;   // lane (ephemeral) space
   const uint32_t *jt = P.ppt + J.pt_off;                        // job (persistent) space
 
   if (stage == 0) {                                   // INIT weights (128 x 128 blocks)
     td.kind = T_INIT;
-    uint32_t t = tile, l = 1;
+    uint32_t t = 2 * tile + h, l = 1;
     for (; l <= L; l++) {
       const uint32_t nb = (J.dpad[l] / 128) * (J.dpad[l - 1] / 128);
       if (t < nb) break;
       t -= nb;
     }
+    if (l > L) { td.valid = 0; return; }
     const uint32_t nib = J.dpad[l - 1] / 128, jb = t / nib, ib = t % nib;
     td.layer = l; td.m0 = jb * 128; td.n0 = ib * 128;
     td.rows_valid = J.dims[l]; td.cols_valid = J.dims[l - 1];
@@ -196,7 +230,8 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   }
   if (stage == 1) {                                   // GEN input batch X (128 x 128 blocks)
     td.kind = T_GEN;
-    const uint32_t ncb = J.dpad[0] / 128, mb = tile / ncb, cb = tile % ncb;
+    const uint32_t ncb = J.dpad[0] / 128, blk = 2 * tile + h, mb = blk / ncb, cb = blk % ncb;
+    if (mb >= bp / 128) { td.valid = 0; return; }
     td.m0 = mb * 128; td.n0 = cb * 128;
     td.rows_valid = J.batch; td.cols_valid = J.dims[0];
     for (uint32_t q = 0; q < 2; q++)
@@ -207,10 +242,11 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   td.kind = T_GEMM;
   if (stage <= L + 1) {                               // forward F_l
     const uint32_t l = stage - 1, N = ntile_for(J.dpad[l]), ntn = J.dpad[l] / N;
-    const uint32_t mb = tile / ntn, nb = tile % ntn;
+    const uint32_t mb = 2 * (tile / ntn) + h, nb = tile % ntn;
+    td.valid = mb < bp / 128;
     td.layer = l; td.N = N; td.nk = J.dpad[l - 1] / 64;
     td.a = OpDesc{lt, J.act_off[l - 1], bp, mb * 128, 0};
-    td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * N, 0};
+    td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * N + h * (N / 2), 0};
     td.m0 = mb * 128; td.n0 = nb * N;
     td.rows_valid = J.batch; td.cols_valid = J.dims[l]; td.ld_logical = J.dims[l];
     uint32_t out_off;
@@ -219,55 +255,66 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
       td.epi = EPI_LOSS; out_off = J.g_off[0];
       td.key = gen_key(J.seed, J.job_id, GEN_T, L, k);
     } else { td.epi = EPI_OUT; out_off = J.act_off[L]; }
-    if (l == L && (J.dump & SALUS_DUMP_OUTPUTS))
-      td.dump_off = (int64_t)(J.dump_out_off + (uint64_t)k * J.batch * J.dims[L]);
-    for (uint32_t q = 0; q < N / 64; q++)
-      defer(td, PTR_OUT + q, lt, out_off + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
+    if (td.valid) {
+      if (l == L && (J.dump & SALUS_DUMP_OUTPUTS))
+        td.dump_off = (int64_t)(J.dump_out_off + (uint64_t)k * J.batch * J.dims[L]);
+      for (uint32_t q = 0; q < N / 64; q++)
+        defer(td, PTR_OUT + q, lt, out_off + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
+    }
   } else {                                            // backward B_l
     const uint32_t l = L - (stage - (L + 2));
-    const uint32_t N = ntile_for(J.dpad[l - 1]), ntn = J.dpad[l - 1] / N, nW = (J.dpad[l] / 128) * ntn;
+    const uint32_t N = ntile_for(J.dpad[l - 1]), ntn = J.dpad[l - 1] / N;
+    const uint32_t nW = ((J.dpad[l] / 128 + 1) / 2) * ntn;     // dW pair tasks
     const uint32_t gin = J.g_off[(L - l) & 1], gout = J.g_off[(L - l + 1) & 1];
     td.layer = l; td.N = N;
     if (tile < nW) {                                  // dW_l^T = G_l^T A_{l-1}; SGD
-      const uint32_t mb = tile / ntn, nb = tile % ntn;
+      const uint32_t mb = 2 * (tile / ntn) + h, nb = tile % ntn;
+      td.valid = mb < J.dpad[l] / 128;
       td.epi = EPI_SGD; td.nk = bp / 64;
       td.a = OpDesc{lt, gin, bp, mb * 128, 1};
-      td.b = OpDesc{lt, J.act_off[l - 1], bp, nb * N, 1};
+      td.b = OpDesc{lt, J.act_off[l - 1], bp, nb * N + h * (N / 2), 1};
       td.m0 = mb * 128; td.n0 = nb * N;
       td.rows_valid = J.dims[l]; td.cols_valid = J.dims[l - 1]; td.ld_logical = J.dims[l];
       td.lr = J.lr;
       // the 128 x N fp32 master tile is N/128 contiguous 64 KiB pages
       // (j-blocked layout), streamed to the epilogue in 64-column chunks
       const uint32_t w32 = J.w32_off[l - 1] + (mb * (J.dpad[l - 1] / 4) + nb * N / 4) * 2048u;
-      for (uint32_t q = 0; q < N / 128; q++) defer(td, PTR_W32 + q, jt, w32 + q * 65536u);
-      td.n_ech = N / 64;
-      for (uint32_t q = 0; q < N / 64; q++)
-        defer(td, PTR_AUX + q, jt, J.wb_off[l - 1][(k + 1) & 1] + (td.n0 / 64 + q) * J.dpad[l] * 128u + mb * 16384u);
-      if ((J.dump & SALUS_DUMP_WEIGHTS) && k + 1 == J.n_iters) {
+      if (td.valid) {
+        for (uint32_t q = 0; q < N / 128; q++) defer(td, PTR_W32 + q, jt, w32 + q * 65536u);
+        td.n_ech = N / 64;
+        for (uint32_t q = 0; q < N / 64; q++)
+          defer(td, PTR_AUX + q, jt, J.wb_off[l - 1][(k + 1) & 1] + (td.n0 / 64 + q) * J.dpad[l] * 128u + mb * 16384u);
+      }
+      if (td.valid && (J.dump & SALUS_DUMP_WEIGHTS) && k + 1 == J.n_iters) {
         uint64_t base = J.dump_w_off;
         for (uint32_t q = 1; q < l; q++) base += (uint64_t)J.dims[q - 1] * J.dims[q];
         td.dump_off = (int64_t)base;
       }
     } else {                                          // G_{l-1} = (G_l W_l^T) * [A_{l-1} > 0]
-      const uint32_t u = tile - nW, mb = u / ntn, nb = u % ntn;
+      const uint32_t u = tile - nW, mb = 2 * (u / ntn) + h, nb = u % ntn;
+      td.valid = mb < bp / 128;
       td.epi = EPI_DX; td.nk = J.dpad[l] / 64;
       td.a = OpDesc{lt, gin, bp, mb * 128, 0};
-      td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * N, 1};
+      td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * N + h * (N / 2), 1};
       td.m0 = mb * 128; td.n0 = nb * N;
       td.rows_valid = J.batch; td.cols_valid = J.dims[l - 1];
-      for (uint32_t q = 0; q < N / 64; q++) {
-        defer(td, PTR_OUT + q, lt, gout + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
-        defer(td, PTR_EPI + q, lt, J.act_off[l - 1] + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
+      if (td.valid) {
+        for (uint32_t q = 0; q < N / 64; q++) {
+          defer(td, PTR_OUT + q, lt, gout + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
+          defer(td, PTR_EPI + q, lt, J.act_off[l - 1] + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
+        }
+        td.n_ech = N / 128;                           // 2 mask panels (32 KiB) per chunk
       }
-      td.n_ech = N / 128;                             // 2 mask panels (32 KiB) per chunk
     }
   }
-  // A is always M = 128 rows; B is N rows (K-major) or N/64 panels (MN-major)
-  td.ncopy_a = td.a.mn ? 2 : 1;
+  // this CTA's A is M = 128 rows (none if its half is empty); its B is N/2
+  // rows (K-major, 64 or 128 rows per copy) or N/128 panels (MN-major)
+  const uint32_t nh = td.N / 2;
+  td.ncopy_a = td.valid ? (td.a.mn ? 2 : 1) : 0;
   td.abytes = td.a.mn ? 8192u : 16384u;
-  td.ncopy_b = td.b.mn ? td.N / 64 : td.N / 128;
-  td.bbytes = td.b.mn ? 8192u : 16384u;
-  td.idesc = ptx::idesc_bf16(128, td.N, td.a.mn, td.b.mn);
+  td.ncopy_b = td.b.mn ? nh / 64 : (nh + 127) / 128;
+  td.bbytes = td.b.mn ? 8192u : (nh >= 128 ? 16384u : nh * 128u);
+  td.idesc = ptx::idesc_bf16(256, td.N, td.a.mn, td.b.mn);
 }
 
 // global byte offset (inside the operand's space) of copy q of K-chunk kc
@@ -278,9 +325,9 @@ __device__ __forceinline__ uint32_t copy_off(const OpDesc &o, uint32_t kc, uint3
 
 // ---------------------------------------------------------------------------
 // Epilogue over accumulator column blocks [cc0, cc1) (32 columns each):
-// thread r of the 4 epilogue warps owns accumulator row r (TMEM lane r, warp
-// % 4 = lane quarter).  `buf` is the smem epilogue-input chunk holding the
-// W32 columns [32*cc0, +64) (SGD) or the mask columns [32*cc0, +128) (DX).
+// thread r of an epilogue warp owns accumulator row r (TMEM lane r, warp % 4
+// = lane quarter).  `buf` is the smem epilogue-input chunk holding the W32
+// columns [32*ccb, +64) (SGD) or the mask columns [32*ccb, +128) (DX).
 // ---------------------------------------------------------------------------
 struct EpiView {   // register copy of the descriptor fields the epilogue uses
   uint32_t m0, n0, rows_valid, cols_valid, ld_logical, epi;
@@ -290,7 +337,7 @@ struct EpiView {   // register copy of the descriptor fields the epilogue uses
 };
 
 __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiView &td, uint32_t tacc,
-                              uint32_t r, uint32_t cc0, uint32_t cc1, const uint8_t *buf) {
+                              uint32_t r, uint32_t ccb, uint32_t cc0, uint32_t cc1, uint8_t *buf) {
   const uint32_t qw = r >> 5;
   const uint32_t row = td.m0 + r;
   const bool row_ok = row < td.rows_valid;
@@ -310,12 +357,18 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
 #pragma unroll
       for (int g = 0; g < 8; g++) {
         const uint32_t grp = cc * 8 + g;                    // float4 column group in the tile
-        float4 w = *reinterpret_cast<const float4 *>(buf + ((cc - cc0) * 8 + g) * 2048u + r * 16u);
+        float4 *wp = reinterpret_cast<float4 *>(buf + ((cc - ccb) * 8 + g) * 2048u + r * 16u);
+        float4 w = *wp;
         w.x = fmaf(-td.lr, v[4 * g + 0], w.x);
         w.y = fmaf(-td.lr, v[4 * g + 1], w.y);
         w.z = fmaf(-td.lr, v[4 * g + 2], w.z);
         w.w = fmaf(-td.lr, v[4 * g + 3], w.w);
+#if SALUS_SGD_BULK
+        *wp = w;                                            // written back by one bulk store
+        (void)grp;
+#else
         *reinterpret_cast<float4 *>(tds.ptr[PTR_W32 + (grp >> 5)] + (grp & 31u) * 2048u + r * 16u) = w;
+#endif
         v[4 * g + 0] = w.x; v[4 * g + 1] = w.y; v[4 * g + 2] = w.z; v[4 * g + 3] = w.w;
       }
       {
@@ -336,7 +389,7 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
       continue;
     }
     if (td.epi == EPI_DX) {
-      const uint8_t *mp = buf + ((cc - cc0) >> 1) * 16384u;
+      const uint8_t *mp = buf + ((cc - ccb) >> 1) * 16384u;
 #pragma unroll
       for (int q = 0; q < 4; q++) {
         const uint4 m = *reinterpret_cast<const uint4 *>(mp + swz(r, ch0 + q));
@@ -385,7 +438,7 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
 }
 
 // INIT: W_l block (rows j = m0 + r of W^T storage, 128 columns i)
-__device__ void init_tile(const TileDesc &td, uint32_t r) {
+__device__ void init_tile(const TileDesc &td, uint32_t r, uint32_t h) {
   // descriptor fields in registers: global stores below may alias smem for
   // the compiler, which would otherwise reload them after every store
   const uint32_t j = td.m0 + r, n0 = td.n0, rows = td.rows_valid, cols = td.cols_valid;
@@ -395,7 +448,7 @@ __device__ void init_tile(const TileDesc &td, uint32_t r) {
   uint8_t *const aux0 = td.ptr[PTR_AUX], *const aux1 = td.ptr[PTR_AUX + 1];
   const int ncol = j < rows ? (int)cols - (int)n0 : 0;
 #pragma unroll 2
-  for (uint32_t cg = 0; cg < 128; cg += 8) {
+  for (uint32_t cg = h * (128 / EPI_HALVES); cg < (h + 1) * (128 / EPI_HALVES); cg += 8) {
     float v[8];
 #pragma unroll
     for (int x = 0; x < 8; x++) {
@@ -416,13 +469,13 @@ __device__ void init_tile(const TileDesc &td, uint32_t r) {
 }
 
 // GEN: X block (rows m = m0 + r, 128 columns)
-__device__ void gen_tile(const TileDesc &td, uint32_t r) {
+__device__ void gen_tile(const TileDesc &td, uint32_t r, uint32_t h) {
   const uint32_t m = td.m0 + r, n0 = td.n0, cols = td.cols_valid;
   const uint64_t key = td.key, base = (uint64_t)m * cols + n0;
   uint8_t *const out0 = td.ptr[PTR_OUT], *const out1 = td.ptr[PTR_OUT + 1];
   const int ncol = m < td.rows_valid ? (int)cols - (int)n0 : 0;
 #pragma unroll 2
-  for (uint32_t cg = 0; cg < 128; cg += 8) {
+  for (uint32_t cg = h * (128 / EPI_HALVES); cg < (h + 1) * (128 / EPI_HALVES); cg += 8) {
     float v[8];
 #pragma unroll
     for (int x = 0; x < 8; x++) {
@@ -439,24 +492,38 @@ __device__ void gen_tile(const TileDesc &td, uint32_t r) {
 // ---------------------------------------------------------------------------
 // Roles
 // ---------------------------------------------------------------------------
-__device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
+// Every consumer of descriptor slot d, in both CTAs, releases it on the
+// leader's desc_empty[d] (8 arrivals per use): the leader mails task d only
+// when the slot is free in both CTAs.
+__device__ __forceinline__ void release_desc(WorkerSmem &W, uint32_t d) { ptx::mbar_arrive_remote(&W.desc_empty[d], 0); }
+
+__device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint32_t h) {
   uint32_t d = 0, d_phase = 0;
   for (;;) {
-    ptx::mbar_wait_abortable(&W.desc_empty[d], d_phase ^ 1, &P.ctrl->abort);
     TileDesc &td = W.desc[d];
     uint32_t payload = TASK_EXIT;
     uint64_t t_claim = 0;
-    if (lane == 0) {
-      const unsigned long long pos = atomicAdd(&P.ctrl->q_tail, 1ull);
-      uint32_t spins = 0;
-      for (;;) {
-        const unsigned long long v = ptx::ld_acquire_u64(&P.ring[pos & P.ring_mask]);
-        if ((uint32_t)(v >> 32) == (uint32_t)(pos + 1)) { payload = (uint32_t)v; break; }
-        if ((++spins & 255) == 0 && *(volatile uint32_t *)&P.ctrl->abort) break;
+    if (h == 0) {                             // leader: claim, mail to the peer
+      ptx::mbar_wait_cluster(&W.desc_empty[d], d_phase ^ 1, &P.ctrl->abort);
+      if (lane == 0) {
+        const unsigned long long pos = atomicAdd(&P.ctrl->q_tail, 1ull);
+        uint32_t spins = 0;
+        for (;;) {
+          const unsigned long long v = ptx::ld_acquire_u64(&P.ring[pos & P.ring_mask]);
+          if ((uint32_t)(v >> 32) == (uint32_t)(pos + 1)) { payload = (uint32_t)v; break; }
+          if ((++spins & 255) == 0 && *(volatile uint32_t *)&P.ctrl->abort) break;
+        }
+        t_claim = ptx::globaltimer();
+        ptx::st_cluster_u32(ptx::mapa(&W.mail[d].payload, 1), payload);
+        ptx::st_cluster_u64(ptx::mapa(&W.mail[d].t_claim, 1), t_claim);
+        ptx::mbar_arrive_remote(&W.mail_full[d], 1);
       }
-      t_claim = ptx::globaltimer();
+      payload = __shfl_sync(0xffffffffu, payload, 0);
+    } else {                                  // peer: take the leader's mail
+      ptx::mbar_wait_cluster(&W.mail_full[d], d_phase, &P.ctrl->abort);
+      payload = W.mail[d].payload;
+      t_claim = W.mail[d].t_claim;
     }
-    payload = __shfl_sync(0xffffffffu, payload, 0);
     __syncwarp();   // lane 0's acquire orders the other lanes' reads below
     if (payload == TASK_EXIT) {
       if (lane == 0) {
@@ -472,14 +539,14 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
     for (uint32_t x = lane; x < sizeof(DevJob) / 4; x += 32) W.job_cache[x] = src[x];
     __syncwarp();
     if (lane == 0) {
-      decode_task(P, payload, *reinterpret_cast<const DevJob *>(W.job_cache), sl, td);
+      decode_task(P, payload, *reinterpret_cast<const DevJob *>(W.job_cache), sl, td, h);
       td.t_claim = t_claim;
     }
     __syncwarp();
     if (lane < NPTR && ((td.xt_mask >> lane) & 1u)) td.ptr[lane] = xlate(P, td.xt_table[lane], td.xt_off[lane]);
     __syncwarp();
     if (lane == 0) {
-      if (td.stage == td.first_stage)
+      if (h == 0 && td.stage == td.first_stage)
         atomicMin((unsigned long long *)&P.slots[td.slot].start_ns, (unsigned long long)ptx::globaltimer());
       ptx::fence_proxy_async_global();
       ptx::mbar_arrive(&W.desc_full[d]);
@@ -489,6 +556,27 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
   }
 }
 
+// Page numbers of one K-chunk's copies (A: <= 2, B: <= 2)
+struct ChunkPages { uint32_t a0, a1, b0, b1; };
+
+__device__ __forceinline__ ChunkPages chunk_pages(const OpDesc &a, const OpDesc &b, uint32_t nca, uint32_t ncb,
+                                                  uint32_t kc) {
+  ChunkPages p = {0, 0, 0, 0};
+  if (nca > 0) p.a0 = a.table[copy_off(a, kc, 0) >> PAGE_SHIFT];
+  if (nca > 1) p.a1 = a.table[copy_off(a, kc, 1) >> PAGE_SHIFT];
+  if (ncb > 0) p.b0 = b.table[copy_off(b, kc, 0) >> PAGE_SHIFT];
+  if (ncb > 1) p.b1 = b.table[copy_off(b, kc, 1) >> PAGE_SHIFT];
+  return p;
+}
+
+__device__ __forceinline__ const uint8_t *page_ptr(const Params &P, uint32_t page, uint32_t off) {
+  return P.arena + ((uint64_t)page << PAGE_SHIFT) + (off & (PAGE_BYTES - 1));
+}
+
+// Operand loader (1 thread).  The page-table reads of chunk kc + 2 are issued
+// before the copies of chunk kc, so their latency (an L2 round trip: the
+// completion warp's gpu-scope fences keep invalidating L1) is off the
+// per-chunk critical path.
 __device__ void operand_loader(const Params &P, WorkerSmem &W) {
   uint32_t d = 0, d_phase = 0, s = 0, s_phase = 0;
   for (;;) {
@@ -499,18 +587,28 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W) {
       const OpDesc a = td.a, b = td.b;
       const uint32_t nk = td.nk, nca = td.ncopy_a, ncb = td.ncopy_b, ab = td.abytes, bb = td.bbytes;
       const uint32_t tx = nca * ab + ncb * bb;
+      ChunkPages p0 = chunk_pages(a, b, nca, ncb, 0);
+      ChunkPages p1 = nk > 1 ? chunk_pages(a, b, nca, ncb, 1) : p0;
       for (uint32_t kc = 0; kc < nk; kc++) {
-        ptx::mbar_wait_abortable(&W.empty[s], s_phase ^ 1, &P.ctrl->abort);
+        const ChunkPages cur = p0;
+        p0 = p1;
+        if (kc + 2 < nk) p1 = chunk_pages(a, b, nca, ncb, kc + 2);
+        // stage s is free once the pair's MMA has consumed it (multicast commit)
+        ptx::mbar_wait_cluster(&W.empty[s], s_phase ^ 1, &P.ctrl->abort);
         ptx::mbar_arrive_expect_tx(&W.full[s], tx);
         uint8_t *sa = W.stage[s], *sb = W.stage[s] + STAGE_A_BYTES;
-        for (uint32_t q = 0; q < nca; q++)
-          ptx::bulk_g2s(sa + q * ab, xlate(P, a.table, copy_off(a, kc, q)), ab, &W.full[s]);
-        for (uint32_t q = 0; q < ncb; q++)
-          ptx::bulk_g2s(sb + q * bb, xlate(P, b.table, copy_off(b, kc, q)), bb, &W.full[s]);
+        if (nca > 0) ptx::bulk_g2s(sa, page_ptr(P, cur.a0, copy_off(a, kc, 0)), ab, &W.full[s]);
+        if (nca > 1) ptx::bulk_g2s(sa + ab, page_ptr(P, cur.a1, copy_off(a, kc, 1)), ab, &W.full[s]);
+        if (ncb > 0) ptx::bulk_g2s(sb, page_ptr(P, cur.b0, copy_off(b, kc, 0)), bb, &W.full[s]);
+        if (ncb > 1) ptx::bulk_g2s(sb + bb, page_ptr(P, cur.b1, copy_off(b, kc, 1)), bb, &W.full[s]);
+#if SALUS_DBG_CHUNKS   // trace fields re-purposed: loader issue of chunk 0 / last chunk
+        if (kc == 0) const_cast<TileDesc &>(td).t_ready = ptx::globaltimer();
+        if (kc + 1 == nk) const_cast<TileDesc &>(td).t_mma = ptx::globaltimer();
+#endif
         if (++s == PIPE) { s = 0; s_phase ^= 1; }
       }
     }
-    ptx::mbar_arrive(&W.desc_empty[d]);
+    release_desc(W, d);
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
 }
@@ -538,11 +636,13 @@ __device__ void epi_loader(const Params &P, WorkerSmem &W) {
         if (++e == 2) { e = 0; e_phase ^= 1; }
       }
     }
-    ptx::mbar_arrive(&W.desc_empty[d]);
+    release_desc(W, d);
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
 }
 
+// Leader: one tcgen05.mma.cta_group::2 per K16 step over both CTAs' smem;
+// commits arrive on the stage / accumulator barriers of both CTAs.
 __device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
   uint32_t d = 0, d_phase = 0, s = 0, s_phase = 0, b = 0, b_phase = 0;
   for (;;) {
@@ -550,13 +650,18 @@ __device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
     const TileDesc &td = W.desc[d];
     if (td.kind == T_EXIT) break;
     if (td.kind == T_GEMM) {
-      ptx::mbar_wait_abortable(&W.acc_empty[b], b_phase ^ 1, &P.ctrl->abort);
+      // both CTAs' epilogues have drained accumulator b
+      ptx::mbar_wait_cluster(&W.acc_empty[b], b_phase ^ 1, &P.ctrl->abort);
       ptx::tc_fence_after();
       const uint32_t tacc = tmem + b * ACC_COLS, idesc = td.idesc, nk = td.nk;
       const uint32_t a_lbo = td.a.mn ? 8192u : 16u, b_lbo = td.b.mn ? 8192u : 16u;
       const uint32_t a_step = td.a.mn ? 2048u : 32u, b_step = td.b.mn ? 2048u : 32u;
       for (uint32_t kc = 0; kc < nk; kc++) {
         ptx::mbar_wait_abortable(&W.full[s], s_phase, &P.ctrl->abort);
+        ptx::mbar_wait_cluster(&W.pair_full[s], s_phase, &P.ctrl->abort);
+#if SALUS_DBG_CHUNKS   // MMA thread: last chunk landed in both CTAs
+        if (kc + 1 == nk) const_cast<TileDesc &>(td).t_end = ptx::globaltimer();
+#endif
         ptx::tc_fence_after();
         const uint32_t sa = ptx::smem_u32(W.stage[s]), sb = sa + STAGE_A_BYTES;
 #pragma unroll
@@ -565,13 +670,32 @@ __device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
           const uint64_t bd = ptx::smem_desc_sw128(sb + ks * b_step, b_lbo, 1024);
           ptx::mma_bf16(tacc, ad, bd, idesc, (kc | ks) != 0);
         }
-        ptx::mma_commit(&W.empty[s]);
+        ptx::mma_commit_pair(&W.empty[s]);
         if (++s == PIPE) { s = 0; s_phase ^= 1; }
       }
-      ptx::mma_commit(&W.acc_full[b]);
+      ptx::mma_commit_pair(&W.acc_full[b]);
       if (++b == 2) { b = 0; b_phase ^= 1; }
     }
-    ptx::mbar_arrive(&W.desc_empty[d]);
+    release_desc(W, d);
+    if (++d == NDESC) { d = 0; d_phase ^= 1; }
+  }
+}
+
+// Peer: tells the leader's MMA thread when each K-chunk has landed here.
+__device__ void pair_forwarder(const Params &P, WorkerSmem &W) {
+  uint32_t d = 0, d_phase = 0, s = 0, s_phase = 0;
+  for (;;) {
+    ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
+    const TileDesc &td = W.desc[d];
+    if (td.kind == T_EXIT) break;
+    if (td.kind == T_GEMM) {
+      for (uint32_t kc = 0, nk = td.nk; kc < nk; kc++) {
+        ptx::mbar_wait_abortable(&W.full[s], s_phase, &P.ctrl->abort);
+        ptx::mbar_arrive_remote(&W.pair_full[s], 0);
+        if (++s == PIPE) { s = 0; s_phase ^= 1; }
+      }
+    }
+    release_desc(W, d);
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
 }
@@ -580,43 +704,67 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
                                unsigned long long &my_tasks) {
   const uint32_t warp = tid >> 5, lane = tid & 31;
   const uint32_t r = ((warp & 3u) << 5) | lane;   // TMEM lane quarter = warp % 4
+  const uint32_t h = (warp - EPI_WARP0) >> 2;     // column half (8 epilogue warps)
   const uint32_t et = tid - 32 * EPI_WARP0;       // 0..EPI_THREADS-1
   uint32_t d = 0, d_phase = 0, b = 0, b_phase = 0, e = 0, e_phase = 0;
   for (;;) {
     ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
     const TileDesc &td = W.desc[d];
     if (td.kind == T_EXIT) break;
-    my_tasks++;
+    if (td.valid) my_tasks++;
     const uint64_t t_ready = ptx::globaltimer();
     uint64_t t_mma = t_ready;
     if (td.kind == T_GEMM) {
       const EpiView ev = {td.m0, td.n0, td.rows_valid, td.cols_valid, td.ld_logical, td.epi, td.lr, td.key,
                           td.dump_off};
       const uint32_t ncc = td.N / 32, n = td.n_ech;
-      ptx::mbar_wait_abortable(&W.acc_full[b], b_phase, &P.ctrl->abort);
+      ptx::mbar_wait_cluster(&W.acc_full[b], b_phase, &P.ctrl->abort);
       ptx::tc_fence_after();
       t_mma = ptx::globaltimer();
       const uint32_t tacc = tmem + b * ACC_COLS;
-      if (n == 0) {
-        epilogue_cols(P, td, ev, tacc, r, 0, ncc, nullptr);
+      if (!td.valid) {
+        // the peer half of a super-tile past the last M block: nothing to store
+      } else if (n == 0) {
+        const uint32_t sub = ncc / EPI_HALVES;
+        epilogue_cols(P, td, ev, tacc, r, 0, h * sub, (h + 1) * sub, nullptr);
       } else {
         const uint32_t per = ncc / n;                 // column blocks per input chunk
+        const uint32_t sub = per / EPI_HALVES;
         for (uint32_t c = 0; c < n; c++) {
           ptx::mbar_wait_abortable(&W.epi_full[e], e_phase, &P.ctrl->abort);
-          epilogue_cols(P, td, ev, tacc, r, c * per, (c + 1) * per, W.epi_in[e]);
+          epilogue_cols(P, td, ev, tacc, r, c * per, c * per + h * sub, c * per + (h + 1) * sub, W.epi_in[e]);
+#if SALUS_SGD_BULK
+          const bool sgd = ev.epi == EPI_SGD;
+          if (sgd) ptx::fence_proxy_async_smem();     // smem writes -> async-proxy reader
+#endif
           named_bar(1, EPI_THREADS);                  // every thread is done with this chunk
-          if (et == 0) ptx::mbar_arrive(&W.epi_empty[e]);
+          if (et == 0) {
+#if SALUS_SGD_BULK
+            if (sgd) {                                // updated W32 chunk -> its page
+              ptx::bulk_s2g(td.ptr[PTR_W32 + (c >> 1)] + (c & 1) * 32768u, W.epi_in[e], ECH_BYTES);
+              ptx::bulk_commit();
+              ptx::bulk_wait_read0();
+            }
+#endif
+            ptx::mbar_arrive(&W.epi_empty[e]);
+          }
           if (++e == 2) { e = 0; e_phase ^= 1; }
         }
       }
       ptx::tc_fence_before();
       named_bar(1, EPI_THREADS);
-      if (et == 0) ptx::mbar_arrive(&W.acc_empty[b]);
+      if (et == 0) {
+        ptx::mbar_arrive_remote(&W.acc_empty[b], 0);  // the leader's MMA may reuse it
+#if SALUS_SGD_BULK
+        if (n != 0) ptx::bulk_wait0();                // bulk stores complete before the handoff
+#endif
+      }
       if (++b == 2) { b = 0; b_phase ^= 1; }
+    } else if (!td.valid) {
     } else if (td.kind == T_INIT) {
-      init_tile(td, r);
+      init_tile(td, r, h);
     } else {
-      gen_tile(td, r);
+      gen_tile(td, r, h);
     }
     // hand the tile to the completion warp: all epilogue stores are issued
     // before the CTA barrier; the completion thread's gpu-scope fence after
@@ -624,7 +772,11 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
     ptx::fence_proxy_async_global();
     named_bar(1, EPI_THREADS);
     if (et == 0) {
+#if !SALUS_DBG_CHUNKS
       W.desc[d].t_ready = t_ready; W.desc[d].t_mma = t_mma; W.desc[d].t_end = ptx::globaltimer();
+#else
+      (void)t_ready; (void)t_mma;
+#endif
       ptx::mbar_arrive(&W.epi_done[d]);
     }
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
@@ -632,7 +784,8 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
 }
 
 // Completion warp: per tile, in order — fence, stage counter, and publication
-// of the next stage's tiles or (last stage) the slot's next iteration.
+// of the next stage's tiles or (last stage) the slot's next iteration.  Each
+// CTA of the pair counts its half: a stage of n pair tasks is complete at 2n.
 __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
   uint32_t d = 0, d_phase = 0;
   for (;;) {
@@ -644,7 +797,7 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
     unsigned long long pb = 0;
     if (lane == 0) {
       __threadfence();
-      if (P.flags & SALUS_FLAG_TRACE) {
+      if ((P.flags & SALUS_FLAG_TRACE) && td.valid) {
         const unsigned long long i = atomicAdd(&P.ctrl->n_trace, 1ull);
         if (i < P.trace_cap) {
           uint32_t smid;
@@ -657,7 +810,7 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
       }
       Slot &sl = P.slots[td.slot];
       const uint32_t old = ptx::atom_add_acqrel_u32(&sl.stage_done[td.stage], 1u);
-      if (old + 1 == td.ntiles) {
+      if (old + 1 == 2 * td.ntiles) {
         if (td.is_last) {                      // the iteration is physically complete
           const uint64_t end = ptx::globaltimer(), start = sl.start_ns;
           sl.end_ns = end;
@@ -695,27 +848,34 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
       }
     }
     __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&W.desc_empty[d]);
+    if (lane == 0) release_desc(W, d);
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
 }
 
 __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
-  const uint32_t base = ptx::smem_u32(smem_raw);
-  WorkerSmem &W = *reinterpret_cast<WorkerSmem *>(smem_raw + (((base + 1023u) & ~1023u) - base));
+  // the dynamic smem window starts 1 KiB-aligned (no static smem); the
+  // SWIZZLE_128B operand stages rely on it, and there is no room for slack
+  if (ptx::smem_u32(smem_raw) & 1023u) __trap();
+  WorkerSmem &W = *reinterpret_cast<WorkerSmem *>(smem_raw);
   const uint32_t tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t h = ptx::cluster_ctarank();
 
   if (tid == 0) {
-    for (uint32_t s = 0; s < PIPE; s++) { ptx::mbar_init(&W.full[s], 1); ptx::mbar_init(&W.empty[s], 1); }
-    // a descriptor is released by its 4 consumers: operand loader, epilogue-
-    // input loader, MMA thread, completion warp (after the epilogue is done)
+    for (uint32_t s = 0; s < PIPE; s++) {
+      ptx::mbar_init(&W.full[s], 1); ptx::mbar_init(&W.empty[s], 1); ptx::mbar_init(&W.pair_full[s], 1);
+    }
+    // (leader) a descriptor is released by its 4 consumers in each CTA:
+    // operand loader, epilogue-input loader, MMA / forwarder thread,
+    // completion warp (after the epilogue is done)
     for (uint32_t d = 0; d < NDESC; d++) {
       ptx::mbar_init(&W.desc_full[d], 1);
-      ptx::mbar_init(&W.desc_empty[d], 4);
+      ptx::mbar_init(&W.desc_empty[d], 8);
       ptx::mbar_init(&W.epi_done[d], 1);
+      ptx::mbar_init(&W.mail_full[d], 1);
     }
     for (uint32_t b = 0; b < 2; b++) {
-      ptx::mbar_init(&W.acc_full[b], 1); ptx::mbar_init(&W.acc_empty[b], 1);
+      ptx::mbar_init(&W.acc_full[b], 1); ptx::mbar_init(&W.acc_empty[b], 2);
       ptx::mbar_init(&W.epi_full[b], 1); ptx::mbar_init(&W.epi_empty[b], 1);
     }
     ptx::fence_mbar_init();
@@ -723,16 +883,17 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
   if (warp == 2) { ptx::tmem_alloc(&W.tmem_base, TMEM_COLS); ptx::tmem_relinquish(); }
   ptx::tc_fence_before();
   __syncthreads();
+  ptx::cluster_sync();           // the peer's barriers exist before any remote arrive
   ptx::tc_fence_after();
   const uint32_t tmem = W.tmem_base;
   unsigned long long my_tasks = 0;
 
   if (warp == 0) {
-    decoder_warp(P, W, lane);
+    decoder_warp(P, W, lane, h);
   } else if (warp < EPI_WARP0) {
     if (lane == 0) {
       if (warp == 1) operand_loader(P, W);
-      else if (warp == 2) mma_thread(P, W, tmem);
+      else if (warp == 2) { if (h == 0) mma_thread(P, W, tmem); else pair_forwarder(P, W); }
       else epi_loader(P, W);
     }
     __syncwarp();
@@ -743,6 +904,9 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
   }
   __syncthreads();
   if (tid == 32 * EPI_WARP0) atomicAdd(&P.ctrl->n_tasks, my_tasks);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();           // no remote smem / TMEM traffic after this point
+  ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc(tmem, TMEM_COLS);
 }
 

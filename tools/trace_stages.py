@@ -1,5 +1,5 @@
 """Per-stage timeline of one config from the device tile trace.
-usage: python tools/trace_stages.py c1|c2s [policy]"""
+usage: python tools/trace_stages.py c1|c2s|c2one [policy]"""
 import os, sys
 sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), ".."))
 import numpy as np
@@ -8,7 +8,8 @@ from workloads import c1_trace, c2_trace
 build.build()
 name = sys.argv[1]
 pol = {"fifo": S.FIFO, "srtf": S.SRTF, "pack": S.PACK}[sys.argv[2] if len(sys.argv) > 2 else "fifo"]
-jobs, cap = c1_trace() if name == "c1" else c2_trace("a", n_jobs=37, n_iters=10)
+jobs, cap = (c1_trace() if name == "c1" else c2_trace("a", n_jobs=1, n_iters=20) if name == "c2one"
+             else c2_trace("a", n_jobs=37, n_iters=10))
 ctx = S.Context(jobs, cap, pol, trace=True)
 for rep in range(2):
     ctx.run()
