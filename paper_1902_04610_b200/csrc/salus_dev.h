@@ -130,7 +130,7 @@ __host__ __device__ inline uint32_t last_stage(uint32_t kind, uint32_t L) {
 
 // GEMM N tile for an output width (padded to 128): 256 when it divides, else
 // 128.  Wide tiles halve operand re-reads; the epilogue streams its input
-// (fp32 master weights / ReLU mask) through two 32 KiB smem chunk buffers.
+// (fp32 master weights / ReLU mask) through four 32 KiB smem chunk buffers.
 __host__ __device__ inline uint32_t ntile_for(uint32_t dpad) { return (dpad % 256 == 0) ? 256 : 128; }
 
 }  // namespace salus

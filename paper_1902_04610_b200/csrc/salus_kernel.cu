@@ -8,6 +8,7 @@
 // accesses".
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include "salus_dev.h"
 #include "scheduler.cuh"
 #include "worker.cuh"
@@ -59,7 +60,12 @@ int launch_persistent(const Params &P, uint32_t grid, cudaStream_t stream) {
                                        (int)smem);
   if (e != cudaSuccess) return (int)e;
   cudaLaunchAttribute attrs[2];
-  cudaLaunchConfig_t cfg = pair_config(grid, smem, stream, attrs, true);
+  // SALUS_COOP=0 (diagnostics, e.g. under ncu, whose replay refuses
+  // cooperative cluster launches): plain cluster launch; `grid` still fits
+  // one wave (max_coresident_grid), so all CTAs are resident together.
+  const char *coop = getenv("SALUS_COOP");
+  const bool cooperative = !(coop && coop[0] == '0');
+  cudaLaunchConfig_t cfg = pair_config(grid, smem, stream, attrs, cooperative);
   e = cudaLaunchKernelEx(&cfg, salus_persistent_kernel, P);
   return (int)e;
 }

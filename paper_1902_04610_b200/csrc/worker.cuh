@@ -14,7 +14,7 @@
 //              translates the epilogue's page addresses, lanes in parallel.
 //   warp 1     operand loader (1 thread): issues every K-chunk of the A/B
 //              operands as bulk async copies (cp.async.bulk, TMA unit) into a
-//              5-stage mbarrier ring (page-table reads two chunks ahead).
+//              3-stage mbarrier ring (page-table reads two chunks ahead).
 //   warp 2     leader: MMA (1 thread): tcgen05.mma.cta_group::2 kind::f16
 //              (bf16 in, fp32 accumulate) into one of two TMEM accumulators
 //              of 256 columns in both CTAs (double buffered: the epilogue of
@@ -22,7 +22,7 @@
 //              landed K-chunk of its smem to the leader's pair_full barrier.
 //   warp 3     epilogue-input loader (1 thread): streams the tile's epilogue
 //              input (fp32 master weights of a dW tile, ReLU mask of a dX
-//              tile) in 32 KiB chunks through two smem buffers.
+//              tile) in 32 KiB chunks through four smem buffers.
 //   warps 4-11 epilogue: drain TMEM (tcgen05.ld), fused epilogue, stores.
 //   warp 12    completion: gpu-scope fence, stage accounting, publication of
 //              the next stage / start of the slot's next iteration (run-ahead)
@@ -44,13 +44,19 @@
 namespace salus {
 
 #ifndef SALUS_PIPE
-#define SALUS_PIPE 5
+#define SALUS_PIPE 3
 #endif
 constexpr uint32_t PIPE = SALUS_PIPE;                 // operand stages in flight
 constexpr uint32_t STAGE_A_BYTES = 16384;             // 128 x 64 bf16 (this CTA's rows)
 constexpr uint32_t STAGE_B_BYTES = 16384;             // <= 128 x 64 bf16 (this CTA's half of N)
 constexpr uint32_t STAGE_BYTES = STAGE_A_BYTES + STAGE_B_BYTES;
 constexpr uint32_t ECH_BYTES = 32768;                 // epilogue-input chunk
+#ifndef SALUS_EBUF
+#define SALUS_EBUF 4
+#endif
+// epilogue-input chunk buffers: 4 hold a whole 128 x 256 fp32 master tile,
+// so its HBM read overlaps the tile's MMA instead of the epilogue
+constexpr uint32_t EBUF = SALUS_EBUF;
 #ifndef SALUS_NDESC
 #define SALUS_NDESC 4
 #endif
@@ -70,9 +76,6 @@ constexpr uint32_t DONE_WARP = EPI_WARP0 + EPI_WARPS;          // completion war
 constexpr uint32_t WORKER_THREADS = 32 * (DONE_WARP + 1);
 constexpr uint32_t ACC_COLS = 256;
 constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;          // all of TMEM: 2 accumulators
-#ifndef SALUS_SGD_BULK
-#define SALUS_SGD_BULK 1   // SGD epilogue writes W32 back in smem, one bulk store per chunk
-#endif
 
 enum : uint32_t { T_EXIT = 0, T_INIT = 1, T_GEN = 2, T_GEMM = 3 };
 enum : uint32_t { EPI_RELU = 0, EPI_OUT = 1, EPI_LOSS = 2, EPI_DX = 3, EPI_SGD = 4 };
@@ -84,6 +87,11 @@ struct OpDesc {
   const uint32_t *table;   // page table of the operand's space
   uint32_t off, R, start, mn;
 };
+
+#ifndef SALUS_L2HINT
+#define SALUS_L2HINT 1
+#endif
+
 
 struct TileDesc {
   uint32_t kind, payload, slot, stage, job, iter, ntiles, next_ntiles, is_last, first_stage;
@@ -106,12 +114,12 @@ struct TileDesc {
 
 struct WorkerSmem {
   uint8_t stage[PIPE][STAGE_BYTES];   // 1024-aligned (first member)
-  uint8_t epi_in[2][ECH_BYTES];       // 1024-aligned
+  uint8_t epi_in[EBUF][ECH_BYTES];    // 1024-aligned
   TileDesc desc[NDESC];
   uint64_t full[PIPE], empty[PIPE];
   uint64_t desc_full[NDESC], desc_empty[NDESC];
   uint64_t acc_full[2], acc_empty[2];
-  uint64_t epi_full[2], epi_empty[2];
+  uint64_t epi_full[EBUF], epi_empty[EBUF];
   uint64_t epi_done[NDESC];           // epilogue -> completion warp
   uint64_t pair_full[PIPE];           // leader: the peer's K-chunk has landed
   uint64_t mail_full[NDESC];          // peer: the leader mailed task d
@@ -157,7 +165,9 @@ __device__ __forceinline__ uint4 shfl_xor_u4(uint4 v, int m) {
 // instruction write 8 rows x 64 contiguous bytes (the swizzle keeps a
 // row-half's 4 chunks inside one 64-byte half) instead of 32 rows x 16 bytes.
 // `r` = this lane's row in the tile (warp-uniform quarter base + lane).
-__device__ __forceinline__ void store_bf16_rows(uint8_t *panel, uint4 (&u)[4], uint32_t r, uint32_t ch0) {
+template <bool kStream = false>
+__device__ __forceinline__ void store_bf16_rows(uint8_t *panel, uint4 (&u)[4], uint32_t r, uint32_t ch0,
+                                                uint64_t policy = 0) {
   const uint32_t lane = r & 31u, base = r & ~31u;
   const bool b0 = lane & 1u, b1 = lane & 2u;
 #pragma unroll
@@ -173,7 +183,10 @@ __device__ __forceinline__ void store_bf16_rows(uint8_t *panel, uint4 (&u)[4], u
   // lane now holds chunk c = lane & 3 of rows 4*(lane>>2) + k, k = 0..3
   const uint32_t c = ch0 + (lane & 3u), g = base + 4u * (lane >> 2);
 #pragma unroll
-  for (int k = 0; k < 4; k++) *reinterpret_cast<uint4 *>(panel + swz(g + k, c)) = u[k];
+  for (int k = 0; k < 4; k++) {
+    if (kStream) ptx::st_global_v4_hint(panel + swz(g + k, c), u[k], policy);
+    else *reinterpret_cast<uint4 *>(panel + swz(g + k, c)) = u[k];
+  }
 }
 
 __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
@@ -354,18 +367,23 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
     const uint32_t pan = cc >> 1, ch0 = (cc & 1) * 4;
     if (td.epi == EPI_SGD) {
       // rows are j (d_l), columns i (d_{l-1}): W32[j][i] -= lr * dW^T[j][i]
+#if SALUS_L2HINT
+      const uint64_t pol_stream = ptx::policy_evict_first();   // masters + Wb: streamed
+#endif
 #pragma unroll
       for (int g = 0; g < 8; g++) {
         const uint32_t grp = cc * 8 + g;                    // float4 column group in the tile
-        float4 *wp = reinterpret_cast<float4 *>(buf + ((cc - ccb) * 8 + g) * 2048u + r * 16u);
+        const float4 *wp = reinterpret_cast<const float4 *>(buf + ((cc - ccb) * 8 + g) * 2048u + r * 16u);
         float4 w = *wp;
         w.x = fmaf(-td.lr, v[4 * g + 0], w.x);
         w.y = fmaf(-td.lr, v[4 * g + 1], w.y);
         w.z = fmaf(-td.lr, v[4 * g + 2], w.z);
         w.w = fmaf(-td.lr, v[4 * g + 3], w.w);
-#if SALUS_SGD_BULK
-        *wp = w;                                            // written back by one bulk store
-        (void)grp;
+#if SALUS_L2HINT
+        ptx::st_global_v4_hint(tds.ptr[PTR_W32 + (grp >> 5)] + (grp & 31u) * 2048u + r * 16u,
+                               make_uint4(__float_as_uint(w.x), __float_as_uint(w.y), __float_as_uint(w.z),
+                                          __float_as_uint(w.w)),
+                               pol_stream);
 #else
         *reinterpret_cast<float4 *>(tds.ptr[PTR_W32 + (grp >> 5)] + (grp & 31u) * 2048u + r * 16u) = w;
 #endif
@@ -380,7 +398,11 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
           u[q].z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
           u[q].w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
         }
+#if SALUS_L2HINT
+        store_bf16_rows<true>(tds.ptr[PTR_AUX + pan], u, r, ch0, pol_stream);
+#else
         store_bf16_rows(tds.ptr[PTR_AUX + pan], u, r, ch0);
+#endif
       }
       if (dump && row_ok) {                     // W[i][j], logical d_{l-1} x d_l
         for (int x = 0; x < 32; x++)
@@ -492,6 +514,12 @@ __device__ void gen_tile(const TileDesc &td, uint32_t r, uint32_t h) {
 // ---------------------------------------------------------------------------
 // Roles
 // ---------------------------------------------------------------------------
+// Barrier scopes: waits on barriers the peer CTA (or the pair's MMA commit)
+// arrives on use CTA-scope try_wait like CUTLASS's cluster barriers -- the
+// data they guard is shared memory / TMEM written by the async proxy, and a
+// cluster-scope acquire would invalidate the SM's L1 on every wait.  Only the
+// mailbox (a generic st.shared::cluster from the leader) is acquired at
+// cluster scope.
 // Every consumer of descriptor slot d, in both CTAs, releases it on the
 // leader's desc_empty[d] (8 arrivals per use): the leader mails task d only
 // when the slot is free in both CTAs.
@@ -504,13 +532,18 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint
     uint32_t payload = TASK_EXIT;
     uint64_t t_claim = 0;
     if (h == 0) {                             // leader: claim, mail to the peer
-      ptx::mbar_wait_cluster(&W.desc_empty[d], d_phase ^ 1, &P.ctrl->abort);
+      ptx::mbar_wait_abortable(&W.desc_empty[d], d_phase ^ 1, &P.ctrl->abort);
       if (lane == 0) {
         const unsigned long long pos = atomicAdd(&P.ctrl->q_tail, 1ull);
         uint32_t spins = 0;
+        // spin relaxed (an acquire load invalidates the SM's L1 every time),
+        // then one acquire load of the published entry
         for (;;) {
-          const unsigned long long v = ptx::ld_acquire_u64(&P.ring[pos & P.ring_mask]);
-          if ((uint32_t)(v >> 32) == (uint32_t)(pos + 1)) { payload = (uint32_t)v; break; }
+          const unsigned long long v = ptx::ld_relaxed_u64(&P.ring[pos & P.ring_mask]);
+          if ((uint32_t)(v >> 32) == (uint32_t)(pos + 1)) {
+            payload = (uint32_t)ptx::ld_acquire_u64(&P.ring[pos & P.ring_mask]);
+            break;
+          }
           if ((++spins & 255) == 0 && *(volatile uint32_t *)&P.ctrl->abort) break;
         }
         t_claim = ptx::globaltimer();
@@ -579,6 +612,8 @@ __device__ __forceinline__ const uint8_t *page_ptr(const Params &P, uint32_t pag
 // per-chunk critical path.
 __device__ void operand_loader(const Params &P, WorkerSmem &W) {
   uint32_t d = 0, d_phase = 0, s = 0, s_phase = 0;
+  const uint64_t first = ptx::policy_evict_first(), last = ptx::policy_evict_last();
+  const uint64_t normal = ptx::policy_evict_normal();
   for (;;) {
     ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
     const TileDesc &td = W.desc[d];
@@ -587,6 +622,13 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W) {
       const OpDesc a = td.a, b = td.b;
       const uint32_t nk = td.nk, nca = td.ncopy_a, ncb = td.ncopy_b, ab = td.abytes, bb = td.bbytes;
       const uint32_t tx = nca * ab + ncb * bb;
+      const uint32_t *jt = P.ppt + P.jobs[td.job].pt_off;
+      // weights (the job's persistent space) stream; a lane's activations stay
+#if SALUS_L2HINT
+      const uint64_t pol_a = a.table == jt ? first : last, pol_b = b.table == jt ? first : last;
+#else
+      const uint64_t pol_a = normal, pol_b = normal;
+#endif
       ChunkPages p0 = chunk_pages(a, b, nca, ncb, 0);
       ChunkPages p1 = nk > 1 ? chunk_pages(a, b, nca, ncb, 1) : p0;
       for (uint32_t kc = 0; kc < nk; kc++) {
@@ -594,13 +636,13 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W) {
         p0 = p1;
         if (kc + 2 < nk) p1 = chunk_pages(a, b, nca, ncb, kc + 2);
         // stage s is free once the pair's MMA has consumed it (multicast commit)
-        ptx::mbar_wait_cluster(&W.empty[s], s_phase ^ 1, &P.ctrl->abort);
+        ptx::mbar_wait_abortable(&W.empty[s], s_phase ^ 1, &P.ctrl->abort);
         ptx::mbar_arrive_expect_tx(&W.full[s], tx);
         uint8_t *sa = W.stage[s], *sb = W.stage[s] + STAGE_A_BYTES;
-        if (nca > 0) ptx::bulk_g2s(sa, page_ptr(P, cur.a0, copy_off(a, kc, 0)), ab, &W.full[s]);
-        if (nca > 1) ptx::bulk_g2s(sa + ab, page_ptr(P, cur.a1, copy_off(a, kc, 1)), ab, &W.full[s]);
-        if (ncb > 0) ptx::bulk_g2s(sb, page_ptr(P, cur.b0, copy_off(b, kc, 0)), bb, &W.full[s]);
-        if (ncb > 1) ptx::bulk_g2s(sb + bb, page_ptr(P, cur.b1, copy_off(b, kc, 1)), bb, &W.full[s]);
+        if (nca > 0) ptx::bulk_g2s_hint(sa, page_ptr(P, cur.a0, copy_off(a, kc, 0)), ab, &W.full[s], pol_a);
+        if (nca > 1) ptx::bulk_g2s_hint(sa + ab, page_ptr(P, cur.a1, copy_off(a, kc, 1)), ab, &W.full[s], pol_a);
+        if (ncb > 0) ptx::bulk_g2s_hint(sb, page_ptr(P, cur.b0, copy_off(b, kc, 0)), bb, &W.full[s], pol_b);
+        if (ncb > 1) ptx::bulk_g2s_hint(sb + bb, page_ptr(P, cur.b1, copy_off(b, kc, 1)), bb, &W.full[s], pol_b);
 #if SALUS_DBG_CHUNKS   // trace fields re-purposed: loader issue of chunk 0 / last chunk
         if (kc == 0) const_cast<TileDesc &>(td).t_ready = ptx::globaltimer();
         if (kc + 1 == nk) const_cast<TileDesc &>(td).t_mma = ptx::globaltimer();
@@ -617,6 +659,11 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W) {
 // [64c, 64c+64) (half of a 64 KiB page); DX chunk c = mask panels 2c, 2c+1.
 __device__ void epi_loader(const Params &P, WorkerSmem &W) {
   uint32_t d = 0, d_phase = 0, e = 0, e_phase = 0;
+#if SALUS_L2HINT
+  const uint64_t pol_w = ptx::policy_evict_first(), pol_a = ptx::policy_evict_last();
+#else
+  const uint64_t pol_w = ptx::policy_evict_normal(), pol_a = pol_w;
+#endif
   for (;;) {
     ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
     const TileDesc &td = W.desc[d];
@@ -628,12 +675,13 @@ __device__ void epi_loader(const Params &P, WorkerSmem &W) {
         ptx::mbar_wait_abortable(&W.epi_empty[e], e_phase ^ 1, &P.ctrl->abort);
         ptx::mbar_arrive_expect_tx(&W.epi_full[e], ECH_BYTES);
         if (sgd) {
-          ptx::bulk_g2s(W.epi_in[e], td.ptr[PTR_W32 + (c >> 1)] + (c & 1) * 32768u, ECH_BYTES, &W.epi_full[e]);
+          ptx::bulk_g2s_hint(W.epi_in[e], td.ptr[PTR_W32 + (c >> 1)] + (c & 1) * 32768u, ECH_BYTES, &W.epi_full[e],
+                             pol_w);
         } else {
-          ptx::bulk_g2s(W.epi_in[e], td.ptr[PTR_EPI + 2 * c], 16384u, &W.epi_full[e]);
-          ptx::bulk_g2s(W.epi_in[e] + 16384u, td.ptr[PTR_EPI + 2 * c + 1], 16384u, &W.epi_full[e]);
+          ptx::bulk_g2s_hint(W.epi_in[e], td.ptr[PTR_EPI + 2 * c], 16384u, &W.epi_full[e], pol_a);
+          ptx::bulk_g2s_hint(W.epi_in[e] + 16384u, td.ptr[PTR_EPI + 2 * c + 1], 16384u, &W.epi_full[e], pol_a);
         }
-        if (++e == 2) { e = 0; e_phase ^= 1; }
+        if (++e == EBUF) { e = 0; e_phase ^= 1; }
       }
     }
     release_desc(W, d);
@@ -651,14 +699,14 @@ __device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
     if (td.kind == T_EXIT) break;
     if (td.kind == T_GEMM) {
       // both CTAs' epilogues have drained accumulator b
-      ptx::mbar_wait_cluster(&W.acc_empty[b], b_phase ^ 1, &P.ctrl->abort);
+      ptx::mbar_wait_abortable(&W.acc_empty[b], b_phase ^ 1, &P.ctrl->abort);
       ptx::tc_fence_after();
       const uint32_t tacc = tmem + b * ACC_COLS, idesc = td.idesc, nk = td.nk;
       const uint32_t a_lbo = td.a.mn ? 8192u : 16u, b_lbo = td.b.mn ? 8192u : 16u;
       const uint32_t a_step = td.a.mn ? 2048u : 32u, b_step = td.b.mn ? 2048u : 32u;
       for (uint32_t kc = 0; kc < nk; kc++) {
         ptx::mbar_wait_abortable(&W.full[s], s_phase, &P.ctrl->abort);
-        ptx::mbar_wait_cluster(&W.pair_full[s], s_phase, &P.ctrl->abort);
+        ptx::mbar_wait_abortable(&W.pair_full[s], s_phase, &P.ctrl->abort);
 #if SALUS_DBG_CHUNKS   // MMA thread: last chunk landed in both CTAs
         if (kc + 1 == nk) const_cast<TileDesc &>(td).t_end = ptx::globaltimer();
 #endif
@@ -718,7 +766,7 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
       const EpiView ev = {td.m0, td.n0, td.rows_valid, td.cols_valid, td.ld_logical, td.epi, td.lr, td.key,
                           td.dump_off};
       const uint32_t ncc = td.N / 32, n = td.n_ech;
-      ptx::mbar_wait_cluster(&W.acc_full[b], b_phase, &P.ctrl->abort);
+      ptx::mbar_wait_abortable(&W.acc_full[b], b_phase, &P.ctrl->abort);
       ptx::tc_fence_after();
       t_mma = ptx::globaltimer();
       const uint32_t tacc = tmem + b * ACC_COLS;
@@ -733,32 +781,14 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
         for (uint32_t c = 0; c < n; c++) {
           ptx::mbar_wait_abortable(&W.epi_full[e], e_phase, &P.ctrl->abort);
           epilogue_cols(P, td, ev, tacc, r, c * per, c * per + h * sub, c * per + (h + 1) * sub, W.epi_in[e]);
-#if SALUS_SGD_BULK
-          const bool sgd = ev.epi == EPI_SGD;
-          if (sgd) ptx::fence_proxy_async_smem();     // smem writes -> async-proxy reader
-#endif
-          named_bar(1, EPI_THREADS);                  // every thread is done with this chunk
-          if (et == 0) {
-#if SALUS_SGD_BULK
-            if (sgd) {                                // updated W32 chunk -> its page
-              ptx::bulk_s2g(td.ptr[PTR_W32 + (c >> 1)] + (c & 1) * 32768u, W.epi_in[e], ECH_BYTES);
-              ptx::bulk_commit();
-              ptx::bulk_wait_read0();
-            }
-#endif
-            ptx::mbar_arrive(&W.epi_empty[e]);
-          }
-          if (++e == 2) { e = 0; e_phase ^= 1; }
+          __syncwarp();                               // each warp releases the chunk on its own
+          if (lane == 0) ptx::mbar_arrive(&W.epi_empty[e]);
+          if (++e == EBUF) { e = 0; e_phase ^= 1; }
         }
       }
       ptx::tc_fence_before();
       named_bar(1, EPI_THREADS);
-      if (et == 0) {
-        ptx::mbar_arrive_remote(&W.acc_empty[b], 0);  // the leader's MMA may reuse it
-#if SALUS_SGD_BULK
-        if (n != 0) ptx::bulk_wait0();                // bulk stores complete before the handoff
-#endif
-      }
+      if (et == 0) ptx::mbar_arrive_remote(&W.acc_empty[b], 0);  // the leader's MMA may reuse it
       if (++b == 2) { b = 0; b_phase ^= 1; }
     } else if (!td.valid) {
     } else if (td.kind == T_INIT) {
@@ -874,10 +904,8 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
       ptx::mbar_init(&W.epi_done[d], 1);
       ptx::mbar_init(&W.mail_full[d], 1);
     }
-    for (uint32_t b = 0; b < 2; b++) {
-      ptx::mbar_init(&W.acc_full[b], 1); ptx::mbar_init(&W.acc_empty[b], 2);
-      ptx::mbar_init(&W.epi_full[b], 1); ptx::mbar_init(&W.epi_empty[b], 1);
-    }
+    for (uint32_t b = 0; b < 2; b++) { ptx::mbar_init(&W.acc_full[b], 1); ptx::mbar_init(&W.acc_empty[b], 2); }
+    for (uint32_t e = 0; e < EBUF; e++) { ptx::mbar_init(&W.epi_full[e], 1); ptx::mbar_init(&W.epi_empty[e], EPI_WARPS); }
     ptx::fence_mbar_init();
   }
   if (warp == 2) { ptx::tmem_alloc(&W.tmem_base, TMEM_COLS); ptx::tmem_relinquish(); }
