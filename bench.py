@@ -133,20 +133,29 @@ def switch_latency(S, device):
     w = ctx.wall()
     ctx.close()
     w = w[np.argsort(w["seq"])]
-    sw, gap, last = [], [], {}
+    sw, rdy, gap, last = [], [], [], {}
     for r in w:
         ln = int(r["lane"])
         if ln in last:
             prev = last[ln]
             d = (int(r["start_ns"]) - int(prev["end_ns"])) / 1e3
-            (gap if prev["job"] == r["job"] else sw).append(d)
+            if prev["job"] == r["job"]:
+                gap.append(d)
+            else:
+                sw.append(d)
+                # from the moment the switch could happen (previous iteration
+                # done AND the scheduler's dispatch appended) to the first tile
+                rdy.append((int(r["start_ns"]) - max(int(prev["end_ns"]), int(r["append_ns"]))) / 1e3)
         last[ln] = r
+
+    def pct(a):
+        return {"n": len(a), "p50": float(np.median(a)) if a else None,
+                "p99": float(np.percentile(a, 99)) if a else None}
     return {"config": "C3: 42 inference models (14 archs x 3), FAIR, 8 lanes, 16 GiB",
             "models_coresident": len(jobs), "requests": int(rs["n_dispatch"]),
             "requests_per_s": rs["n_dispatch"] / (rs["kernel_ns"] / 1e9),
-            "switch_us": {"n": len(sw), "p50": float(np.median(sw)) if sw else None,
-                          "p99": float(np.percentile(sw, 99)) if sw else None},
-            "same_job_gap_us": {"n": len(gap), "p50": float(np.median(gap)) if gap else None}}
+            "switch_us": pct(sw), "switch_from_ready_us": pct(rdy),
+            "same_job_gap_us": pct(gap)}
 
 
 def overhead_vs_standalone(S, device, dims=(1024, 1024, 1024, 1024), batch=256, iters=100):

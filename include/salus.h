@@ -104,11 +104,13 @@ enum {
 };
 
 /* Physical timing of one dispatched iteration (not part of the compared log):
- * globaltimer ns of its first tile start and last tile end. */
+ * globaltimer ns of its first tile start and last tile end, and of the
+ * scheduler's append of its dispatch record to the lane's ring. */
 typedef struct {
   uint64_t seq;
   uint32_t lane, job;
   uint64_t start_ns, end_ns;
+  uint64_t append_ns;
 } salus_wall_rec;
 
 /* ---------------------------------------------------------------------
@@ -225,6 +227,8 @@ typedef struct {
   uint32_t n_workers;         /* worker CTA pairs                                 */
   uint64_t h2d_bytes;         /* host->device bytes of salus_prepare (job tables) */
   uint64_t d2h_bytes;         /* device->host bytes read back by salus_run        */
+  uint64_t sched_fence_ns;    /* part of sched_wait_ns: page-reuse fences (A30)    */
+  uint64_t sched_ring_ns;     /* part of sched_wait_ns: a lane's dispatch ring full */
 } salus_run_stats;
 
 int salus_read_run_stats(const salus_ctx *ctx, salus_run_stats *out);

@@ -33,6 +33,7 @@ __device__ __forceinline__ bool take_next(Slot &sl, DispRec *rec) {
     if (h != t) {
       const volatile DispRec *vr = &sl.recs[h % RQ];
       rec->job = vr->job; rec->iter = vr->iter; rec->seq = vr->seq; rec->lane_id = vr->lane_id; rec->pad = 0;
+      rec->append_ns = vr->append_ns;
       st_release_u32(&sl.q_head, h + 1);
       return true;
     }
@@ -52,6 +53,7 @@ __device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec
   sl.iter = rec.iter;
   sl.seq = rec.seq;
   sl.lane_id = rec.lane_id;
+  sl.append_ns = rec.append_ns;
   sl.start_ns = ~0ull;
   sl.end_ns = 0;
   for (uint32_t k = 0; k < MAX_STAGES + 2; k++) sl.stage_done[k] = 0;

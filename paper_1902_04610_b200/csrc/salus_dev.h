@@ -48,12 +48,19 @@ struct DevJob {
 // Run-ahead execution (A30 mode 2): the scheduler appends dispatch records to
 // a per-slot ring; the thread that completes an iteration starts the slot's
 // next record itself, so a lane never waits for the scheduler.
-constexpr uint32_t RQ = 32;            // records queued per slot (run-ahead depth)
+#ifndef SALUS_RQ
+#define SALUS_RQ 4096
+#endif
+// records queued per slot (run-ahead depth): deep enough that the scheduler,
+// which emits dispatches in logical order, is never held back by one lane's
+// full ring while another lane runs dry (C3: 1k+ requests per lane)
+constexpr uint32_t RQ = SALUS_RQ;
 
 struct DispRec {
   uint32_t job, iter;                  // dense job index, iteration index
   uint64_t seq;                        // global dispatch seq
   uint32_t lane_id, pad;               // logical lane id (for the wall log)
+  uint64_t append_ns;                  // globaltimer of the scheduler's append
 };
 
 // One physical lane slot.  256-B aligned.
@@ -66,6 +73,7 @@ struct alignas(256) Slot {
   uint64_t end_ns;          // globaltimer when the last stage completed
   uint64_t done_seq;        // seq + 1 of the last physically completed iteration (monotonic)
   uint32_t lane_id;
+  uint64_t append_ns;       // when the in-flight iteration's record was appended
   uint32_t stage_done[MAX_STAGES + 2];
   // dispatch ring
   uint32_t q_tail;          // records appended (scheduler; release)
@@ -82,7 +90,7 @@ struct alignas(256) Ctrl {
   uint32_t abort;                // set on device error or host abort
   int32_t status;                // SALUS_OK or SALUS_E_*
   uint32_t err_info[4];
-  uint64_t n_dispatch, n_ticks, n_log, sched_wait_ns;
+  uint64_t n_dispatch, n_ticks, n_log, sched_wait_ns, sched_fence_ns, sched_ring_ns;
   uint64_t wall_first_ns, wall_last_ns;
   uint32_t log_overflow, n_workers;
   unsigned long long n_trace;

@@ -452,7 +452,7 @@ int salus_run(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_
   rs.n_dispatch = ctrl.n_dispatch; rs.n_ticks = ctrl.n_ticks; rs.n_log = std::min<uint64_t>(ctrl.n_log, ctx->log_cap);
   rs.n_tasks = ctrl.n_tasks; rs.kernel_ns = (uint64_t)((double)ms * 1e6);
   rs.wall_first_ns = ctrl.wall_first_ns; rs.wall_last_ns = ctrl.wall_last_ns;
-  rs.sched_wait_ns = ctrl.sched_wait_ns; rs.status = ctrl.status; rs.n_workers = ctx->grid / 2 - 1;
+  rs.sched_wait_ns = ctrl.sched_wait_ns; rs.sched_fence_ns = ctrl.sched_fence_ns; rs.sched_ring_ns = ctrl.sched_ring_ns; rs.status = ctrl.status; rs.n_workers = ctx->grid / 2 - 1;
   ctx->n_trace = std::min<uint64_t>(ctrl.n_trace, ctx->trace_cap);
   rs.h2d_bytes = ctx->h2d_bytes;
   rs.d2h_bytes = sizeof(Ctrl) + (stats ? sizeof(salus_job_stat) * ctx->jobs.size() : 0);

@@ -44,6 +44,17 @@ struct SchedShared {
   // run-ahead: records appended per physical slot, last appended seq + 1
   uint32_t sq_tail[MAX_LANES];
   uint64_t last_app[MAX_LANES];
+  // last appended seq + 1 of a record that may translate through the slot's
+  // page-table entries at or beyond the lane's current backing (set when the
+  // backing shrinks or the lane closes): growing into those entries waits
+  // for it, nothing else does
+  uint64_t tail_seq[MAX_LANES];
+  // static per-job data the per-tick loops read, cached from global memory
+  uint16_t infer[MAX_JOBS];                 // dense indices of INFER jobs, ascending
+  uint32_t req_off[MAX_JOBS];
+  // phase_dispatch: per-slot minimum dispatch key over runnable residents
+  unsigned long long slot_key[MAX_LANES];
+  uint32_t q_head_seen[MAX_LANES];          // last q_head read per slot (backpressure)
 };
 
 __device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
@@ -78,6 +89,7 @@ struct Sched {
   // warp-uniform scalar state
   int64_t t = 0;
   uint64_t seq = 0, n_log = 0, n_ticks = 0, wait_ns = 0;
+  uint64_t wait_fence_ns = 0, wait_ring_ns = 0;     // parts of wait_ns: page fences, full dispatch ring
   uint32_t nl = 0, qn = 0, an = 0, next_lane = 0, sumP = 0, sumL = 0, arr_ptr = 0, n_done = 0;
   uint32_t free_top = 0, max_lanes = 0, err = 0;
   uint64_t slot_free = ~0ull;
@@ -232,12 +244,16 @@ struct Sched {
       S.n[j] = J.n_iters; S.p[j] = J.p_pages; S.e[j] = J.e_pages; S.ap[j] = J.ap_pages; S.ae[j] = J.ae_pages;
       S.id[j] = J.job_id; S.st[j] = ST_NOT_ARRIVED; S.jslot[j] = 0xFF; S.kind[j] = (uint8_t)J.kind;
       S.nrt[j] = J.kind == SALUS_INFER ? P.req_ticks[J.req_off] : IDLE_T;
+      S.req_off[j] = J.req_off;
       salus_job_stat &st = P.stats[j];
       st.job_id = J.job_id; st.first_lane = NONE32; st.admit_tick = -1; st.first_start_tick = -1;
       st.completion_tick = -1; st.completion_seq = ~0ull; st.wall_start_ns = 0; st.wall_end_ns = 0;
     }
     for (uint32_t i = tid; i < P.Cp; i += 32) P.free_stack[i] = P.Cp - 1 - i;
-    for (uint32_t i = tid; i < MAX_LANES; i += 32) { S.sq_tail[i] = 0; S.last_app[i] = 0; }
+    for (uint32_t i = tid; i < MAX_LANES; i += 32) {
+      S.sq_tail[i] = 0; S.last_app[i] = 0; S.tail_seq[i] = 0; S.q_head_seen[i] = 0;
+    }
+    for (uint32_t k = tid; k < P.n_infer; k += 32) S.infer[k] = P.infer_list[k];
     free_top = P.Cp;
     max_lanes = P.max_lanes;
     next_arrival = N ? P.jobs[0].arrival : IDLE_T;
@@ -248,7 +264,7 @@ struct Sched {
     int64_t m = IDLE_T;
     for (uint32_t i = tid; i < nl; i += 32) m = min(m, S.lane_busy[i]);
     for (uint32_t k = tid; k < P.n_infer; k += 32) {
-      uint32_t j = P.infer_list[k];
+      uint32_t j = S.infer[k];
       if (S.st[j] == ST_QUEUED || S.st[j] == ST_ADMITTED) m = min(m, S.nrt[j]);
     }
     m = warp_min_i64(m);
@@ -308,6 +324,7 @@ struct Sched {
           emit(SALUS_REC_LANE_CLOSE, S.lane_id[i], S.id[j], 0, 0);
           push_pages(lane_table(slot), S.lane_back[i], slot, S.lane_seq[i]);
           sumL -= S.lane_L[i];
+          if (tid == 0) S.tail_seq[slot] = S.last_app[slot];
           slot_free |= (1ull << slot);
           remove_lane(i);
           continue;
@@ -319,7 +336,7 @@ struct Sched {
         }
         if (maxae < S.lane_back[i]) {
           push_pages(lane_table(slot) + maxae, S.lane_back[i] - maxae, slot, S.lane_seq[i]);
-          if (tid == 0) S.lane_back[i] = maxae;
+          if (tid == 0) { S.lane_back[i] = maxae; S.tail_seq[slot] = S.last_app[slot]; }
         }
         __syncwarp();
       }
@@ -379,9 +396,9 @@ struct Sched {
       const uint32_t k = k0 + tid;
       uint32_t j = 0, cnt = 0;
       if (k < P.n_infer) {
-        j = P.infer_list[k];
+        j = S.infer[k];
         if ((S.st[j] == ST_QUEUED || S.st[j] == ST_ADMITTED) && S.nrt[j] == t) {
-          const uint32_t off = P.jobs[j].req_off;
+          const uint32_t off = S.req_off[j];
           uint32_t nr = S.next_req[j];
           while (nr < S.n[j] && P.req_ticks[off + nr] == t) { nr++; cnt++; }
           S.next_req[j] = nr;
@@ -419,7 +436,15 @@ struct Sched {
   __device__ void admit(uint32_t j, int branch, uint32_t li) {
     uint32_t slot;
     if (branch == 1) {                                   // new lane
-      slot = __ffsll((long long)slot_free) - 1;
+      // any free slot will do (slots are physical, never logged): prefer
+      // one whose past records have all completed, so no drain is needed
+      uint32_t idle = 0;
+      for (uint32_t q = tid; q < MAX_LANES; q += 32)
+        if (((slot_free >> q) & 1ull) &&
+            (!physical || ptx::ld_acquire_u64(&P.slots[q].done_seq) >= S.tail_seq[q])) idle |= 1u << (q >> 5);
+      // lanes hold bit q>>5 of slots q = tid, tid + 32: find the lowest idle slot
+      const uint32_t m0 = __ballot_sync(0xffffffffu, idle & 1u), m1 = __ballot_sync(0xffffffffu, (idle >> 1) & 1u);
+      slot = m0 ? (uint32_t)__ffs(m0) - 1 : m1 ? 32u + (uint32_t)__ffs(m1) - 1 : (uint32_t)__ffsll((long long)slot_free) - 1;
       slot_free &= ~(1ull << slot);
       li = nl;
       if (tid == 0) {
@@ -444,9 +469,11 @@ struct Sched {
     // physical backing: the lane grows to the max actual E of its residents,
     // the job's persistent tensors get their own pages (Observation 2)
     if (S.ae[j] > S.lane_back[li]) {
-      // the slot's page table is about to be rewritten: iterations already
-      // queued on this slot (run-ahead) translate through it, so drain them
-      if (physical && S.last_app[slot]) wait_slot(slot, S.last_app[slot]);
+      // the slot's page-table entries past the backing are about to be
+      // rewritten: records that may still translate through them (queued
+      // before the last shrink / close, run-ahead) must have completed.
+      // Records of current residents only use entries below the backing.
+      if (physical && S.tail_seq[slot]) wait_slot(slot, S.tail_seq[slot]);
       pop_pages(lane_table(slot) + S.lane_back[li], S.ae[j] - S.lane_back[li], slot);
       if (tid == 0) S.lane_back[li] = S.ae[j];
     }
@@ -502,7 +529,9 @@ struct Sched {
       unsigned long long *pf = &P.pend_fence[slot * MAX_LANES + q];
       const uint64_t want = *(volatile unsigned long long *)pf;
       if (want) {
+        const uint64_t w0 = wait_ns;
         wait_slot(q, want);
+        wait_fence_ns += wait_ns - w0;
         if (err) return;
         if (tid == 0) *pf = 0;
       }
@@ -523,7 +552,11 @@ struct Sched {
       uint64_t t0 = 0;
       uint32_t full = 1, spins = 0;
       while (true) {
-        if (tid == 0) full = tl - ld_acquire_u32(&sl.q_head) >= RQ;
+        // the cached head usually proves there is room without a load
+        if (tid == 0) {
+          full = tl - S.q_head_seen[slot] >= RQ;
+          if (full) { S.q_head_seen[slot] = ld_acquire_u32(&sl.q_head); full = tl - S.q_head_seen[slot] >= RQ; }
+        }
         full = __shfl_sync(0xffffffffu, full, 0);
         if (!full) break;
         if (t0 == 0) t0 = ptx::globaltimer();
@@ -534,12 +567,13 @@ struct Sched {
           if (__shfl_sync(0xffffffffu, bad, 0)) { fail(host_abort() ? SALUS_E_TIMEOUT : SALUS_E_STUCK, 6); return; }
         }
       }
-      if (t0) wait_ns += ptx::globaltimer() - t0;
+      if (t0) { wait_ns += ptx::globaltimer() - t0; wait_ring_ns += ptx::globaltimer() - t0; }
     }
     uint32_t won = 0;
     if (tid == 0) {
       volatile DispRec *vr = &sl.recs[tl % RQ];
       vr->job = j; vr->iter = S.done[j]; vr->seq = seq; vr->lane_id = lane_id; vr->pad = 0;
+      vr->append_ns = ptx::globaltimer();
       st_release_u32(&sl.q_tail, tl + 1);
       __threadfence();                                     // store q_tail -> CAS running (SC)
       won = atomicCAS(&sl.running, 0u, 1u) == 0u;
@@ -570,23 +604,31 @@ struct Sched {
 
   // P4: every idle lane dispatches its next iteration
   __device__ void phase_dispatch() {
+    // one pass over the residents: the minimum key of each slot (a lane owns
+    // one slot and a job one lane, so dispatching on one lane never changes
+    // another lane's minimum)
+    uint32_t idle = 0;
+    for (uint32_t i = 0; i < nl; i++) idle |= (S.lane_busy[i] == IDLE_T) ? 1u : 0u;
+    if (!idle) return;
+    for (uint32_t i = tid; i < nl; i += 32) S.slot_key[S.lane_slot[i]] = ~0ull;
+    __syncwarp();
+    for (uint32_t a = tid; a < an; a += 32) {
+      const uint32_t j = S.adm[a];
+      if (!runnable(j)) continue;
+      uint64_t key;
+      if (P.policy == SALUS_SRTF)          // A11: remaining = (n - done) * c
+        key = ((uint64_t)((int64_t)(S.n[j] - S.done[j]) * S.c[j]) << KEY_BITS) | j;
+      else if (P.policy == SALUS_FAIR)     // least service
+        key = ((uint64_t)S.svc[j] << KEY_BITS) | j;
+      else                                 // FIFO / PACK (A13): earliest arrival
+        key = j;
+      atomicMin(&S.slot_key[S.jslot[j]], (unsigned long long)key);
+    }
+    __syncwarp();
     for (uint32_t i = 0; i < nl; i++) {
       if (S.lane_busy[i] != IDLE_T) continue;
       const uint32_t slot = S.lane_slot[i];
-      uint64_t best = ~0ull;
-      for (uint32_t a = tid; a < an; a += 32) {
-        const uint32_t j = S.adm[a];
-        if (S.jslot[j] != slot || !runnable(j)) continue;
-        uint64_t key;
-        if (P.policy == SALUS_SRTF)        // A11: remaining = (n - done) * c
-          key = ((uint64_t)((int64_t)(S.n[j] - S.done[j]) * S.c[j]) << KEY_BITS) | j;
-        else if (P.policy == SALUS_FAIR)   // least service
-          key = ((uint64_t)S.svc[j] << KEY_BITS) | j;
-        else                               // FIFO / PACK (A13): earliest arrival
-          key = j;
-        best = key < best ? key : best;
-      }
-      best = warp_min_u64(best);
+      const uint64_t best = S.slot_key[slot];
       if (best == ~0ull) continue;
       const uint32_t j = (uint32_t)(best & ((1u << KEY_BITS) - 1));
       const uint16_t last = S.lane_last[i];
@@ -645,6 +687,7 @@ struct Sched {
     if (tid == 0) {
       P.ctrl->n_dispatch = seq; P.ctrl->n_ticks = n_ticks; P.ctrl->n_log = n_log;
       P.ctrl->sched_wait_ns = wait_ns; P.ctrl->wall_first_ns = wall0;
+      P.ctrl->sched_fence_ns = wait_fence_ns; P.ctrl->sched_ring_ns = wait_ring_ns;
       P.ctrl->wall_last_ns = ptx::globaltimer();
       P.ctrl->log_overflow = ((P.flags & SALUS_FLAG_LOG) && n_log > P.log_cap) ? 1u : 0u;
     }

@@ -848,6 +848,7 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
           if ((P.flags & SALUS_FLAG_LOG) && td.seq < P.log_cap) {
             salus_wall_rec w;
             w.seq = td.seq; w.lane = sl.lane_id; w.job = J.job_id; w.start_ns = start; w.end_ns = end;
+            w.append_ns = sl.append_ns;
             P.wall[td.seq] = w;
           }
           if (td.iter == 0) P.stats[td.job].wall_start_ns = start;

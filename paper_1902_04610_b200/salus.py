@@ -60,11 +60,12 @@ class RunStats(C.Structure):
     _fields_ = [("n_dispatch", C.c_uint64), ("n_ticks", C.c_uint64), ("n_log", C.c_uint64),
                 ("n_tasks", C.c_uint64), ("kernel_ns", C.c_uint64), ("wall_first_ns", C.c_uint64),
                 ("wall_last_ns", C.c_uint64), ("sched_wait_ns", C.c_uint64), ("status", C.c_int32),
-                ("n_workers", C.c_uint32), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64)]
+                ("n_workers", C.c_uint32), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
+                ("sched_fence_ns", C.c_uint64), ("sched_ring_ns", C.c_uint64)]
 
 
 WALL_DTYPE = np.dtype([("seq", "<u8"), ("lane", "<u4"), ("job", "<u4"), ("start_ns", "<u8"),
-                       ("end_ns", "<u8")])
+                       ("end_ns", "<u8"), ("append_ns", "<u8")])
 TRACE_DTYPE = np.dtype([("task", "<u4"), ("smid", "<u4"), ("job", "<u4"), ("iter", "<u4"),
                         ("t_claim", "<u8"), ("t_ready", "<u8"), ("t_mma", "<u8"), ("t_end", "<u8")])
 LOG_DTYPE = np.dtype([("tick", "<i8"), ("kind", "<u4"), ("lane", "<u4"), ("job", "<u4"),
