@@ -12,7 +12,7 @@
 __device__ __forceinline__ uint32_t sa(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint64_t gt() { uint64_t t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t; }
 
-template <int MODE, int PIPE, int CH>
+template <int MODE, int PIPE, int CH, int SPIN = 0>
 __global__ void __launch_bounds__(32, 1) bench(const __grid_constant__ CUtensorMap tmap, const uint8_t *src,
                                                uint64_t src_bytes, int iters, unsigned long long *out_ns) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -27,9 +27,14 @@ __global__ void __launch_bounds__(32, 1) bench(const __grid_constant__ CUtensorM
     if (i >= PIPE) {   // wait for the copy issued PIPE iterations ago
       const uint32_t par = ((i / PIPE) - 1) & 1;
       uint32_t ok = 0;
-      while (!ok)
-        asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
-                     : "=r"(ok) : "r"(sa(&full[s])), "r"(par));
+      if (SPIN)   // non-blocking test_wait spin
+        while (!ok)
+          asm volatile("{.reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                       : "=r"(ok) : "r"(sa(&full[s])), "r"(par));
+      else
+        while (!ok)
+          asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0,1,0,p;}"
+                       : "=r"(ok) : "r"(sa(&full[s])), "r"(par));
     }
     if (i >= iters) continue;
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&full[s])), "r"(CH));
@@ -50,14 +55,14 @@ __global__ void __launch_bounds__(32, 1) bench(const __grid_constant__ CUtensorM
   out_ns[blockIdx.x] = gt() - t0;
 }
 
-template <int MODE, int PIPE, int CH>
+template <int MODE, int PIPE, int CH, int SPIN = 0>
 void run(const CUtensorMap &tm, const uint8_t *src, uint64_t bytes, int grid, const char *name) {
   unsigned long long *d_ns;
   cudaMalloc(&d_ns, grid * 8);
   const int iters = 4000, smem = PIPE * CH;
-  cudaFuncSetAttribute(bench<MODE, PIPE, CH>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  bench<MODE, PIPE, CH><<<grid, 32, smem>>>(tm, src, bytes, iters, d_ns);   // warm
-  bench<MODE, PIPE, CH><<<grid, 32, smem>>>(tm, src, bytes, iters, d_ns);
+  cudaFuncSetAttribute(bench<MODE, PIPE, CH, SPIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  bench<MODE, PIPE, CH, SPIN><<<grid, 32, smem>>>(tm, src, bytes, iters, d_ns);   // warm
+  bench<MODE, PIPE, CH, SPIN><<<grid, 32, smem>>>(tm, src, bytes, iters, d_ns);
   cudaError_t e = cudaDeviceSynchronize();
   unsigned long long h[1024];
   cudaMemcpy(h, d_ns, grid * 8, cudaMemcpyDeviceToHost);
@@ -86,6 +91,9 @@ int main() {
                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   printf("tensor map encode: %d\n", (int)r);
   for (int grid : {1, 148}) {
+    run<0, 4, 32768, 1>(tm, src, bytes, grid, "bulk 16K x2 test_wait");
+    run<0, 6, 65536, 0>(tm, src, bytes, grid, "bulk 16K x4");
+    run<0, 3, 65536, 1>(tm, src, bytes, grid, "bulk 16K x4 test_wait");
     run<0, 2, 32768>(tm, src, bytes, grid, "bulk 16K x2");
     run<0, 4, 32768>(tm, src, bytes, grid, "bulk 16K x2");
     run<0, 6, 32768>(tm, src, bytes, grid, "bulk 16K x2");
