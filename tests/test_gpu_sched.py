@@ -34,6 +34,29 @@ def test_c3_inference(policy, max_lanes):
     assert_schedule_parity(jobs, cap, policy, max_lanes=max_lanes)[0].close()
 
 
+@pytest.mark.parametrize("policy,max_lanes", [(OS.FAIR, 8), (OS.PACK, 0)])
+def test_c3_real_work_wall_stamps(policy, max_lanes):
+    """C3 with every request executing (the bench's switch-latency config):
+    schedule parity, and physically consistent wall stamps -- a lane starts
+    an iteration only after the scheduler appended its record and after the
+    lane's previous iteration ended (run-ahead, A30)."""
+    jobs, cap = c3_trace()
+    ctx, ref, stats = assert_schedule_parity(jobs, cap, policy, max_lanes=max_lanes, null_work=False)
+    try:
+        w = ctx.wall()
+        rs = ctx.run_stats()
+        assert len(w) == rs["n_dispatch"] == 8400
+        assert np.all(w["end_ns"] > w["start_ns"])
+        assert np.all(w["append_ns"] <= w["start_ns"])
+        w = w[np.argsort(w["seq"])]
+        for ln in np.unique(w["lane"]):
+            m = w[w["lane"] == ln]
+            assert np.all(m["start_ns"][1:] >= m["end_ns"][:-1])
+        assert rs["sched_fence_ns"] + rs["sched_ring_ns"] <= rs["sched_wait_ns"]
+    finally:
+        ctx.close()
+
+
 @pytest.mark.parametrize("policy", [OS.FIFO, OS.SRTF, OS.PACK, OS.FAIR])
 def test_c4_mixed(policy):
     jobs, cap = c4_trace()
