@@ -647,6 +647,12 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W) {
         if (kc == 0) const_cast<TileDesc &>(td).t_ready = ptx::globaltimer();
         if (kc + 1 == nk) const_cast<TileDesc &>(td).t_mma = ptx::globaltimer();
 #endif
+#if SALUS_DBG_CHUNKS2  // per-chunk stamps of one F tile (job 0, iter 10, stage 2, task 0) -> trace tail
+        if (td.job == 0 && td.iter == 10 && td.stage == 2 && (td.payload & 0x1FFFFF) == 0 && kc < 32) {
+          uint64_t *dbg = reinterpret_cast<uint64_t *>(P.trace + P.trace_cap) - 256;
+          dbg[ptx::cluster_ctarank() * 64 + kc] = ptx::globaltimer();
+        }
+#endif
         if (++s == PIPE) { s = 0; s_phase ^= 1; }
       }
     }
@@ -706,6 +712,12 @@ __device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
       const uint32_t a_step = td.a.mn ? 2048u : 32u, b_step = td.b.mn ? 2048u : 32u;
       for (uint32_t kc = 0; kc < nk; kc++) {
         ptx::mbar_wait_abortable(&W.full[s], s_phase, &P.ctrl->abort);
+#if SALUS_DBG_CHUNKS2
+        if (td.job == 0 && td.iter == 10 && td.stage == 2 && (td.payload & 0x1FFFFF) == 0 && kc < 32) {
+          uint64_t *dbg = reinterpret_cast<uint64_t *>(P.trace + P.trace_cap) - 256;
+          dbg[160 + kc] = ptx::globaltimer();                      // own chunk landed
+        }
+#endif
         ptx::mbar_wait_abortable(&W.pair_full[s], s_phase, &P.ctrl->abort);
 #if SALUS_DBG_CHUNKS   // MMA thread: last chunk landed in both CTAs
         if (kc + 1 == nk) const_cast<TileDesc &>(td).t_end = ptx::globaltimer();
@@ -719,6 +731,12 @@ __device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
           ptx::mma_bf16(tacc, ad, bd, idesc, (kc | ks) != 0);
         }
         ptx::mma_commit_pair(&W.empty[s]);
+#if SALUS_DBG_CHUNKS2
+        if (td.job == 0 && td.iter == 10 && td.stage == 2 && (td.payload & 0x1FFFFF) == 0 && kc < 32) {
+          uint64_t *dbg = reinterpret_cast<uint64_t *>(P.trace + P.trace_cap) - 256;
+          dbg[192 + kc] = ptx::globaltimer();                      // MMAs issued
+        }
+#endif
         if (++s == PIPE) { s = 0; s_phase ^= 1; }
       }
       ptx::mma_commit_pair(&W.acc_full[b]);
@@ -739,6 +757,12 @@ __device__ void pair_forwarder(const Params &P, WorkerSmem &W) {
     if (td.kind == T_GEMM) {
       for (uint32_t kc = 0, nk = td.nk; kc < nk; kc++) {
         ptx::mbar_wait_abortable(&W.full[s], s_phase, &P.ctrl->abort);
+#if SALUS_DBG_CHUNKS2
+        if (td.job == 0 && td.iter == 10 && td.stage == 2 && (td.payload & 0x1FFFFF) == 0 && kc < 32) {
+          uint64_t *dbg = reinterpret_cast<uint64_t *>(P.trace + P.trace_cap) - 256;
+          dbg[224 + kc] = ptx::globaltimer();                      // peer chunk landed
+        }
+#endif
         ptx::mbar_arrive_remote(&W.pair_full[s], 0);
         if (++s == PIPE) { s = 0; s_phase ^= 1; }
       }

@@ -148,7 +148,8 @@ class Context:
     def __init__(self, jobs: Iterable, capacity_bytes: int, policy: int, *, device: int = 0,
                  max_lanes: int = 0, switch_ticks: int = 0, log: bool = True, null_work: bool = False,
                  check: bool = False, dump: Optional[Dict[int, int]] = None, n_workers: int = 0,
-                 timeout_ms: int = 0, page_bytes: int = 65536, trace: bool = False):
+                 timeout_ms: int = 0, page_bytes: int = 65536, trace: bool = False,
+                 trace_capacity: int = 0):
         import torch
         self._torch = torch
         self.L = lib()
@@ -173,6 +174,7 @@ class Context:
         cfg.switch_ticks = switch_ticks
         cfg.n_workers = n_workers
         cfg.timeout_ms = timeout_ms
+        cfg.trace_capacity = trace_capacity
         self.flags = cfg.flags
         self.ctx = C.c_void_p()
         self._check(self.L.salus_open(C.byref(cfg), C.byref(self.ctx)), "open")
