@@ -180,6 +180,23 @@ __device__ __forceinline__ void st_global_v4_hint(void *p, uint4 v, uint64_t pol
 __device__ __forceinline__ void prefetch_l2(const void *gmem_src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem_src), "r"(bytes) : "memory");
 }
+// 2-D tensor TMA of one box into this CTA's smem, completing on the mbarrier
+// at shared::cluster address `mbar_cluster` -- with .cta_group::2 that may be
+// the pair leader's barrier.
+__device__ __forceinline__ void tma_load_2d_pair(void *smem_dst, const void *tmap, int32_t c0, int32_t c1,
+                                                 uint32_t mbar_cluster, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3}], [%4], %5;" ::"r"(smem_u32(smem_dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(mbar_cluster), "l"(policy)
+      : "memory");
+}
+// arrive + expect_tx on a (possibly remote) mbarrier, cluster scope
+__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t mbar_cluster, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(mbar_cluster),
+               "r"(bytes)
+               : "memory");
+}
 // global -> shared, completion reported to an mbarrier as transaction bytes.
 // shared -> global bulk copy (async proxy), completion tracked by bulk groups
 __device__ __forceinline__ void bulk_s2g(void *gmem_dst, const void *smem_src, uint32_t bytes) {

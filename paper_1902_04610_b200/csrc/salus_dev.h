@@ -3,6 +3,7 @@
 // ("Data layout in HBM", "Meta buffer").
 #pragma once
 #include <stdint.h>
+#include <cuda.h>
 #include "../../include/salus.h"
 
 namespace salus {
@@ -97,6 +98,13 @@ struct alignas(256) Ctrl {
 };
 
 struct Params {
+  // The arena viewed as a 2-D tensor of 128-byte rows (uint8, no swizzle:
+  // the data are already stored in the smem image).  Box = 128 or 64 rows,
+  // i.e. one 16 KiB / 8 KiB operand block per TMA.  Tensor copies are the
+  // only bulk copies that can complete on the PEER CTA's mbarrier
+  // (.cta_group::2), which lets both CTAs of a pair fill the leader's stage
+  // barrier directly.
+  CUtensorMap tmap16, tmap8;
   uint8_t *arena;
   Ctrl *ctrl;
   const DevJob *jobs;
@@ -138,7 +146,7 @@ __host__ __device__ inline uint32_t last_stage(uint32_t kind, uint32_t L) {
 
 // GEMM N tile for an output width (padded to 128): 256 when it divides, else
 // 128.  Wide tiles halve operand re-reads; the epilogue streams its input
-// (fp32 master weights / ReLU mask) through four 32 KiB smem chunk buffers.
+// (fp32 master weights / ReLU mask) through three 32 KiB smem chunk buffers.
 __host__ __device__ inline uint32_t ntile_for(uint32_t dpad) { return (dpad % 256 == 0) ? 256 : 128; }
 
 }  // namespace salus

@@ -2,6 +2,8 @@
 // page rounding (A18), device-layout footprints, meta-buffer layout, job
 // table upload, cooperative launch of the persistent kernel, watchdog, and
 // readback.  No per-iteration host work: one launch per salus_run.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -374,6 +376,25 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
 
   Params &P = ctx->P;
   P.arena = static_cast<uint8_t *>(ctx->cfg.arena);
+  {   // the arena as rows of 128 B for the operand TMA (see salus_dev.h)
+    PFN_cuTensorMapEncodeTiled enc = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if ((e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void **>(&enc), cudaEnableDefault,
+                                     &q)) || !enc || q != cudaDriverEntryPointSuccess)
+      return fail(ctx, SALUS_E_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t rows = (cuuint64_t)ctx->Cp * ctx->cfg.page_bytes / 128;
+    cuuint64_t gdim[2] = {128, rows};
+    cuuint64_t gstride[1] = {128};
+    cuuint32_t estride[2] = {1, 1};
+    cuuint32_t box16[2] = {128, 128}, box8[2] = {128, 64};
+    if (enc(&P.tmap16, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, ctx->cfg.arena, gdim, gstride, box16, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS ||
+        enc(&P.tmap8, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, ctx->cfg.arena, gdim, gstride, box8, estride,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return fail(ctx, SALUS_E_CUDA, "tensor map encoding failed");
+  }
   P.ctrl = reinterpret_cast<Ctrl *>(m + ctx->off_ctrl);
   P.jobs = reinterpret_cast<const DevJob *>(m + ctx->off_jobs);
   P.req_ticks = reinterpret_cast<const int64_t *>(m + ctx->off_req);

@@ -15,7 +15,7 @@
 
 namespace salus {
 
-__global__ void __launch_bounds__(WORKER_THREADS, 1) salus_persistent_kernel(Params P) {
+__global__ void __launch_bounds__(WORKER_THREADS, 1) salus_persistent_kernel(const __grid_constant__ Params P) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if (blockIdx.x == 0) {
     if (threadIdx.x < 32) {

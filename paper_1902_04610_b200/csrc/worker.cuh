@@ -13,16 +13,16 @@
 //              half (stage -> GEMM / epilogue kind, tensors, coordinates) and
 //              translates the epilogue's page addresses, lanes in parallel.
 //   warp 1     operand loader (1 thread): issues every K-chunk of the A/B
-//              operands as bulk async copies (cp.async.bulk, TMA unit) into a
-//              3-stage mbarrier ring (page-table reads two chunks ahead).
+//              operands as 2-D tensor TMAs (one 8/16 KiB block each) into a
+//              4-stage mbarrier ring (page-table reads two chunks ahead).
 //   warp 2     leader: MMA (1 thread): tcgen05.mma.cta_group::2 kind::f16
 //              (bf16 in, fp32 accumulate) into one of two TMEM accumulators
 //              of 256 columns in both CTAs (double buffered: the epilogue of
-//              tile i overlaps the MMA of tile i+1).  peer: forwards each
-//              landed K-chunk of its smem to the leader's pair_full barrier.
+//              tile i overlaps the MMA of tile i+1).  Both CTAs' operand TMAs
+//              complete on the leader's stage barrier (.cta_group::2).
 //   warp 3     epilogue-input loader (1 thread): streams the tile's epilogue
 //              input (fp32 master weights of a dW tile, ReLU mask of a dX
-//              tile) in 32 KiB chunks through four smem buffers.
+//              tile) in 32 KiB chunks through three smem buffers.
 //   warps 4-11 epilogue: drain TMEM (tcgen05.ld), fused epilogue, stores.
 //   warp 12    completion: gpu-scope fence, stage accounting, publication of
 //              the next stage / start of the slot's next iteration (run-ahead)
@@ -44,7 +44,7 @@
 namespace salus {
 
 #ifndef SALUS_PIPE
-#define SALUS_PIPE 3
+#define SALUS_PIPE 4
 #endif
 constexpr uint32_t PIPE = SALUS_PIPE;                 // operand stages in flight
 constexpr uint32_t STAGE_A_BYTES = 16384;             // 128 x 64 bf16 (this CTA's rows)
@@ -52,10 +52,11 @@ constexpr uint32_t STAGE_B_BYTES = 16384;             // <= 128 x 64 bf16 (this 
 constexpr uint32_t STAGE_BYTES = STAGE_A_BYTES + STAGE_B_BYTES;
 constexpr uint32_t ECH_BYTES = 32768;                 // epilogue-input chunk
 #ifndef SALUS_EBUF
-#define SALUS_EBUF 4
+#define SALUS_EBUF 3
 #endif
-// epilogue-input chunk buffers: 4 hold a whole 128 x 256 fp32 master tile,
-// so its HBM read overlaps the tile's MMA instead of the epilogue
+// epilogue-input chunk buffers: 3 of the 4 chunks of a 128 x 256 fp32 master
+// tile are read from HBM while the tile's MMA runs, not during its epilogue
+// (smem: 4 operand stages x 32 KiB + 3 x 32 KiB + descriptors = 227 KiB)
 constexpr uint32_t EBUF = SALUS_EBUF;
 #ifndef SALUS_NDESC
 #define SALUS_NDESC 4
@@ -96,6 +97,8 @@ struct OpDesc {
 struct TileDesc {
   uint32_t kind, payload, slot, stage, job, iter, ntiles, next_ntiles, is_last, first_stage;
   uint32_t valid;          // this CTA's half exists (odd block counts leave the peer's empty)
+  uint32_t peer_valid;     // the pair's second M block exists
+  uint32_t peer_nca;       // (leader) A copies per K-chunk of the peer CTA
   uint64_t seq, t_claim, t_ready, t_mma, t_end;   // trace stamps
   // GEMM
   uint32_t N, nk, idesc, epi, layer, ncopy_a, ncopy_b, abytes, bbytes;
@@ -121,7 +124,6 @@ struct WorkerSmem {
   uint64_t acc_full[2], acc_empty[2];
   uint64_t epi_full[EBUF], epi_empty[EBUF];
   uint64_t epi_done[NDESC];           // epilogue -> completion warp
-  uint64_t pair_full[PIPE];           // leader: the peer's K-chunk has landed
   uint64_t mail_full[NDESC];          // peer: the leader mailed task d
   struct { uint32_t payload, pad; uint64_t t_claim; } mail[NDESC];
   uint32_t tmem_base;
@@ -257,6 +259,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     const uint32_t l = stage - 1, N = ntile_for(J.dpad[l]), ntn = J.dpad[l] / N;
     const uint32_t mb = 2 * (tile / ntn) + h, nb = tile % ntn;
     td.valid = mb < bp / 128;
+    td.peer_valid = (mb | 1u) < bp / 128;
     td.layer = l; td.N = N; td.nk = J.dpad[l - 1] / 64;
     td.a = OpDesc{lt, J.act_off[l - 1], bp, mb * 128, 0};
     td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * N + h * (N / 2), 0};
@@ -283,6 +286,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     if (tile < nW) {                                  // dW_l^T = G_l^T A_{l-1}; SGD
       const uint32_t mb = 2 * (tile / ntn) + h, nb = tile % ntn;
       td.valid = mb < J.dpad[l] / 128;
+      td.peer_valid = (mb | 1u) < J.dpad[l] / 128;
       td.epi = EPI_SGD; td.nk = bp / 64;
       td.a = OpDesc{lt, gin, bp, mb * 128, 1};
       td.b = OpDesc{lt, J.act_off[l - 1], bp, nb * N + h * (N / 2), 1};
@@ -306,6 +310,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     } else {                                          // G_{l-1} = (G_l W_l^T) * [A_{l-1} > 0]
       const uint32_t u = tile - nW, mb = 2 * (u / ntn) + h, nb = u % ntn;
       td.valid = mb < bp / 128;
+      td.peer_valid = (mb | 1u) < bp / 128;
       td.epi = EPI_DX; td.nk = J.dpad[l] / 64;
       td.a = OpDesc{lt, gin, bp, mb * 128, 0};
       td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * N + h * (N / 2), 1};
@@ -324,6 +329,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   // rows (K-major, 64 or 128 rows per copy) or N/128 panels (MN-major)
   const uint32_t nh = td.N / 2;
   td.ncopy_a = td.valid ? (td.a.mn ? 2 : 1) : 0;
+  td.peer_nca = td.peer_valid ? (td.a.mn ? 2 : 1) : 0;
   td.abytes = td.a.mn ? 8192u : 16384u;
   td.ncopy_b = td.b.mn ? nh / 64 : (nh + 127) / 128;
   td.bbytes = td.b.mn ? 8192u : (nh >= 128 ? 16384u : nh * 128u);
@@ -602,15 +608,16 @@ __device__ __forceinline__ ChunkPages chunk_pages(const OpDesc &a, const OpDesc 
   return p;
 }
 
-__device__ __forceinline__ const uint8_t *page_ptr(const Params &P, uint32_t page, uint32_t off) {
-  return P.arena + ((uint64_t)page << PAGE_SHIFT) + (off & (PAGE_BYTES - 1));
+// row coordinate of byte `off` of a page in the arena's 128-byte-row tensor map
+__device__ __forceinline__ int32_t tma_row(uint32_t page, uint32_t off) {
+  return (int32_t)((page << (PAGE_SHIFT - 7)) + ((off & (PAGE_BYTES - 1)) >> 7));
 }
 
 // Operand loader (1 thread).  The page-table reads of chunk kc + 2 are issued
 // before the copies of chunk kc, so their latency (an L2 round trip: the
 // completion warp's gpu-scope fences keep invalidating L1) is off the
 // per-chunk critical path.
-__device__ void operand_loader(const Params &P, WorkerSmem &W) {
+__device__ void operand_loader(const Params &P, WorkerSmem &W, uint32_t h) {
   uint32_t d = 0, d_phase = 0, s = 0, s_phase = 0;
   const uint64_t first = ptx::policy_evict_first(), last = ptx::policy_evict_last();
   const uint64_t normal = ptx::policy_evict_normal();
@@ -621,7 +628,9 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W) {
     if (td.kind == T_GEMM) {
       const OpDesc a = td.a, b = td.b;
       const uint32_t nk = td.nk, nca = td.ncopy_a, ncb = td.ncopy_b, ab = td.abytes, bb = td.bbytes;
-      const uint32_t tx = nca * ab + ncb * bb;
+      // bytes of one K-chunk in both CTAs: B halves are symmetric, A exists
+      // in the peer iff its M block does
+      const uint32_t tx_pair = (nca + td.peer_nca) * ab + 2 * ncb * bb;
       const uint32_t *jt = P.ppt + P.jobs[td.job].pt_off;
       // weights (the job's persistent space) stream; a lane's activations stay
 #if SALUS_L2HINT
@@ -637,12 +646,19 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W) {
         if (kc + 2 < nk) p1 = chunk_pages(a, b, nca, ncb, kc + 2);
         // stage s is free once the pair's MMA has consumed it (multicast commit)
         ptx::mbar_wait_abortable(&W.empty[s], s_phase ^ 1, &P.ctrl->abort);
-        ptx::mbar_arrive_expect_tx(&W.full[s], tx);
+        // both CTAs' copies complete on the LEADER's full[s]: the leader alone
+        // arms it with the pair's bytes (one arrival); the peer's TMAs only
+        // add their bytes through the async proxy -- no thread-issued remote
+        // arrive on the per-chunk path (those take ~1 us to be observed)
+        const uint32_t bar = ptx::mapa(&W.full[s], 0);
+        if (h == 0) ptx::mbar_arrive_expect_tx(&W.full[s], tx_pair);
         uint8_t *sa = W.stage[s], *sb = W.stage[s] + STAGE_A_BYTES;
-        if (nca > 0) ptx::bulk_g2s_hint(sa, page_ptr(P, cur.a0, copy_off(a, kc, 0)), ab, &W.full[s], pol_a);
-        if (nca > 1) ptx::bulk_g2s_hint(sa + ab, page_ptr(P, cur.a1, copy_off(a, kc, 1)), ab, &W.full[s], pol_a);
-        if (ncb > 0) ptx::bulk_g2s_hint(sb, page_ptr(P, cur.b0, copy_off(b, kc, 0)), bb, &W.full[s], pol_b);
-        if (ncb > 1) ptx::bulk_g2s_hint(sb + bb, page_ptr(P, cur.b1, copy_off(b, kc, 1)), bb, &W.full[s], pol_b);
+        const void *ta = ab == 16384u ? (const void *)&P.tmap16 : (const void *)&P.tmap8;
+        const void *tb = bb == 16384u ? (const void *)&P.tmap16 : (const void *)&P.tmap8;
+        if (nca > 0) ptx::tma_load_2d_pair(sa, ta, 0, tma_row(cur.a0, copy_off(a, kc, 0)), bar, pol_a);
+        if (nca > 1) ptx::tma_load_2d_pair(sa + ab, ta, 0, tma_row(cur.a1, copy_off(a, kc, 1)), bar, pol_a);
+        if (ncb > 0) ptx::tma_load_2d_pair(sb, tb, 0, tma_row(cur.b0, copy_off(b, kc, 0)), bar, pol_b);
+        if (ncb > 1) ptx::tma_load_2d_pair(sb + bb, tb, 0, tma_row(cur.b1, copy_off(b, kc, 1)), bar, pol_b);
 #if SALUS_DBG_CHUNKS   // trace fields re-purposed: loader issue of chunk 0 / last chunk
         if (kc == 0) const_cast<TileDesc &>(td).t_ready = ptx::globaltimer();
         if (kc + 1 == nk) const_cast<TileDesc &>(td).t_mma = ptx::globaltimer();
@@ -711,14 +727,14 @@ __device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
       const uint32_t a_lbo = td.a.mn ? 8192u : 16u, b_lbo = td.b.mn ? 8192u : 16u;
       const uint32_t a_step = td.a.mn ? 2048u : 32u, b_step = td.b.mn ? 2048u : 32u;
       for (uint32_t kc = 0; kc < nk; kc++) {
+        // the chunk has landed in both CTAs (both loaders' copies complete here)
         ptx::mbar_wait_abortable(&W.full[s], s_phase, &P.ctrl->abort);
 #if SALUS_DBG_CHUNKS2
         if (td.job == 0 && td.iter == 10 && td.stage == 2 && (td.payload & 0x1FFFFF) == 0 && kc < 32) {
           uint64_t *dbg = reinterpret_cast<uint64_t *>(P.trace + P.trace_cap) - 256;
-          dbg[160 + kc] = ptx::globaltimer();                      // own chunk landed
+          dbg[160 + kc] = ptx::globaltimer();                      // chunk landed (both CTAs)
         }
 #endif
-        ptx::mbar_wait_abortable(&W.pair_full[s], s_phase, &P.ctrl->abort);
 #if SALUS_DBG_CHUNKS   // MMA thread: last chunk landed in both CTAs
         if (kc + 1 == nk) const_cast<TileDesc &>(td).t_end = ptx::globaltimer();
 #endif
@@ -747,26 +763,13 @@ __device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
   }
 }
 
-// Peer: tells the leader's MMA thread when each K-chunk has landed here.
-__device__ void pair_forwarder(const Params &P, WorkerSmem &W) {
-  uint32_t d = 0, d_phase = 0, s = 0, s_phase = 0;
+// Peer: no MMA to issue (the leader's covers both CTAs); it only releases
+// its descriptors like the leader's MMA thread does.
+__device__ void peer_mma_role(const Params &P, WorkerSmem &W) {
+  uint32_t d = 0, d_phase = 0;
   for (;;) {
     ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
-    const TileDesc &td = W.desc[d];
-    if (td.kind == T_EXIT) break;
-    if (td.kind == T_GEMM) {
-      for (uint32_t kc = 0, nk = td.nk; kc < nk; kc++) {
-        ptx::mbar_wait_abortable(&W.full[s], s_phase, &P.ctrl->abort);
-#if SALUS_DBG_CHUNKS2
-        if (td.job == 0 && td.iter == 10 && td.stage == 2 && (td.payload & 0x1FFFFF) == 0 && kc < 32) {
-          uint64_t *dbg = reinterpret_cast<uint64_t *>(P.trace + P.trace_cap) - 256;
-          dbg[224 + kc] = ptx::globaltimer();                      // peer chunk landed
-        }
-#endif
-        ptx::mbar_arrive_remote(&W.pair_full[s], 0);
-        if (++s == PIPE) { s = 0; s_phase ^= 1; }
-      }
-    }
+    if (W.desc[d].kind == T_EXIT) break;
     release_desc(W, d);
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
@@ -917,11 +920,10 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
   const uint32_t h = ptx::cluster_ctarank();
 
   if (tid == 0) {
-    for (uint32_t s = 0; s < PIPE; s++) {
-      ptx::mbar_init(&W.full[s], 1); ptx::mbar_init(&W.empty[s], 1); ptx::mbar_init(&W.pair_full[s], 1);
-    }
+    // full[s]: the leader's, armed by the leader's loader for both CTAs' bytes
+    for (uint32_t s = 0; s < PIPE; s++) { ptx::mbar_init(&W.full[s], 1); ptx::mbar_init(&W.empty[s], 1); }
     // (leader) a descriptor is released by its 4 consumers in each CTA:
-    // operand loader, epilogue-input loader, MMA / forwarder thread,
+    // operand loader, epilogue-input loader, MMA thread (peer: its stand-in),
     // completion warp (after the epilogue is done)
     for (uint32_t d = 0; d < NDESC; d++) {
       ptx::mbar_init(&W.desc_full[d], 1);
@@ -945,8 +947,8 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
     decoder_warp(P, W, lane, h);
   } else if (warp < EPI_WARP0) {
     if (lane == 0) {
-      if (warp == 1) operand_loader(P, W);
-      else if (warp == 2) { if (h == 0) mma_thread(P, W, tmem); else pair_forwarder(P, W); }
+      if (warp == 1) operand_loader(P, W, h);
+      else if (warp == 2) { if (h == 0) mma_thread(P, W, tmem); else peer_mma_role(P, W); }
       else epi_loader(P, W);
     }
     __syncwarp();
