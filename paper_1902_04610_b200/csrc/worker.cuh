@@ -125,7 +125,8 @@ struct WorkerSmem {
   uint64_t epi_full[EBUF], epi_empty[EBUF];
   uint64_t epi_done[NDESC];           // epilogue -> completion warp
   uint64_t mail_full[NDESC];          // peer: the leader mailed task d
-  struct { uint32_t payload, pad; uint64_t t_claim; } mail[NDESC];
+  struct alignas(16) { uint32_t payload, pad; uint64_t t_claim; } mail[NDESC];
+  uint32_t sink[4];                   // target of the peer's signalling st.async
   uint32_t tmem_base;
   alignas(16) uint32_t job_cache[128]; // decoder scratch: the task's DevJob (<= 512 B)
 };
@@ -527,9 +528,19 @@ __device__ void gen_tile(const TileDesc &td, uint32_t r, uint32_t h) {
 // mailbox (a generic st.shared::cluster from the leader) is acquired at
 // cluster scope.
 // Every consumer of descriptor slot d, in both CTAs, releases it on the
-// leader's desc_empty[d] (8 arrivals per use): the leader mails task d only
-// when the slot is free in both CTAs.
-__device__ __forceinline__ void release_desc(WorkerSmem &W, uint32_t d) { ptx::mbar_arrive_remote(&W.desc_empty[d], 0); }
+// leader's desc_empty[d]: the leader's four consumers arrive (its MMA thread
+// also arms 16 transaction bytes), the peer's four each complete 4 bytes with
+// an st.async -- the async-proxy path, observed far sooner than a
+// thread-issued remote mbarrier.arrive.  The leader mails task d only when
+// the slot is free in both CTAs.
+__device__ __forceinline__ void release_desc(WorkerSmem &W, uint32_t d, uint32_t h, bool arm = false) {
+  if (h == 0) {
+    if (arm) ptx::mbar_arrive_expect_tx(&W.desc_empty[d], 16);
+    else ptx::mbar_arrive(&W.desc_empty[d]);
+  } else {
+    ptx::st_async_b32(ptx::mapa(&W.sink[0], 0), 0u, ptx::mapa(&W.desc_empty[d], 0));
+  }
+}
 
 __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint32_t h) {
   uint32_t d = 0, d_phase = 0;
@@ -553,13 +564,13 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint
           if ((++spins & 255) == 0 && *(volatile uint32_t *)&P.ctrl->abort) break;
         }
         t_claim = ptx::globaltimer();
-        ptx::st_cluster_u32(ptx::mapa(&W.mail[d].payload, 1), payload);
-        ptx::st_cluster_u64(ptx::mapa(&W.mail[d].t_claim, 1), t_claim);
-        ptx::mbar_arrive_remote(&W.mail_full[d], 1);
+        ptx::st_async_v4(ptx::mapa(&W.mail[d], 1), payload, 0u, (uint32_t)t_claim, (uint32_t)(t_claim >> 32),
+                         ptx::mapa(&W.mail_full[d], 1));
       }
       payload = __shfl_sync(0xffffffffu, payload, 0);
     } else {                                  // peer: take the leader's mail
-      ptx::mbar_wait_cluster(&W.mail_full[d], d_phase, &P.ctrl->abort);
+      if (lane == 0) ptx::mbar_arrive_expect_tx(&W.mail_full[d], 16);   // armed for this use
+      ptx::mbar_wait_abortable(&W.mail_full[d], d_phase, &P.ctrl->abort);
       payload = W.mail[d].payload;
       t_claim = W.mail[d].t_claim;
     }
@@ -672,14 +683,14 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W, uint32_t h) {
         if (++s == PIPE) { s = 0; s_phase ^= 1; }
       }
     }
-    release_desc(W, d);
+    release_desc(W, d, h);
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
 }
 
 // Streams a tile's epilogue input in 32 KiB chunks: SGD chunk c = W32 columns
 // [64c, 64c+64) (half of a 64 KiB page); DX chunk c = mask panels 2c, 2c+1.
-__device__ void epi_loader(const Params &P, WorkerSmem &W) {
+__device__ void epi_loader(const Params &P, WorkerSmem &W, uint32_t h) {
   uint32_t d = 0, d_phase = 0, e = 0, e_phase = 0;
 #if SALUS_L2HINT
   const uint64_t pol_w = ptx::policy_evict_first(), pol_a = ptx::policy_evict_last();
@@ -706,7 +717,7 @@ __device__ void epi_loader(const Params &P, WorkerSmem &W) {
         if (++e == EBUF) { e = 0; e_phase ^= 1; }
       }
     }
-    release_desc(W, d);
+    release_desc(W, d, h);
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
 }
@@ -758,7 +769,7 @@ __device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
       ptx::mma_commit_pair(&W.acc_full[b]);
       if (++b == 2) { b = 0; b_phase ^= 1; }
     }
-    release_desc(W, d);
+    release_desc(W, d, 0, true);
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
 }
@@ -770,7 +781,7 @@ __device__ void peer_mma_role(const Params &P, WorkerSmem &W) {
   for (;;) {
     ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
     if (W.desc[d].kind == T_EXIT) break;
-    release_desc(W, d);
+    release_desc(W, d, 1);
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
 }
@@ -815,7 +826,10 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
       }
       ptx::tc_fence_before();
       named_bar(1, EPI_THREADS);
-      if (et == 0) ptx::mbar_arrive_remote(&W.acc_empty[b], 0);  // the leader's MMA may reuse it
+      if (et == 0) {                                // the leader's MMA may reuse it (both CTAs drained)
+        if (ptx::cluster_ctarank() == 0) ptx::mbar_arrive_expect_tx(&W.acc_empty[b], 4);
+        else ptx::st_async_b32(ptx::mapa(&W.sink[1], 0), 0u, ptx::mapa(&W.acc_empty[b], 0));
+      }
       if (++b == 2) { b = 0; b_phase ^= 1; }
     } else if (!td.valid) {
     } else if (td.kind == T_INIT) {
@@ -843,7 +857,7 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
 // Completion warp: per tile, in order — fence, stage counter, and publication
 // of the next stage's tiles or (last stage) the slot's next iteration.  Each
 // CTA of the pair counts its half: a stage of n pair tasks is complete at 2n.
-__device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
+__device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint32_t h) {
   uint32_t d = 0, d_phase = 0;
   for (;;) {
     ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
@@ -906,7 +920,7 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane) {
       }
     }
     __syncwarp();
-    if (lane == 0) release_desc(W, d);
+    if (lane == 0) release_desc(W, d, h);
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
 }
@@ -927,11 +941,11 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
     // completion warp (after the epilogue is done)
     for (uint32_t d = 0; d < NDESC; d++) {
       ptx::mbar_init(&W.desc_full[d], 1);
-      ptx::mbar_init(&W.desc_empty[d], 8);
+      ptx::mbar_init(&W.desc_empty[d], 4);
       ptx::mbar_init(&W.epi_done[d], 1);
       ptx::mbar_init(&W.mail_full[d], 1);
     }
-    for (uint32_t b = 0; b < 2; b++) { ptx::mbar_init(&W.acc_full[b], 1); ptx::mbar_init(&W.acc_empty[b], 2); }
+    for (uint32_t b = 0; b < 2; b++) { ptx::mbar_init(&W.acc_full[b], 1); ptx::mbar_init(&W.acc_empty[b], 1); }
     for (uint32_t e = 0; e < EBUF; e++) { ptx::mbar_init(&W.epi_full[e], 1); ptx::mbar_init(&W.epi_empty[e], EPI_WARPS); }
     ptx::fence_mbar_init();
   }
@@ -949,13 +963,13 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
     if (lane == 0) {
       if (warp == 1) operand_loader(P, W, h);
       else if (warp == 2) { if (h == 0) mma_thread(P, W, tmem); else peer_mma_role(P, W); }
-      else epi_loader(P, W);
+      else epi_loader(P, W, h);
     }
     __syncwarp();
   } else if (warp < DONE_WARP) {
     epilogue_warps(P, W, tmem, tid, my_tasks);
   } else {
-    completion_warp(P, W, lane);
+    completion_warp(P, W, lane, h);
   }
   __syncthreads();
   if (tid == 32 * EPI_WARP0) atomicAdd(&P.ctrl->n_tasks, my_tasks);
