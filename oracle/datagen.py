@@ -4,8 +4,10 @@ Real datasets and trained weights are unavailable, so
 inputs X, targets T and initial weights W are a pure function of
 (seed, job, tensor_id, element index):
 
-    h  = splitmix64(splitmix64(splitmix64(seed) ^ job) ^ (tensor_id << 40 | idx))
-    u  = (h >> 40) * 2^-24                         (24 random bits, in [0,1))
+    h  = splitmix64(splitmix64(splitmix64(seed) ^ job) ^ (tensor_id << 40 | idx >> 1))
+    u  = b * 2^-24, b = h >> 40 for even idx, (h >> 16) & (2^24 - 1) for odd idx
+                                                   (24 random bits, in [0,1); one
+                                                    hash serves two elements)
     v  = fp32((2u - 1) * scale)                    (fp32 multiply, RNE)
     value = bf16_rne(v), held exactly as a wider float
 
@@ -55,7 +57,8 @@ def gen(seed: int, job: int, kind: int, layer: int, iteration: int, rows: int, c
         s = splitmix64(s ^ np.uint64(job))
         tid = np.uint64(tensor_id(kind, layer, iteration)) << np.uint64(40)
         idx = np.arange(rows * cols, dtype=np.uint64)
-        h = splitmix64(s ^ (tid | idx))
-    u = (h >> np.uint64(40)).astype(np.float32) * np.float32(2.0 ** -24)
+        h = splitmix64(s ^ (tid | (idx >> np.uint64(1))))
+    bits = np.where((idx & np.uint64(1)) == 0, h >> np.uint64(40), (h >> np.uint64(16)) & np.uint64(0xFFFFFF))
+    u = bits.astype(np.float32) * np.float32(2.0 ** -24)
     v = (np.float32(2.0) * u - np.float32(1.0)) * np.float32(scale)
     return bf16_rne(v.astype(np.float32)).astype(np.float64).reshape(rows, cols)

@@ -1,7 +1,8 @@
 // datagen.cuh — counter-based synthetic data (DESIGN.md "Input recipe",
 // SURVEY §8(c)-A29), implemented from the written spec:
-//   h = splitmix64(splitmix64(splitmix64(seed) ^ job) ^ (tensor_id << 40 | idx))
-//   u = (h >> 40) * 2^-24;  v = fp32((2u - 1) * scale);  value = bf16_rne(v)
+//   h = splitmix64(splitmix64(splitmix64(seed) ^ job) ^ (tensor_id << 40 | idx >> 1))
+//   u = b * 2^-24, b = h >> 40 (idx even) or (h >> 16) & 0xFFFFFF (idx odd)
+//   v = fp32((2u - 1) * scale);  value = bf16_rne(v)
 //   tensor_id = kind << 20 | layer << 16 | (iteration & 0xFFFF)
 #pragma once
 #include <stdint.h>
@@ -31,12 +32,33 @@ __device__ __forceinline__ float bf16_rne_f32(float v) {
   return __uint_as_float(b);
 }
 
-// value of element idx; `key` from gen_key (xor with idx == or, idx < 2^40)
-__device__ __forceinline__ float gen_value(uint64_t key, uint64_t idx, float scale) {
-  uint64_t h = splitmix64(key ^ idx);
-  float u = __fmul_rn((float)(uint32_t)(h >> 40), 5.9604644775390625e-08f);   // 2^-24, exact
+__device__ __forceinline__ float gen_from_bits(uint32_t bits, float scale) {
+  float u = __fmul_rn((float)bits, 5.9604644775390625e-08f);   // 2^-24, exact
   float v = __fmul_rn(__fsub_rn(__fmul_rn(2.0f, u), 1.0f), scale);
   return bf16_rne_f32(v);
+}
+
+// value of element idx; `key` from gen_key (xor with idx/2 == or, idx < 2^41)
+__device__ __forceinline__ float gen_value(uint64_t key, uint64_t idx, float scale) {
+  const uint64_t h = splitmix64(key ^ (idx >> 1));
+  return gen_from_bits((idx & 1) ? (uint32_t)(h >> 16) & 0xFFFFFFu : (uint32_t)(h >> 40), scale);
+}
+
+// N consecutive elements base .. base+N-1 (N even): one hash per element pair
+// when base is even (the usual case: even row lengths)
+template <int N>
+__device__ __forceinline__ void gen_run(uint64_t key, uint64_t base, float scale, float (&v)[N]) {
+  if ((base & 1) == 0) {
+#pragma unroll
+    for (int p = 0; p < N / 2; p++) {
+      const uint64_t h = splitmix64(key ^ ((base >> 1) + p));
+      v[2 * p] = gen_from_bits((uint32_t)(h >> 40), scale);
+      v[2 * p + 1] = gen_from_bits((uint32_t)(h >> 16) & 0xFFFFFFu, scale);
+    }
+  } else {
+#pragma unroll
+    for (int x = 0; x < N; x++) v[x] = gen_value(key, base + x, scale);
+  }
 }
 
 // fp32(1/sqrt(d)) computed in double then rounded, as the oracle does

@@ -446,11 +446,21 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
         const float inv_b = 1.0f / (float)td.rows_valid;
         const uint64_t key = td.key, base = (uint64_t)row * td.ld_logical + col0;
         const int ncol = row_ok ? (int)td.cols_valid - (int)col0 : 0;
+        if ((base & 1) == 0) {          // one hash per element pair (A29)
 #pragma unroll
-        for (int x = 0; x < 32; x++) {
-          const float tv = gen_value(key, base + x, 1.0f);
-          const float gl = (v[x] - tv) * inv_b;
-          v[x] = x < ncol ? gl : 0.f;
+          for (int p = 0; p < 16; p++) {
+            const uint64_t hv = splitmix64(key ^ ((base >> 1) + p));
+            const float t0 = gen_from_bits((uint32_t)(hv >> 40), 1.0f);
+            const float t1 = gen_from_bits((uint32_t)(hv >> 16) & 0xFFFFFFu, 1.0f);
+            v[2 * p] = 2 * p < ncol ? (v[2 * p] - t0) * inv_b : 0.f;
+            v[2 * p + 1] = 2 * p + 1 < ncol ? (v[2 * p + 1] - t1) * inv_b : 0.f;
+          }
+        } else {
+#pragma unroll
+          for (int x = 0; x < 32; x++) {
+            const float gl = (v[x] - gen_value(key, base + x, 1.0f)) * inv_b;
+            v[x] = x < ncol ? gl : 0.f;
+          }
         }
       }
     }
@@ -506,11 +516,9 @@ __device__ void gen_tile(const TileDesc &td, uint32_t r, uint32_t h) {
 #pragma unroll 2
   for (uint32_t cg = h * (128 / EPI_HALVES); cg < (h + 1) * (128 / EPI_HALVES); cg += 8) {
     float v[8];
+    gen_run(key, base + cg, 1.0f, v);
 #pragma unroll
-    for (int x = 0; x < 8; x++) {
-      const float g = gen_value(key, base + cg + x, 1.0f);
-      v[x] = (int)(cg + x) < ncol ? g : 0.f;
-    }
+    for (int x = 0; x < 8; x++) v[x] = (int)(cg + x) < ncol ? v[x] : 0.f;
     uint4 u;
     u.x = pack_bf16x2(v[0], v[1]); u.y = pack_bf16x2(v[2], v[3]);
     u.z = pack_bf16x2(v[4], v[5]); u.w = pack_bf16x2(v[6], v[7]);

@@ -44,6 +44,22 @@ def test_gen_distribution_and_determinism():
     assert np.array_equal(flat, a)
 
 
+def test_gen_pair_streams_are_independent_uniform():
+    """A29: one splitmix64 value feeds an element pair (bits 40-63 -> even
+    index, bits 16-39 -> odd).  Both streams must be U(-1,1) and the two
+    halves of a pair uncorrelated, and the pairing must follow the flat
+    index, not the row (odd row length)."""
+    a = DG.gen(11, 5, DG.KIND_X, 0, 3, 1, 1 << 18, 1.0).ravel()
+    ev, od = a[0::2], a[1::2]
+    for st in (ev, od):
+        assert abs(st.mean()) < 0.01 and abs(st.var() - 1.0 / 3.0) < 0.01
+        h, _ = np.histogram(st, bins=16, range=(-1, 1))
+        assert h.min() > 0.9 * len(st) / 16
+    assert abs(np.corrcoef(ev, od)[0, 1]) < 0.01
+    odd = DG.gen(11, 5, DG.KIND_X, 0, 3, 3, 7, 1.0)          # 21 elements, rows of 7
+    assert np.array_equal(odd.ravel(), DG.gen(11, 5, DG.KIND_X, 0, 3, 1, 21, 1.0).ravel())
+
+
 def _tiny_job(dims, B, kind=TRAIN, lr=0.05):
     return make_job(0, kind, 0, dims, B, 3, lr=lr, seed=9, request_ticks=(0, 1, 2) if kind else ())
 
