@@ -68,16 +68,6 @@ __device__ __forceinline__ uint32_t mapa(const void *p, uint32_t rank) {
 __device__ __forceinline__ void cluster_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
-__device__ __forceinline__ void st_cluster_u32(uint32_t caddr, uint32_t v) {
-  asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(caddr), "r"(v) : "memory");
-}
-__device__ __forceinline__ void st_cluster_u64(uint32_t caddr, uint64_t v) {
-  asm volatile("st.shared::cluster.u64 [%0], %1;" ::"r"(caddr), "l"(v) : "memory");
-}
-// arrive (release, cluster scope) on the mbarrier at the same offset in CTA `rank`
-__device__ __forceinline__ void mbar_arrive_remote(uint64_t *bar, uint32_t rank) {
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(mapa(bar, rank)) : "memory");
-}
 
 // 16-byte store into the peer CTA's smem that completes as transaction bytes
 // on the peer's mbarrier (async proxy: observed far sooner than a
@@ -123,10 +113,6 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  while (!mbar_try_wait(bar, parity)) {
-  }
-}
 // Same, but gives up (trap -> kernel error, never a hung GPU) once the
 // kernel-wide abort flag is raised by the scheduler or the host watchdog.
 __device__ __forceinline__ void mbar_wait_abortable(uint64_t *bar, uint32_t parity, const uint32_t *abort_flag) {
@@ -136,25 +122,6 @@ __device__ __forceinline__ void mbar_wait_abortable(uint64_t *bar, uint32_t pari
   }
 }
 
-// acquire at cluster scope: for barriers the peer CTA (or the pair's MMA)
-// arrives on
-__device__ __forceinline__ bool mbar_try_wait_cluster(uint64_t *bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, p;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-__device__ __forceinline__ void mbar_wait_cluster(uint64_t *bar, uint32_t parity, const uint32_t *abort_flag) {
-  uint32_t spins = 0;
-  while (!mbar_try_wait_cluster(bar, parity)) {
-    if ((++spins & 4095u) == 0 && *(const volatile uint32_t *)abort_flag) __trap();
-  }
-}
 
 // ---------------------------------------------------------------- bulk copy
 // L2 eviction-priority policies (createpolicy): streamed weights are read or
@@ -176,6 +143,8 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
   asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+// global -> shared bulk copy (TMA unit), completion reported to an mbarrier
+// as transaction bytes, with an L2 eviction-priority policy
 __device__ __forceinline__ void bulk_g2s_hint(void *smem_dst, const void *gmem_src, uint32_t bytes, uint64_t *bar,
                                               uint64_t policy) {
   asm volatile(
@@ -184,19 +153,10 @@ __device__ __forceinline__ void bulk_g2s_hint(void *smem_dst, const void *gmem_s
       "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
       : "memory");
 }
-__device__ __forceinline__ void bulk_s2g_hint(void *gmem_dst, const void *smem_src, uint32_t bytes, uint64_t policy) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;" ::"l"(gmem_dst),
-               "r"(smem_u32(smem_src)), "r"(bytes), "l"(policy)
-               : "memory");
-}
 __device__ __forceinline__ void st_global_v4_hint(void *p, uint4 v, uint64_t policy) {
   asm volatile("st.global.L2::cache_hint.v4.u32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
                "r"(v.w), "l"(policy)
                : "memory");
-}
-// bulk prefetch of [src, src + bytes) into L2 (no completion tracking)
-__device__ __forceinline__ void prefetch_l2(const void *gmem_src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem_src), "r"(bytes) : "memory");
 }
 // 2-D tensor TMA of one box into this CTA's smem, completing on the mbarrier
 // at shared::cluster address `mbar_cluster` -- with .cta_group::2 that may be
@@ -209,35 +169,7 @@ __device__ __forceinline__ void tma_load_2d_pair(void *smem_dst, const void *tma
       "l"(tmap), "r"(c0), "r"(c1), "r"(mbar_cluster), "l"(policy)
       : "memory");
 }
-// arrive + expect_tx on a (possibly remote) mbarrier, cluster scope
-__device__ __forceinline__ void mbar_arrive_expect_tx_cluster(uint32_t mbar_cluster, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.release.cluster.shared::cluster.b64 _, [%0], %1;" ::"r"(mbar_cluster),
-               "r"(bytes)
-               : "memory");
-}
-// global -> shared, completion reported to an mbarrier as transaction bytes.
-// shared -> global bulk copy (async proxy), completion tracked by bulk groups
-__device__ __forceinline__ void bulk_s2g(void *gmem_dst, const void *smem_src, uint32_t bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
-               "r"(smem_u32(smem_src)), "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-// the smem sources of all committed groups have been read
-__device__ __forceinline__ void bulk_wait_read0() {
-  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
-}
-// all committed groups are complete (their global writes performed)
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
-__device__ __forceinline__ void bulk_g2s(void *smem_dst, const void *gmem_src, uint32_t bytes,
-                                         uint64_t *bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(smem_dst)),
-      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
 
 // ---------------------------------------------------------------- tcgen05
 __device__ __forceinline__ void tmem_alloc(uint32_t *smem_result, uint32_t ncols) {
@@ -257,7 +189,9 @@ __device__ __forceinline__ void tc_fence_before() {
 __device__ __forceinline__ void tc_fence_after() {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
-// D[tmem] (+)= A[smem] * B[smem]; kind::f16 covers bf16 inputs, fp32 accumulate
+// D[tmem] (+)= A[smem] * B[smem] over a CTA pair (M = 256: each CTA holds
+// 128 rows of A and N/2 columns of B at the same smem offsets and receives
+// its 128 rows of D); kind::f16 covers bf16 inputs, fp32 accumulate
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                          uint32_t accumulate) {
   asm volatile(
