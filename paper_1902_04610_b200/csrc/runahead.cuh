@@ -7,8 +7,12 @@
 // within a lane"): whoever holds the slot's `running` token —
 // the scheduler after an append to an idle slot, or the worker thread that
 // completes an iteration's last tile — takes the next record and starts it.
-// The handoff is a Dekker-style store/fence/load on (q_tail, running), so an
-// append racing with the last completion is never lost.
+// The handoff goes through one 64-bit word per slot, qstate = tail << 32 |
+// running: the appender's atomic add (release) publishes a record and tells
+// it whether the slot was idle; the holder releases `running` only with a
+// CAS that expects the tail it has consumed up to, so an append racing with
+// the last completion is never lost and no store/fence/load Dekker pair (two
+// full fences per handoff) is needed.
 #pragma once
 #include "salus_dev.h"
 #include "ptx.cuh"
@@ -24,24 +28,31 @@ __device__ __forceinline__ void st_release_u32(uint32_t *p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+__device__ __forceinline__ unsigned long long ld_acquire_u64q(const unsigned long long *p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long atom_add_release_u64(unsigned long long *p, unsigned long long v) {
+  unsigned long long old;
+  asm volatile("atom.add.release.gpu.global.u64 %0, [%1], %2;" : "=l"(old) : "l"(p), "l"(v) : "memory");
+  return old;
+}
+
 // Caller holds `running`.  Takes the next record (true) or releases the token
-// (false), re-checking for an append that raced with the release.
+// (false): the CAS succeeds only if no record was appended since the load.
 __device__ __forceinline__ bool take_next(Slot &sl, DispRec *rec) {
   for (;;) {
     const uint32_t h = *(volatile uint32_t *)&sl.q_head;
-    uint32_t t = ld_acquire_u32(&sl.q_tail);
-    if (h != t) {
+    const unsigned long long st = ld_acquire_u64q(&sl.qstate);
+    if ((uint32_t)(st >> 32) != h) {
       const volatile DispRec *vr = &sl.recs[h % RQ];
       rec->job = vr->job; rec->iter = vr->iter; rec->seq = vr->seq; rec->lane_id = vr->lane_id; rec->pad = 0;
       rec->append_ns = vr->append_ns;
       st_release_u32(&sl.q_head, h + 1);
       return true;
     }
-    st_release_u32(&sl.running, 0u);
-    __threadfence();                                  // store running -> load q_tail (SC)
-    t = ld_acquire_u32(&sl.q_tail);
-    if (h == t) return false;
-    if (atomicCAS(&sl.running, 0u, 1u) != 0u) return false;   // the appender took it
+    if (atomicCAS(&sl.qstate, st, st & ~1ull) == st) return false;   // released
   }
 }
 

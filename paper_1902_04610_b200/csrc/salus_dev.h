@@ -76,10 +76,11 @@ struct alignas(256) Slot {
   uint32_t lane_id;
   uint64_t append_ns;       // when the in-flight iteration's record was appended
   uint32_t stage_done[MAX_STAGES + 2];
-  // dispatch ring
-  uint32_t q_tail;          // records appended (scheduler; release)
+  // dispatch ring: qstate = records appended << 32 | running (1 while an
+  // iteration is in flight or being started), one word so that append and
+  // release race through single atomics
+  unsigned long long qstate;
   uint32_t q_head;          // records started (only the holder of `running`)
-  uint32_t running;         // 1 while an iteration is in flight or being started
   DispRec recs[RQ];
 };
 
@@ -129,6 +130,7 @@ struct Params {
   float *dump;
   const volatile uint32_t *host_abort;   // mapped pinned host flag
   uint32_t n_jobs, n_infer, Cp, policy, max_lanes, flags, n_workers;
+  uint32_t n_req;                  // request ticks in req_ticks
   int64_t switch_ticks;
   uint64_t timeout_ns;
 };

@@ -419,6 +419,7 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   P.host_abort = ctx->host_abort_dev;
   P.n_jobs = n;
   P.n_infer = (uint32_t)inf.size();
+  P.n_req = (uint32_t)req.size();
   P.Cp = ctx->Cp;
   P.policy = ctx->cfg.policy;
   P.max_lanes = ctx->cfg.max_lanes;

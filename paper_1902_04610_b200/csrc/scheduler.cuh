@@ -25,6 +25,8 @@ constexpr int64_t IDLE_T = INT64_MAX;
 constexpr uint16_t NONE16 = 0xFFFF;
 constexpr uint32_t KEY_BITS = 11;          // dense job index < 2048 in key low bits
 
+constexpr uint32_t REQ_STAGE = 9216;
+
 struct SchedShared {
   // lane table, index order == lane id order
   uint32_t lane_id[MAX_LANES], lane_L[MAX_LANES], lane_slot[MAX_LANES], lane_back[MAX_LANES];
@@ -55,6 +57,9 @@ struct SchedShared {
   // phase_dispatch: per-slot minimum dispatch key over runnable residents
   unsigned long long slot_key[MAX_LANES];
   uint32_t q_head_seen[MAX_LANES];          // last q_head read per slot (backpressure)
+  // request ticks staged in smem when they fit (C3: 8400): every request
+  // arrival otherwise costs a dependent global load on the scheduler's path
+  int64_t req_stage[REQ_STAGE];
 };
 
 __device__ __forceinline__ int64_t warp_min_i64(int64_t v) {
@@ -90,6 +95,8 @@ struct Sched {
   int64_t t = 0;
   uint64_t seq = 0, n_log = 0, n_ticks = 0, wait_ns = 0;
   uint64_t wait_fence_ns = 0, wait_ring_ns = 0;     // parts of wait_ns: page fences, full dispatch ring
+  uint64_t append_ns = 0;                          // SALUS_DBG_SCHED builds
+  const int64_t *rq = nullptr;                     // request ticks (smem stage or global)
   uint32_t nl = 0, qn = 0, an = 0, next_lane = 0, sumP = 0, sumL = 0, arr_ptr = 0, n_done = 0;
   uint32_t free_top = 0, max_lanes = 0, err = 0;
   uint64_t slot_free = ~0ull;
@@ -99,7 +106,7 @@ struct Sched {
   uint64_t pend_mask = 0;                    // target slots with page-reuse fences
 
   __device__ Sched(const Params &p_, SchedShared &s_)
-      : P(p_), S(s_), tid(threadIdx.x & 31), physical(!(p_.flags & SALUS_FLAG_NULL_WORK)) {}
+      : P(p_), S(s_), tid(threadIdx.x & 31), physical(!(p_.flags & SALUS_FLAG_NULL_WORK)), rq(p_.req_ticks) {}
 
   __device__ void fail(int32_t code, uint32_t info) {
     if (tid == 0 && err == 0) {
@@ -238,12 +245,17 @@ struct Sched {
   // ------------------------------------------------------------ phases
   __device__ void init() {
     const uint32_t N = P.n_jobs;
+    if (P.n_req <= REQ_STAGE) {
+      for (uint32_t i = tid; i < P.n_req; i += 32) S.req_stage[i] = P.req_ticks[i];
+      __syncwarp();
+      rq = S.req_stage;
+    }
     for (uint32_t j = tid; j < N; j += 32) {
       const DevJob &J = P.jobs[j];
       S.svc[j] = 0; S.c[j] = J.iter_ticks; S.done[j] = 0; S.pending[j] = 0; S.next_req[j] = 0;
       S.n[j] = J.n_iters; S.p[j] = J.p_pages; S.e[j] = J.e_pages; S.ap[j] = J.ap_pages; S.ae[j] = J.ae_pages;
       S.id[j] = J.job_id; S.st[j] = ST_NOT_ARRIVED; S.jslot[j] = 0xFF; S.kind[j] = (uint8_t)J.kind;
-      S.nrt[j] = J.kind == SALUS_INFER ? P.req_ticks[J.req_off] : IDLE_T;
+      S.nrt[j] = J.kind == SALUS_INFER ? rq[J.req_off] : IDLE_T;
       S.req_off[j] = J.req_off;
       salus_job_stat &st = P.stats[j];
       st.job_id = J.job_id; st.first_lane = NONE32; st.admit_tick = -1; st.first_start_tick = -1;
@@ -309,8 +321,9 @@ struct Sched {
         n_done++; dirty = true; sumP -= S.p[j];
         __syncwarp();
         remove_adm(j);
-        emit(SALUS_REC_JOB_FINISH, S.lane_id[i], S.id[j], S.n[j], P.stats[j].completion_seq);
-        push_pages(job_table(j), S.ap[j], slot, P.stats[j].completion_seq);
+        // completion_seq = seq of the final iteration = the lane's in-flight one
+        emit(SALUS_REC_JOB_FINISH, S.lane_id[i], S.id[j], S.n[j], S.lane_seq[i]);
+        push_pages(job_table(j), S.ap[j], slot, S.lane_seq[i]);
         // residents left in this lane: count, max e, max actual e
         uint32_t cnt = 0, maxe = 0, maxae = 0;
         for (uint32_t a = tid; a < an; a += 32) {
@@ -400,9 +413,13 @@ struct Sched {
         if ((S.st[j] == ST_QUEUED || S.st[j] == ST_ADMITTED) && S.nrt[j] == t) {
           const uint32_t off = S.req_off[j];
           uint32_t nr = S.next_req[j];
-          while (nr < S.n[j] && P.req_ticks[off + nr] == t) { nr++; cnt++; }
+          int64_t nt = t;                  // == rq[off + nr] (that is why we are here)
+          while (nt == t) {
+            nr++; cnt++;
+            nt = nr < S.n[j] ? rq[off + nr] : IDLE_T;
+          }
           S.next_req[j] = nr;
-          S.nrt[j] = nr < S.n[j] ? P.req_ticks[off + nr] : IDLE_T;
+          S.nrt[j] = nt;
         }
       }
       uint32_t mask = __ballot_sync(0xffffffffu, cnt > 0);
@@ -544,6 +561,13 @@ struct Sched {
   // take the `running` token and start it here, else the worker finishing
   // the slot's current iteration will.
   __device__ void append(uint32_t slot, uint32_t lane_id, uint32_t j) {
+#if SALUS_DBG_SCHED
+    const uint64_t ta_ = ptx::globaltimer();
+    append_body(slot, lane_id, j);
+    append_ns += ptx::globaltimer() - ta_;
+  }
+  __device__ void append_body(uint32_t slot, uint32_t lane_id, uint32_t j) {
+#endif
     wait_fences(slot);
     if (err) return;
     Slot &sl = P.slots[slot];
@@ -574,9 +598,10 @@ struct Sched {
       volatile DispRec *vr = &sl.recs[tl % RQ];
       vr->job = j; vr->iter = S.done[j]; vr->seq = seq; vr->lane_id = lane_id; vr->pad = 0;
       vr->append_ns = ptx::globaltimer();
-      st_release_u32(&sl.q_tail, tl + 1);
-      __threadfence();                                     // store q_tail -> CAS running (SC)
-      won = atomicCAS(&sl.running, 0u, 1u) == 0u;
+      // publish (release) and learn whether the slot was idle in one atomic;
+      // only the scheduler ever sets `running`, so taking it needs no CAS
+      won = (atom_add_release_u64(&sl.qstate, 1ull << 32) & 1ull) == 0;
+      if (won) atomicOr(&sl.qstate, 1ull);
       S.sq_tail[slot] = tl + 1;
       S.last_app[slot] = seq + 1;
     }
@@ -638,7 +663,7 @@ struct Sched {
         S.lane_cur[i] = (uint16_t)j; S.lane_last[i] = (uint16_t)j; S.lane_seq[i] = seq;
         if (S.kind[j] == SALUS_INFER) S.pending[j] -= 1;
         salus_job_stat &st = P.stats[j];
-        if (st.first_start_tick < 0) st.first_start_tick = t;
+        if (S.done[j] == 0) st.first_start_tick = t;   // a job's iterations never overlap
         st.completion_seq = seq;
       }
       __syncwarp();
@@ -655,24 +680,39 @@ struct Sched {
   __device__ void run() {
     init();
     const uint64_t wall0 = ptx::globaltimer();
+#if SALUS_DBG_SCHED   // per-phase time (ns) -> the tail of the trace buffer
+    uint64_t ph[6] = {0, 0, 0, 0, 0, 0};
+#define SALUS_PH(i, stmt) { const uint64_t t0_ = ptx::globaltimer(); stmt; ph[i] += ptx::globaltimer() - t0_; }
+#else
+#define SALUS_PH(i, stmt) stmt;
+#endif
     while (n_done < P.n_jobs && !err) {
-      const int64_t tn = next_event();
+      int64_t tn;
+      SALUS_PH(0, tn = next_event())
       if (tn == IDLE_T) { fail(SALUS_E_STUCK, 4); break; }
       t = tn;
       n_ticks++;
       dirty = false;
-      phase_completions();
+      SALUS_PH(1, phase_completions())
       if (err) break;
-      phase_arrivals();
-      if (qn > 0 && dirty) phase_admission();
+      SALUS_PH(2, phase_arrivals())
+      if (qn > 0 && dirty) SALUS_PH(3, phase_admission())
       if (P.flags & SALUS_FLAG_CHECK) check_safety();
-      phase_dispatch();
+      SALUS_PH(4, phase_dispatch())
       if ((n_ticks & 255) == 0) {
         uint32_t bad = 0;
         if (tid == 0) bad = host_abort();
         if (__shfl_sync(0xffffffffu, bad, 0)) fail(SALUS_E_TIMEOUT, 5);
       }
     }
+#if SALUS_DBG_SCHED
+    if (tid == 0 && P.trace_cap) {
+      uint64_t *dbg = reinterpret_cast<uint64_t *>(P.trace + P.trace_cap) - 8;
+      for (int i = 0; i < 6; i++) dbg[i] = ph[i];
+      dbg[6] = append_ns;
+    }
+#endif
+#undef SALUS_PH
     if (physical && !err) drain();
     // release the workers
     {
