@@ -145,7 +145,7 @@ struct Sched {
       dst[i] = pg;
       if (physical) {
         const uint64_t fs = P.fence_seq[pg];
-        const uint32_t src = P.fence_slot[pg];
+        const uint32_t src = fs ? P.fence_slot[pg] : target;   // fence_slot is only set with a fence
         if (fs && src != target) {
           atomicMax(&P.pend_fence[target * MAX_LANES + src], (unsigned long long)fs);
           any = true;
