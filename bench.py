@@ -158,6 +158,40 @@ def switch_latency(S, device):
             "same_job_gap_us": pct(gap)}
 
 
+def online_submission(S, device, n_jobs=64, period_s=0.002, n_iters=20):
+    """C2a-shaped training jobs (MLP [1024]^4, B=256)
+    handed to the RUNNING kernel one every `period_s` (PACK, 1 GiB).  Host
+    cost of salus_submit_live, and device time from the scheduler taking a
+    job's arrival to its first tile (both clocks: globaltimer)."""
+    import time
+    from workloads import make_job
+    jobs = [make_job(1 + k, TRAIN, 0, (1024, 1024, 1024, 1024), 256, n_iters, lr=1e-3, seed=1000 + k)
+            for k in range(n_jobs)]
+    ctx = S.Context([], 1 << 30, S.PACK, device=device, online=True, max_jobs=n_jobs, log=True)
+    host_us = []
+    try:
+        ctx.run_async()
+        time.sleep(0.02)
+        for j in jobs:
+            t0 = time.perf_counter()
+            ctx.submit_live(j)
+            host_us.append((time.perf_counter() - t0) * 1e6)
+            time.sleep(period_s)
+        ctx.end_submissions()
+        stats = ctx.wait()
+        rs = ctx.run_stats()
+    finally:
+        ctx.close()
+    lat = [(s["wall_start_ns"] - s["wall_arrive_ns"]) / 1e3 for s in stats.values()]
+    span = (max(s["wall_end_ns"] for s in stats.values()) - min(s["wall_arrive_ns"] for s in stats.values())) / 1e9
+    return {"config": f"{n_jobs} x MLP[1024]^4 B=256 x {n_iters} iters, one live submission per "
+                      f"{period_s * 1e3:.1f} ms into a running kernel, PACK, 1 GiB",
+            "jobs": len(stats), "iterations": int(rs["n_dispatch"]),
+            "submit_call_us": {"p50": float(np.median(host_us)), "p99": float(np.percentile(host_us, 99))},
+            "arrival_to_first_tile_us": {"p50": float(np.median(lat)), "p99": float(np.percentile(lat, 99))},
+            "iters_per_s_over_span": rs["n_dispatch"] / span}
+
+
 def overhead_vs_standalone(S, device, dims=(1024, 1024, 1024, 1024), batch=256, iters=100):
     """SURVEY NEXT-1 (the analogue of PAPER.md fig:exp5-17): the
     per-iteration time of ONE job running alone inside Salus (device wall
@@ -422,6 +456,10 @@ def main():
             line["c3_switch"] = switch_latency(S, local)
         except Exception as exc:  # noqa: BLE001
             line["c3_switch"] = {"error": str(exc)[:200]}
+        try:
+            line["online_submission"] = online_submission(S, local)
+        except Exception as exc:  # noqa: BLE001
+            line["online_submission"] = {"error": str(exc)[:200]}
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(jobs, cap)
         print(json.dumps(line), flush=True)

@@ -66,7 +66,10 @@ enum {
   SALUS_FLAG_LOG = 1,        /* record the canonical schedule log + wall stamps  */
   SALUS_FLAG_NULL_WORK = 2,  /* schedule only: no iteration work is executed     */
   SALUS_FLAG_CHECK = 4,      /* device asserts the safety invariants every tick  */
-  SALUS_FLAG_TRACE = 8       /* record one salus_trace_rec per executed tile     */
+  SALUS_FLAG_TRACE = 8,      /* record one salus_trace_rec per executed tile     */
+  SALUS_FLAG_ONLINE = 16     /* online submission: the run
+                                also admits jobs submitted with salus_submit_live
+                                while it is live, until salus_end_submissions    */
 };
 
 /* salus_job.dump */
@@ -210,9 +213,34 @@ typedef struct {
   uint64_t completion_seq;    /* dispatch seq of its final iteration (A25)       */
   uint64_t wall_start_ns;     /* globaltimer at its first tile start              */
   uint64_t wall_end_ns;       /* globaltimer at its last tile end                 */
+  uint64_t wall_arrive_ns;    /* globaltimer when the scheduler processed its
+                                 arrival (for a live job: ~when it was seen)      */
 } salus_job_stat;
 
 int salus_run(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats);
+
+/* ---------------------------------------------------------------------
+ * Online submission (SALUS_FLAG_ONLINE, the paper's
+ * "a session is created when a job is submitted").
+ *
+ * salus_run = salus_run_async + salus_wait.  Between the two, on the thread
+ * that owns ctx or any other, salus_submit_live hands the running kernel a
+ * new TRAIN job: the host writes its device descriptor into a reserved slot
+ * (cudaMemcpy on a private stream) and publishes it through mapped pinned
+ * memory; the device scheduler notices it at a tick t once every job known
+ * before has arrived, and gives it arrival tick t + 1 (logged as
+ * JOB_QUEUED), so replaying the logged arrival ticks through the oracle
+ * reproduces the whole log.  Live job ids must exceed every earlier id;
+ * their dumps come out of cfg.dump_bytes; the descriptor is copied.  Errors: E_STATE (not running /
+ * not online / submissions ended), E_INVAL, E_DUPLICATE, E_UNSCHEDULABLE,
+ * E_CAPACITY (max_jobs or the reserved page-table / ring space).
+ * salus_end_submissions lets the kernel exit once every job is done.
+ * salus_wait has salus_run's outputs and errors.
+ * ------------------------------------------------------------------- */
+int salus_run_async(salus_ctx *ctx);
+int salus_submit_live(salus_ctx *ctx, const salus_job *job);
+int salus_end_submissions(salus_ctx *ctx);
+int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats);
 
 /* Whole-run counters of the last salus_run. */
 typedef struct {

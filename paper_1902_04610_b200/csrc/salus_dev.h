@@ -23,7 +23,8 @@ enum : uint8_t { ST_NOT_ARRIVED = 0, ST_QUEUED = 1, ST_ADMITTED = 2, ST_DONE = 3
 // Static per-job descriptor, uploaded by salus_prepare.  The dense index of
 // a job is its rank in (arrival_tick, job_id) order, so every "(arrival, id)"
 // tie-break of the readings (A11-A15) is a comparison of dense indices.
-struct DevJob {
+struct alignas(128) DevJob {   // whole cache lines: a live job's descriptor never
+                               // shares one with a descriptor already read
   uint32_t job_id, kind, n_layers, batch;
   int64_t arrival, iter_ticks;
   uint32_t n_iters, p_pages, e_pages;     // declared sizes in pages (schedule)
@@ -131,6 +132,8 @@ struct Params {
   const volatile uint32_t *host_abort;   // mapped pinned host flag
   uint32_t n_jobs, n_infer, Cp, policy, max_lanes, flags, n_workers;
   uint32_t n_req;                  // request ticks in req_ticks
+  uint32_t max_jobs;               // descriptor capacity (online submission)
+  uint32_t *live;                  // mapped {n_published, closed} (SALUS_FLAG_ONLINE), else null
   int64_t switch_ticks;
   uint64_t timeout_ns;
 };

@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <mutex>
 #include <chrono>
 #include <cmath>
 #include <cstring>
@@ -91,6 +93,15 @@ struct salus_ctx {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   salus_run_stats last{};
   bool ran = false;
+  // online submission (SALUS_FLAG_ONLINE)
+  bool running = false, ended = false;
+  std::mutex live_mu;
+  uint32_t *live = nullptr, *live_dev = nullptr;   // mapped pinned {n_published, closed}
+  cudaStream_t side = nullptr;                     // private stream for descriptor uploads
+  uint64_t ppt_used = 0, ppt_cap = 0, ring_tiles = 0, dump_cur = 0, dump_cap = 0;
+  uint32_t max_id = 0, n_pre = 0;
+  bool t_out = false;
+  std::chrono::steady_clock::time_point t0;
 };
 
 namespace {
@@ -202,25 +213,10 @@ int salus_submit_job(salus_ctx *ctx, const salus_job *job) {
   return SALUS_OK;
 }
 
-static void compute_layout(salus_ctx *c) {
-  const uint32_t n = (uint32_t)c->jobs.size();
-  // dense order = (arrival, id) rank
-  std::vector<uint32_t> order(n);
-  for (uint32_t i = 0; i < n; i++) order[i] = i;
-  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-    const salus_job &x = c->jobs[a].j, &y = c->jobs[b].j;
-    return x.arrival_tick != y.arrival_tick ? x.arrival_tick < y.arrival_tick : x.job_id < y.job_id;
-  });
-  c->dense_to_submit = order;
-  c->djobs.assign(n, DevJob{});
-  c->id_to_dense.clear();
-  const uint64_t G = c->cfg.page_bytes;
-  uint64_t req_total = 0, ppt_total = 0, dump_cur = 0, max_ae = 1, max_tiles = 1, dispatches = 0;
-  for (uint32_t d = 0; d < n; d++) {
-    const HostJob &h = c->jobs[order[d]];
+static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req_total, uint64_t &ppt_total,
+                        uint64_t &dump_cur) {
     const salus_job &j = h.j;
-    DevJob &D = c->djobs[d];
-    c->id_to_dense[j.job_id] = d;
+    const uint64_t G = c->cfg.page_bytes;
     D.job_id = j.job_id; D.kind = j.kind; D.n_layers = j.n_layers; D.batch = j.batch;
     D.arrival = j.arrival_tick; D.iter_ticks = (int64_t)j.iter_ticks; D.n_iters = j.n_iters;
     D.p_pages = (uint32_t)((j.persistent_bytes + G - 1) / G);
@@ -280,15 +276,53 @@ static void compute_layout(salus_ctx *c) {
       }
     }
     D.n_stages = last_stage(j.kind, L) + 1;
-    for (uint32_t s = 0; s < D.n_stages; s++) max_tiles = std::max<uint64_t>(max_tiles, D.stage_tiles[s]);
     D.dump_out_off = dump_cur;
     if (j.dump & SALUS_DUMP_OUTPUTS) dump_cur += (uint64_t)j.n_iters * j.batch * j.dims[L];
     D.dump_w_off = dump_cur;
     if (j.dump & SALUS_DUMP_WEIGHTS)
       for (uint32_t l = 1; l <= L; l++) dump_cur += (uint64_t)j.dims[l - 1] * j.dims[l];
+}
+
+static void compute_layout(salus_ctx *c) {
+  const uint32_t n = (uint32_t)c->jobs.size();
+  // dense order = (arrival, id) rank
+  std::vector<uint32_t> order(n);
+  for (uint32_t i = 0; i < n; i++) order[i] = i;
+  std::sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    const salus_job &x = c->jobs[a].j, &y = c->jobs[b].j;
+    return x.arrival_tick != y.arrival_tick ? x.arrival_tick < y.arrival_tick : x.job_id < y.job_id;
+  });
+  c->dense_to_submit = order;
+  c->djobs.assign(n, DevJob{});
+  c->id_to_dense.clear();
+  const uint64_t G = c->cfg.page_bytes;
+  uint64_t req_total = 0, ppt_total = 0, dump_cur = 0, max_ae = 1, max_tiles = 1, dispatches = 0;
+  for (uint32_t d = 0; d < n; d++) {
+    const HostJob &h = c->jobs[order[d]];
+    const salus_job &j = h.j;
+    DevJob &D = c->djobs[d];
+    c->id_to_dense[j.job_id] = d;
+    fill_devjob(c, h, D, req_total, ppt_total, dump_cur);
+    for (uint32_t s = 0; s < D.n_stages; s++) max_tiles = std::max<uint64_t>(max_tiles, D.stage_tiles[s]);
     max_ae = std::max<uint64_t>(max_ae, D.ae_pages);
     dispatches += j.n_iters;
   }
+  const bool online = (c->cfg.flags & SALUS_FLAG_ONLINE) != 0;
+  c->ppt_used = ppt_total;
+  c->ppt_cap = ppt_total;
+  c->dump_cur = dump_cur;
+  c->n_pre = n;
+  uint32_t n_cap = n;
+  if (online) {
+    // room for live jobs: descriptors and stats up to max_jobs, page-table
+    // entries for 4 x C of persistent memory over the run, lanes up to C,
+    // stages of up to 4096 pair tasks (checked at salus_submit_live)
+    c->ppt_cap += 4ull * c->Cp;
+    max_ae = std::max<uint64_t>(max_ae, c->Cp);
+    max_tiles = std::max<uint64_t>(max_tiles, 4096);
+    n_cap = c->cfg.max_jobs;
+  }
+  c->ring_tiles = max_tiles;
   c->lpt_stride = (uint32_t)max_ae;
   uint64_t rc = 1024;
   const uint64_t need = 2 * (MAX_LANES * max_tiles + 4096);
@@ -296,14 +330,15 @@ static void compute_layout(salus_ctx *c) {
   c->ring_cap = rc;
   c->log_cap = 0;
   if (c->cfg.flags & SALUS_FLAG_LOG)
-    c->log_cap = c->cfg.log_capacity ? c->cfg.log_capacity : dispatches + 6ull * n + 16;
+    c->log_cap = c->cfg.log_capacity ? c->cfg.log_capacity
+                                     : dispatches + 6ull * n + 16 + (online ? (1ull << 20) : 0);
   uint64_t o = 0;
   auto take = [&](uint64_t bytes) { uint64_t r = o; o = align_up(o + bytes, 256); return r; };
   c->off_ctrl = take(sizeof(Ctrl));
-  c->off_jobs = take(sizeof(DevJob) * std::max<uint64_t>(n, 1));
+  c->off_jobs = take(sizeof(DevJob) * std::max<uint64_t>(n_cap, 1));
   c->off_req = take(8 * std::max<uint64_t>(req_total, 1));
   c->off_inf = take(2 * std::max<uint64_t>(n, 1));
-  c->off_ppt = take(4 * std::max<uint64_t>(ppt_total, 1));
+  c->off_ppt = take(4 * std::max<uint64_t>(c->ppt_cap, 1));
   c->off_lpt = take(4ull * MAX_LANES * c->lpt_stride);
   c->off_free = take(4ull * c->Cp);
   c->off_fslot = take(1ull * c->Cp);
@@ -313,8 +348,10 @@ static void compute_layout(salus_ctx *c) {
   c->off_ring = take(8 * c->ring_cap);
   c->off_log = take(sizeof(salus_log_rec) * std::max<uint64_t>(c->log_cap, 1));
   c->off_wall = take(sizeof(salus_wall_rec) * std::max<uint64_t>(c->log_cap, 1));
-  c->off_stats = take(sizeof(salus_job_stat) * std::max<uint64_t>(n, 1));
-  c->off_dump = take(4 * std::max<uint64_t>(dump_cur, 1));
+  c->off_stats = take(sizeof(salus_job_stat) * std::max<uint64_t>(n_cap, 1));
+  // online: cfg.dump_bytes reserves room for live jobs' dumps as well
+  c->dump_cap = online ? std::max<uint64_t>(dump_cur, c->cfg.dump_bytes / 4) : dump_cur;
+  c->off_dump = take(4 * std::max<uint64_t>(c->dump_cap, 1));
   c->trace_cap = (c->cfg.flags & SALUS_FLAG_TRACE) ? (c->cfg.trace_capacity ? c->cfg.trace_capacity : (1ull << 20)) : 0;
   c->off_trace = take(sizeof(salus_trace_rec) * std::max<uint64_t>(c->trace_cap, 1));
   c->total = o;
@@ -330,7 +367,8 @@ int salus_meta_bytes(const salus_ctx *ctx, uint64_t *bytes) {
 int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   if (!ctx) return SALUS_E_INVAL;
   if (ctx->state != 0) return fail(ctx, SALUS_E_STATE, "already prepared");
-  if (ctx->jobs.empty()) return fail(ctx, SALUS_E_STATE, "no jobs submitted");
+  const bool online = (ctx->cfg.flags & SALUS_FLAG_ONLINE) != 0;
+  if (ctx->jobs.empty() && !online) return fail(ctx, SALUS_E_STATE, "no jobs submitted");
   compute_layout(ctx);
   if (!meta || (reinterpret_cast<uintptr_t>(meta) & 255)) return fail(ctx, SALUS_E_INVAL, "meta must be 256-B aligned");
   if (meta_bytes < ctx->total) return fail(ctx, SALUS_E_CAPACITY, "meta buffer too small");
@@ -427,13 +465,26 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   P.n_workers = ctx->grid / 2 - 1;
   P.switch_ticks = (int64_t)ctx->cfg.switch_ticks;
   P.timeout_ns = (uint64_t)ctx->cfg.timeout_ms * 1000000ull;
+  P.live = nullptr;
+  P.max_jobs = ctx->cfg.max_jobs;
+  if (online) {
+    if ((e = cudaHostAlloc(reinterpret_cast<void **>(&ctx->live), 64, cudaHostAllocMapped)))
+      return cuda_fail(ctx, e, "cudaHostAlloc live");
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&ctx->live_dev), ctx->live, 0)))
+      return cuda_fail(ctx, e, "cudaHostGetDevicePointer live");
+    if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking))) return cuda_fail(ctx, e, "side stream");
+    P.live = ctx->live_dev;
+    for (const HostJob &h : ctx->jobs) ctx->max_id = std::max(ctx->max_id, h.j.job_id);
+  }
   ctx->state = 1;
   return SALUS_OK;
 }
 
-int salus_run(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats) {
+int salus_run_async(salus_ctx *ctx) {
   if (!ctx) return SALUS_E_INVAL;
   if (ctx->state != 1) return fail(ctx, SALUS_E_STATE, "salus_prepare first");
+  if (ctx->running) return fail(ctx, SALUS_E_STATE, "already running");
+  if ((ctx->cfg.flags & SALUS_FLAG_ONLINE) && ctx->ran) return fail(ctx, SALUS_E_STATE, "an online context runs once");
   cudaError_t e = cudaSetDevice(ctx->cfg.device);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
   cudaStream_t st = static_cast<cudaStream_t>(ctx->cfg.stream);
@@ -446,25 +497,115 @@ int salus_run(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_
     return cuda_fail(ctx, e, "reset");
   *reinterpret_cast<volatile uint32_t *>(ctx->host_abort) = 0;
   if ((e = cudaEventRecord(ctx->ev0, st))) return cuda_fail(ctx, e, "event");
+  if (ctx->live) {
+    std::lock_guard<std::mutex> g(ctx->live_mu);
+    reinterpret_cast<volatile uint32_t *>(ctx->live)[0] = (uint32_t)ctx->jobs.size();   // published so far
+    reinterpret_cast<volatile uint32_t *>(ctx->live)[1] = 0;                           // submissions open
+    ctx->ended = false;
+  }
   int rc = launch_persistent(ctx->P, ctx->grid, st);
   if (rc) return cuda_fail(ctx, (cudaError_t)rc, "cooperative launch");
   if ((e = cudaEventRecord(ctx->ev1, st))) return cuda_fail(ctx, e, "event");
+  ctx->running = true;
+  ctx->t_out = false;
+  ctx->t0 = std::chrono::steady_clock::now();
+  return SALUS_OK;
+}
+
+int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats);
+
+int salus_run(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats) {
+  int rc = salus_run_async(ctx);
+  if (rc) return rc;
+  if (ctx->live) salus_end_submissions(ctx);
+  return salus_wait(ctx, stats, max_stats, n_stats);
+}
+
+int salus_end_submissions(salus_ctx *ctx) {
+  if (!ctx) return SALUS_E_INVAL;
+  if (!ctx->live) return fail(ctx, SALUS_E_STATE, "not an online context");
+  std::lock_guard<std::mutex> g(ctx->live_mu);
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  reinterpret_cast<volatile uint32_t *>(ctx->live)[1] = 1;
+  ctx->ended = true;
+  return SALUS_OK;
+}
+
+int salus_submit_live(salus_ctx *ctx, const salus_job *job) {
+  if (!ctx || !job) return SALUS_E_INVAL;
+  if (!ctx->live) return fail(ctx, SALUS_E_STATE, "not an online context (SALUS_FLAG_ONLINE)");
+  std::lock_guard<std::mutex> g(ctx->live_mu);
+  if (!ctx->running || ctx->ended) return fail(ctx, SALUS_E_STATE, "no live run accepting submissions");
+  if (ctx->id_to_submit.count(job->job_id)) return fail(ctx, SALUS_E_DUPLICATE, "duplicate job id");
+  if (job->kind != SALUS_TRAIN) return fail(ctx, SALUS_E_INVAL, "live submission takes TRAIN jobs");
+  if (!ctx->jobs.empty() && job->job_id <= ctx->max_id)
+    return fail(ctx, SALUS_E_INVAL, "live job ids must increase");
+  std::string why;
+  int rc = validate_job(job, (ctx->cfg.flags & SALUS_FLAG_NULL_WORK) != 0, &why);
+  if (rc) return fail(ctx, rc, "job " + std::to_string(job->job_id) + ": " + why);
+  const uint64_t G = ctx->cfg.page_bytes;
+  const uint64_t p = (job->persistent_bytes + G - 1) / G, e = (job->ephemeral_bytes + G - 1) / G;
+  if (p + e > ctx->Cp) return fail(ctx, SALUS_E_UNSCHEDULABLE, "p + e > C pages (A22)");
+  if (ctx->jobs.size() >= ctx->cfg.max_jobs) return fail(ctx, SALUS_E_CAPACITY, "max_jobs reached");
+  HostJob h;
+  h.j = *job;
+  h.j.request_ticks = nullptr;
+  h.j.arrival_tick = INT64_MAX;        // stamped by the device scheduler
+  h.fp = footprint(*job);
+  h.submit_idx = (uint32_t)ctx->jobs.size();
+  DevJob D{};
+  uint64_t req_dummy = 0, ppt = ctx->ppt_used, dump = ctx->dump_cur;
+  fill_devjob(ctx, h, D, req_dummy, ppt, dump);
+  if (ppt > ctx->ppt_cap) return fail(ctx, SALUS_E_CAPACITY, "live page-table space exhausted");
+  if (dump > ctx->dump_cap) return fail(ctx, SALUS_E_CAPACITY, "dump_bytes exceeded");
+  for (uint32_t s = 0; s < D.n_stages; s++)
+    if (D.stage_tiles[s] > ctx->ring_tiles) return fail(ctx, SALUS_E_CAPACITY, "stage exceeds the task ring");
+  const uint32_t d = (uint32_t)ctx->jobs.size();   // dense index = publication order
+  cudaError_t ce = cudaSetDevice(ctx->cfg.device);
+  if (ce == cudaSuccess)
+    ce = cudaMemcpyAsync(ctx->meta + ctx->off_jobs + sizeof(DevJob) * d, &D, sizeof(DevJob), cudaMemcpyHostToDevice,
+                         ctx->side);
+  if (ce == cudaSuccess) ce = cudaStreamSynchronize(ctx->side);
+  if (ce != cudaSuccess) return cuda_fail(ctx, ce, "upload live job");
+  ctx->ppt_used = ppt;
+  ctx->dump_cur = dump;
+  ctx->max_id = job->job_id;
+  ctx->id_to_submit[job->job_id] = h.submit_idx;
+  ctx->id_to_dense[job->job_id] = d;
+  ctx->dense_to_submit.push_back(h.submit_idx);
+  ctx->djobs.push_back(D);
+  ctx->jobs.push_back(std::move(h));
+  ctx->h2d_bytes += sizeof(DevJob);
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  reinterpret_cast<volatile uint32_t *>(ctx->live)[0] = d + 1;   // publish
+  return SALUS_OK;
+}
+
+int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats) {
+  if (!ctx) return SALUS_E_INVAL;
+  if (!ctx->running) return fail(ctx, SALUS_E_STATE, "salus_run_async first");
+  cudaError_t e = cudaSetDevice(ctx->cfg.device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  uint8_t *m = ctx->meta;
   // host watchdog: poll, then ask the kernel to abort (mapped pinned flag)
-  const auto t0 = std::chrono::steady_clock::now();
+  const auto t0 = ctx->t0;
   bool timed_out = false;
   for (;;) {
     e = cudaEventQuery(ctx->ev1);
     if (e == cudaSuccess) break;
-    if (e != cudaErrorNotReady) return cuda_fail(ctx, e, "kernel");
+    if (e != cudaErrorNotReady) { ctx->running = false; return cuda_fail(ctx, e, "kernel"); }
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     if (!timed_out && ms > ctx->cfg.timeout_ms) {
       *reinterpret_cast<volatile uint32_t *>(ctx->host_abort) = 1;
       timed_out = true;
     }
-    if (timed_out && ms > ctx->cfg.timeout_ms + 20000.0)
+    if (timed_out && ms > ctx->cfg.timeout_ms + 20000.0) {
+      ctx->running = false;
       return fail(ctx, SALUS_E_TIMEOUT, "kernel did not exit after abort");
+    }
     std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
+  ctx->running = false;
   Ctrl ctrl;
   if ((e = cudaMemcpy(&ctrl, m + ctx->off_ctrl, sizeof(Ctrl), cudaMemcpyDeviceToHost)))
     return cuda_fail(ctx, e, "readback");
@@ -568,7 +709,13 @@ const char *salus_last_error(const salus_ctx *ctx) { return ctx ? ctx->err.c_str
 
 int salus_close(salus_ctx *ctx) {
   if (!ctx) return SALUS_OK;
+  if (ctx->running) {                      // never free under a live kernel
+    if (ctx->live && !ctx->ended) salus_end_submissions(ctx);
+    salus_wait(ctx, nullptr, 0, nullptr);
+  }
   if (ctx->host_abort) cudaFreeHost(ctx->host_abort);
+  if (ctx->live) cudaFreeHost(ctx->live);
+  if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);
   delete ctx;

@@ -98,6 +98,8 @@ struct Sched {
   uint64_t append_ns = 0;                          // SALUS_DBG_SCHED builds
   const int64_t *rq = nullptr;                     // request ticks (smem stage or global)
   uint32_t nl = 0, qn = 0, an = 0, next_lane = 0, sumP = 0, sumL = 0, arr_ptr = 0, n_done = 0;
+  uint32_t n_jobs = 0;                       // known jobs: submitted before the run + live ones seen
+  bool live_done = true;                     // no more live jobs can come
   uint32_t free_top = 0, max_lanes = 0, err = 0;
   uint64_t slot_free = ~0ull;
   int64_t next_arrival = IDLE_T;
@@ -243,6 +245,67 @@ struct Sched {
   }
 
   // ------------------------------------------------------------ phases
+  __device__ void init_job(uint32_t j, const DevJob &J) {
+    S.svc[j] = 0; S.c[j] = J.iter_ticks; S.done[j] = 0; S.pending[j] = 0; S.next_req[j] = 0;
+    S.n[j] = J.n_iters; S.p[j] = J.p_pages; S.e[j] = J.e_pages; S.ap[j] = J.ap_pages; S.ae[j] = J.ae_pages;
+    S.id[j] = J.job_id; S.st[j] = ST_NOT_ARRIVED; S.jslot[j] = 0xFF; S.kind[j] = (uint8_t)J.kind;
+    S.nrt[j] = J.kind == SALUS_INFER ? rq[J.req_off] : IDLE_T;
+    S.req_off[j] = J.req_off;
+    salus_job_stat &st = P.stats[j];
+    st.job_id = J.job_id; st.first_lane = NONE32; st.admit_tick = -1; st.first_start_tick = -1;
+    st.completion_tick = -1; st.completion_seq = ~0ull; st.wall_start_ns = 0; st.wall_end_ns = 0;
+    st.wall_arrive_ns = 0;
+  }
+
+  // Online submission (SALUS_FLAG_ONLINE): once every
+  // job known so far has arrived, take the jobs the host has published since
+  // (descriptors already in P.jobs, in publication order = dense order) and
+  // give them arrival tick t + 1 -- strictly after every processed tick, so
+  // replaying the logged arrival ticks through the oracle gives this log.
+  __device__ void poll_live() {
+    if (live_done || arr_ptr < n_jobs) return;
+    uint32_t np = 0, cl = 0;
+    if (tid == 0) {
+      cl = ptx::ld_volatile_u32(P.live + 1);   // closed first: everything published before it is seen
+      __threadfence_system();
+      np = ptx::ld_volatile_u32(P.live);
+    }
+    cl = __shfl_sync(0xffffffffu, cl, 0);
+    np = __shfl_sync(0xffffffffu, np, 0);
+    if (np > P.max_jobs) { fail(SALUS_E_CAPACITY, 7); return; }
+    if (np > n_jobs) {
+      __threadfence_system();                 // their descriptors were uploaded before publication
+      for (uint32_t j = n_jobs + tid; j < np; j += 32) {
+        DevJob *Jw = const_cast<DevJob *>(P.jobs) + j;
+        *(volatile int64_t *)&Jw->arrival = t + 1;
+        DevJob J;
+        const volatile uint32_t *src = reinterpret_cast<const volatile uint32_t *>(Jw);
+        uint32_t *dst = reinterpret_cast<uint32_t *>(&J);
+        for (uint32_t x = 0; x < sizeof(DevJob) / 4; x++) dst[x] = src[x];
+        init_job(j, J);
+      }
+      __syncwarp();
+      n_jobs = np;
+      next_arrival = t + 1;
+    }
+    if (cl && np == n_jobs) live_done = true;
+  }
+
+  // Nothing scheduled and the host may still submit: wait for it.
+  __device__ bool wait_live() {
+    const uint64_t t0 = ptx::globaltimer();
+    while (!live_done && arr_ptr == n_jobs && !err) {
+      poll_live();
+      if (arr_ptr < n_jobs || live_done) break;
+      uint32_t bad = 0;
+      if (tid == 0) bad = host_abort() || *(volatile uint32_t *)&P.ctrl->abort;
+      if (__shfl_sync(0xffffffffu, bad, 0)) { fail(SALUS_E_TIMEOUT, 8); return false; }
+      __nanosleep(2000);
+    }
+    wait_ns += ptx::globaltimer() - t0;
+    return !err;
+  }
+
   __device__ void init() {
     const uint32_t N = P.n_jobs;
     if (P.n_req <= REQ_STAGE) {
@@ -250,17 +313,9 @@ struct Sched {
       __syncwarp();
       rq = S.req_stage;
     }
-    for (uint32_t j = tid; j < N; j += 32) {
-      const DevJob &J = P.jobs[j];
-      S.svc[j] = 0; S.c[j] = J.iter_ticks; S.done[j] = 0; S.pending[j] = 0; S.next_req[j] = 0;
-      S.n[j] = J.n_iters; S.p[j] = J.p_pages; S.e[j] = J.e_pages; S.ap[j] = J.ap_pages; S.ae[j] = J.ae_pages;
-      S.id[j] = J.job_id; S.st[j] = ST_NOT_ARRIVED; S.jslot[j] = 0xFF; S.kind[j] = (uint8_t)J.kind;
-      S.nrt[j] = J.kind == SALUS_INFER ? rq[J.req_off] : IDLE_T;
-      S.req_off[j] = J.req_off;
-      salus_job_stat &st = P.stats[j];
-      st.job_id = J.job_id; st.first_lane = NONE32; st.admit_tick = -1; st.first_start_tick = -1;
-      st.completion_tick = -1; st.completion_seq = ~0ull; st.wall_start_ns = 0; st.wall_end_ns = 0;
-    }
+    for (uint32_t j = tid; j < N; j += 32) init_job(j, P.jobs[j]);
+    n_jobs = N;
+    live_done = P.live == nullptr;
     for (uint32_t i = tid; i < P.Cp; i += 32) P.free_stack[i] = P.Cp - 1 - i;
     for (uint32_t i = tid; i < MAX_LANES; i += 32) {
       S.sq_tail[i] = 0; S.last_app[i] = 0; S.tail_seq[i] = 0; S.q_head_seen[i] = 0;
@@ -395,15 +450,15 @@ struct Sched {
 
   // P2: JobArrive and inference request arrivals (A27, A28)
   __device__ void phase_arrivals() {
-    while (arr_ptr < P.n_jobs && next_arrival == t) {
+    while (arr_ptr < n_jobs && next_arrival == t) {
       const uint32_t j = arr_ptr;
-      if (tid == 0) S.st[j] = ST_QUEUED;
+      if (tid == 0) { S.st[j] = ST_QUEUED; P.stats[j].wall_arrive_ns = ptx::globaltimer(); }
       __syncwarp();
       q_insert(j);
       emit(SALUS_REC_JOB_QUEUED, NONE32, S.id[j], 0, 0);
       dirty = true;
       arr_ptr++;
-      next_arrival = arr_ptr < P.n_jobs ? P.jobs[arr_ptr].arrival : IDLE_T;
+      next_arrival = arr_ptr < n_jobs ? P.jobs[arr_ptr].arrival : IDLE_T;
     }
     for (uint32_t k0 = 0; k0 < P.n_infer; k0 += 32) {
       const uint32_t k = k0 + tid;
@@ -686,10 +741,16 @@ struct Sched {
 #else
 #define SALUS_PH(i, stmt) stmt;
 #endif
-    while (n_done < P.n_jobs && !err) {
+    while (!err) {
+      if (!live_done && (n_ticks & 15) == 0) poll_live();
+      if (n_done == n_jobs && live_done) break;
       int64_t tn;
       SALUS_PH(0, tn = next_event())
-      if (tn == IDLE_T) { fail(SALUS_E_STUCK, 4); break; }
+      if (tn == IDLE_T) {
+        if (!live_done) { if (!wait_live()) break; continue; }
+        fail(SALUS_E_STUCK, 4);
+        break;
+      }
       t = tn;
       n_ticks++;
       dirty = false;

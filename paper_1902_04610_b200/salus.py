@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("SALUS_LIB", os.path.join(HERE, "libsalus.so"))
 
 FIFO, SRTF, PACK, FAIR = 0, 1, 2, 3
 TRAIN, INFER = 0, 1
-FLAG_LOG, FLAG_NULL_WORK, FLAG_CHECK, FLAG_TRACE = 1, 2, 4, 8
+FLAG_LOG, FLAG_NULL_WORK, FLAG_CHECK, FLAG_TRACE, FLAG_ONLINE = 1, 2, 4, 8, 16
 DUMP_OUTPUTS, DUMP_WEIGHTS = 1, 2
 WEIGHTS = 0xFFFFFFFF
 
@@ -53,7 +53,8 @@ class JobDesc(C.Structure):
 class JobStat(C.Structure):
     _fields_ = [("job_id", C.c_uint32), ("first_lane", C.c_uint32), ("admit_tick", C.c_int64),
                 ("first_start_tick", C.c_int64), ("completion_tick", C.c_int64),
-                ("completion_seq", C.c_uint64), ("wall_start_ns", C.c_uint64), ("wall_end_ns", C.c_uint64)]
+                ("completion_seq", C.c_uint64), ("wall_start_ns", C.c_uint64), ("wall_end_ns", C.c_uint64),
+                ("wall_arrive_ns", C.c_uint64)]
 
 
 class RunStats(C.Structure):
@@ -73,7 +74,8 @@ LOG_DTYPE = np.dtype([("tick", "<i8"), ("kind", "<u4"), ("lane", "<u4"), ("job",
 
 EXPORTS = ["salus_open", "salus_job_footprint", "salus_submit_job", "salus_meta_bytes",
            "salus_prepare", "salus_run", "salus_read_run_stats", "salus_read_log",
-           "salus_read_wall", "salus_read_trace", "salus_read_layers", "salus_last_error", "salus_close"]
+           "salus_read_wall", "salus_read_trace", "salus_read_layers", "salus_last_error", "salus_close",
+           "salus_run_async", "salus_submit_live", "salus_end_submissions", "salus_wait"]
 
 _lib = None
 
@@ -102,6 +104,10 @@ def lib():
         L.salus_last_error.argtypes = [P]
         L.salus_last_error.restype = C.c_char_p
         L.salus_close.argtypes = [P]
+        L.salus_run_async.argtypes = [P]
+        L.salus_submit_live.argtypes = [P, C.POINTER(JobDesc)]
+        L.salus_end_submissions.argtypes = [P]
+        L.salus_wait.argtypes = [P, C.POINTER(JobStat), C.c_uint64, C.POINTER(C.c_uint64)]
         for name in EXPORTS:
             if name != "salus_last_error":
                 getattr(L, name).restype = C.c_int
@@ -149,7 +155,7 @@ class Context:
                  max_lanes: int = 0, switch_ticks: int = 0, log: bool = True, null_work: bool = False,
                  check: bool = False, dump: Optional[Dict[int, int]] = None, n_workers: int = 0,
                  timeout_ms: int = 0, page_bytes: int = 65536, trace: bool = False,
-                 trace_capacity: int = 0):
+                 trace_capacity: int = 0, online: bool = False, max_jobs: int = 0, dump_bytes: int = 0):
         import torch
         self._torch = torch
         self.L = lib()
@@ -168,13 +174,15 @@ class Context:
         cfg.capacity_bytes = capacity_bytes
         cfg.page_bytes = page_bytes
         cfg.max_lanes = max_lanes
-        cfg.max_jobs = max(1, len(self.jobs))
+        cfg.max_jobs = max(1, len(self.jobs), max_jobs)
         cfg.flags = ((FLAG_LOG if log else 0) | (FLAG_NULL_WORK if null_work else 0) |
-                     (FLAG_CHECK if check else 0) | (FLAG_TRACE if trace else 0))
+                     (FLAG_CHECK if check else 0) | (FLAG_TRACE if trace else 0) |
+                     (FLAG_ONLINE if online else 0))
         cfg.switch_ticks = switch_ticks
         cfg.n_workers = n_workers
         cfg.timeout_ms = timeout_ms
         cfg.trace_capacity = trace_capacity
+        cfg.dump_bytes = dump_bytes          # 0: exactly what the submitted jobs dump
         self.flags = cfg.flags
         self.ctx = C.c_void_p()
         self._check(self.L.salus_open(C.byref(cfg), C.byref(self.ctx)), "open")
@@ -192,16 +200,37 @@ class Context:
             msg = self.L.salus_last_error(self.ctx) if getattr(self, "ctx", None) else b""
             raise SalusError(rc, f"{what}: {(msg or b'').decode()}")
 
-    def run(self) -> Dict[int, dict]:
-        """One salus_run; returns {job_id: stat dict}."""
-        n = len(self.jobs)
+    def _stats(self, fn, what) -> Dict[int, dict]:
+        n = max(1, len(self.jobs))
         arr = (JobStat * n)()
         cnt = C.c_uint64()
-        self._check(self.L.salus_run(self.ctx, arr, n, C.byref(cnt)), "run")
+        self._check(fn(self.ctx, arr, n, C.byref(cnt)), what)
         out = {}
         for s in arr[:cnt.value]:
             out[s.job_id] = {k: getattr(s, k) for k, _ in JobStat._fields_}
         return out
+
+    def run(self) -> Dict[int, dict]:
+        """One salus_run; returns {job_id: stat dict}."""
+        return self._stats(self.L.salus_run, "run")
+
+    # ---- online submission (online=True; SURVEY §8(f) NEXT-2)
+    def run_async(self):
+        """Launch the persistent kernel and return while it runs."""
+        self._check(self.L.salus_run_async(self.ctx), "run_async")
+
+    def submit_live(self, job, dump: int = 0):
+        """Hand a TRAIN job to the running kernel (arrival stamped on device)."""
+        d, keep = job_desc(job, dump)
+        self._check(self.L.salus_submit_live(self.ctx, C.byref(d)), f"submit_live {job.job_id}")
+        self.jobs.append(job)
+
+    def end_submissions(self):
+        self._check(self.L.salus_end_submissions(self.ctx), "end_submissions")
+
+    def wait(self) -> Dict[int, dict]:
+        """Wait for the run to finish; returns {job_id: stat dict}."""
+        return self._stats(self.L.salus_wait, "wait")
 
     def run_stats(self) -> dict:
         rs = RunStats()

@@ -1,0 +1,139 @@
+"""Online submission (the paper's "a session is created
+when a job is submitted"): jobs handed to the RUNNING
+persistent kernel with salus_submit_live.  The device stamps each live job's
+arrival tick (logged as JOB_QUEUED); parity = replaying those logged ticks
+through the oracle reproduces the whole canonical log byte for byte, and
+the math of a live job still matches the oracle."""
+import dataclasses
+import time
+
+import numpy as np
+import pytest
+
+from oracle import layers as OL
+from oracle import scheduler as OS
+from workloads import TRAIN, make_job
+
+from gpu_helpers import first_diff, normwise_rel
+
+pytestmark = pytest.mark.gpu
+
+JOB_QUEUED = 7
+
+
+def _queued_ticks(log_bytes, S):
+    recs = np.frombuffer(log_bytes, dtype=S.LOG_DTYPE)
+    m = recs["kind"] == JOB_QUEUED
+    return {int(j): int(t) for j, t in zip(recs["job"][m], recs["tick"][m])}
+
+
+def _small(job_id, seed, n_iters=6):
+    rng = np.random.default_rng(seed)
+    w = int(rng.choice([128, 256, 384]))
+    depth = int(rng.integers(1, 4))
+    batch = int(rng.choice([64, 128, 200]))
+    return make_job(job_id, TRAIN, 0, (w,) * (depth + 1), batch, n_iters, lr=1e-2, seed=seed)
+
+
+def _run_online(policy, pre, live, cap, delays_s, null_work, max_lanes=0):
+    from paper_1902_04610_b200 import salus as S
+    ctx = S.Context(pre, cap, policy, online=True, max_jobs=len(pre) + len(live), null_work=null_work,
+                    max_lanes=max_lanes)
+    ctx.run_async()
+    for j, dt in zip(live, delays_s):
+        time.sleep(dt)
+        ctx.submit_live(j)
+    ctx.end_submissions()
+    stats = ctx.wait()
+    return ctx, stats
+
+
+def _check_replay(ctx, jobs, cap, policy, stats, max_lanes=0):
+    from paper_1902_04610_b200 import salus as S
+    got = ctx.log_bytes()
+    arr = _queued_ticks(got, S)
+    assert sorted(arr) == sorted(j.job_id for j in jobs)
+    replay = [dataclasses.replace(j, arrival_tick=arr[j.job_id]) for j in jobs]
+    ref = OS.simulate(replay, cap, policy, max_lanes=max_lanes)
+    want = ref.log_bytes()
+    assert got == want, first_diff(got, want)
+    for jid, s in ref.stats.items():
+        assert stats[jid]["completion_tick"] == s.completion_tick
+        assert stats[jid]["completion_seq"] == s.completion_seq
+    return arr
+
+
+@pytest.mark.parametrize("policy", [OS.PACK, OS.SRTF, OS.FAIR])
+def test_live_jobs_replay_to_the_oracle_log(policy):
+    pre = [_small(i, 100 + i) for i in range(3)]
+    live = [_small(10 + i, 200 + i) for i in range(12)]
+    delays = [0.0005 * (i % 4) for i in range(12)]
+    cap = 1 << 30
+    ctx, stats = _run_online(policy, pre, live, cap, delays, null_work=False)
+    try:
+        arr = _check_replay(ctx, pre + live, cap, policy, stats)
+        # live arrivals are stamped after every pre-submitted arrival, in order
+        ticks = [arr[j.job_id] for j in live]
+        assert ticks == sorted(ticks) and min(ticks) >= 1
+        assert all(stats[j.job_id]["completion_tick"] > 0 for j in pre + live)
+    finally:
+        ctx.close()
+
+
+def test_idle_kernel_waits_for_live_jobs_and_their_math_matches():
+    """No job at launch: the kernel idles until the host submits, then runs
+    them; a live job's outputs and weight updates match the oracle."""
+    from paper_1902_04610_b200 import salus as S
+    live = [_small(1 + i, 300 + i, n_iters=4) for i in range(6)]
+    cap = 1 << 30
+    ctx = S.Context([], cap, S.PACK, online=True, max_jobs=len(live), dump_bytes=64 << 20)
+    try:
+        ctx.run_async()
+        time.sleep(0.05)                       # the kernel is up and idle
+        for j in live:
+            ctx.submit_live(j, dump=S.DUMP_OUTPUTS | S.DUMP_WEIGHTS)
+            time.sleep(0.002)
+        ctx.end_submissions()
+        stats = ctx.wait()
+        _check_replay(ctx, live, cap, OS.PACK, stats)
+        wall = ctx.wall()
+        assert len(wall) == sum(j.n_iters for j in live)
+        assert np.all(wall["end_ns"] > wall["start_ns"])
+        for j in live[-2:]:
+            outs64, _ = OL.run_job(j)
+            _, W = OL.run_job(j, store=OL.bf16)   # A31/A32: weight updates vs the bf16-storage oracle
+            g = ctx.layers(j.job_id, j.n_iters - 1).reshape(j.batch, j.dims[-1])
+            assert normwise_rel(g, outs64[j.n_iters - 1]) <= 2e-2
+            flat = ctx.layers(j.job_id, S.WEIGHTS)
+            W0 = OL.init_weights(j)
+            Wg = flat[:j.dims[0] * j.dims[1]].reshape(j.dims[0], j.dims[1])
+            dg, dr = Wg - W0[0], W[0] - W0[0]
+            assert np.linalg.norm(dg - dr) / np.linalg.norm(dr) <= 2e-2
+    finally:
+        ctx.close()
+
+
+def test_live_submission_errors():
+    from paper_1902_04610_b200 import salus as S
+    cap = 1 << 30
+    plain = S.Context([_small(1, 1)], cap, S.PACK)
+    try:
+        with pytest.raises(S.SalusError):
+            plain.submit_live(_small(2, 2))          # not an online context
+    finally:
+        plain.close()
+    ctx = S.Context([_small(5, 5)], cap, S.PACK, online=True, max_jobs=4, null_work=True)
+    try:
+        with pytest.raises(S.SalusError):
+            ctx.submit_live(_small(6, 6))            # not running yet
+        ctx.run_async()
+        with pytest.raises(S.SalusError):
+            ctx.submit_live(_small(4, 4))            # ids must increase
+        ctx.submit_live(_small(7, 7))
+        ctx.end_submissions()
+        with pytest.raises(S.SalusError):
+            ctx.submit_live(_small(8, 8))            # submissions ended
+        stats = ctx.wait()
+        assert sorted(stats) == [5, 7]
+    finally:
+        ctx.close()
