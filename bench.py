@@ -158,6 +158,26 @@ def switch_latency(S, device):
             "same_job_gap_us": pct(gap)}
 
 
+def jct_physical(S, device, jobs, cap):
+    """The sweep executed (not simulated) under PACK and under FIFO (the
+    baseline): average JCT and makespan from the device stamps (every job
+    arrives at tick 0, so a job's JCT = its last tile end - kernel start)."""
+    out = {}
+    for name, pol in (("pack", S.PACK), ("fifo", S.FIFO)):
+        ctx = S.Context(jobs, cap, pol, device=device, log=False)
+        try:
+            st = ctx.run()
+            rs = ctx.run_stats()
+        finally:
+            ctx.close()
+        t0 = rs["wall_first_ns"]
+        jct = [(v["wall_end_ns"] - t0) / 1e6 for v in st.values()]
+        out[name] = {"avg_jct_ms": float(np.mean(jct)), "makespan_ms": float(max(jct))}
+    out["fifo_over_pack_avg_jct"] = out["fifo"]["avg_jct_ms"] / out["pack"]["avg_jct_ms"]
+    out["fifo_over_pack_makespan"] = out["fifo"]["makespan_ms"] / out["pack"]["makespan_ms"]
+    return out
+
+
 def online_submission(S, device, n_jobs=64, period_s=0.002, n_iters=20):
     """C2a-shaped training jobs (MLP [1024]^4, B=256)
     handed to the RUNNING kernel one every `period_s` (PACK, 1 GiB).  Host
@@ -456,6 +476,10 @@ def main():
             line["c3_switch"] = switch_latency(S, local)
         except Exception as exc:  # noqa: BLE001
             line["c3_switch"] = {"error": str(exc)[:200]}
+        try:
+            line["jct_physical"] = jct_physical(S, local, jobs, cap)
+        except Exception as exc:  # noqa: BLE001
+            line["jct_physical"] = {"error": str(exc)[:200]}
         try:
             line["online_submission"] = online_submission(S, local)
         except Exception as exc:  # noqa: BLE001
