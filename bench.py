@@ -158,6 +158,30 @@ def switch_latency(S, device):
             "same_job_gap_us": pct(gap)}
 
 
+def c1_config(S, device):
+    """BASELINE configs[0] (C1: 2 jobs, FIFO vs SRTF): the device schedule's
+    average JCT in logical ticks (bit-identical to the oracle's) and the
+    physical per-iteration time and job-switch gap on the lane."""
+    from workloads import c1_trace
+    jobs, cap = c1_trace()
+    arr = {j.job_id: j.arrival_tick for j in jobs}
+    out = {}
+    for name, pol in (("fifo", S.FIFO), ("srtf", S.SRTF)):
+        ctx = S.Context(jobs, cap, pol, device=device, log=True)
+        try:
+            st = ctx.run()
+            w = ctx.wall()
+        finally:
+            ctx.close()
+        w = w[np.argsort(w["seq"])]
+        sw = [(int(b["start_ns"]) - int(a["end_ns"])) / 1e3 for a, b in zip(w[:-1], w[1:]) if a["job"] != b["job"]]
+        out[name] = {"avg_jct_ticks": float(np.mean([v["completion_tick"] - arr[k] for k, v in st.items()])),
+                     "iter_us_p50": float(np.median((w["end_ns"] - w["start_ns"]) / 1e3)),
+                     "switch_gap_us": sw}
+    out["fifo_over_srtf_avg_jct"] = out["fifo"]["avg_jct_ticks"] / out["srtf"]["avg_jct_ticks"]
+    return out
+
+
 def jct_physical(S, device, jobs, cap):
     """The sweep executed (not simulated) under PACK and under FIFO (the
     baseline): average JCT and makespan from the device stamps (every job
@@ -476,6 +500,10 @@ def main():
             line["c3_switch"] = switch_latency(S, local)
         except Exception as exc:  # noqa: BLE001
             line["c3_switch"] = {"error": str(exc)[:200]}
+        try:
+            line["c1"] = c1_config(S, local)
+        except Exception as exc:  # noqa: BLE001
+            line["c1"] = {"error": str(exc)[:200]}
         try:
             line["jct_physical"] = jct_physical(S, local, jobs, cap)
         except Exception as exc:  # noqa: BLE001
