@@ -67,9 +67,21 @@ enum {
   SALUS_FLAG_NULL_WORK = 2,  /* schedule only: no iteration work is executed     */
   SALUS_FLAG_CHECK = 4,      /* device asserts the safety invariants every tick  */
   SALUS_FLAG_TRACE = 8,      /* record one salus_trace_rec per executed tile     */
-  SALUS_FLAG_ONLINE = 16     /* online submission: the run
+  SALUS_FLAG_ONLINE = 16,    /* online submission: the run
                                 also admits jobs submitted with salus_submit_live
                                 while it is live, until salus_end_submissions    */
+  SALUS_FLAG_EVICT = 32      /* SRTF admission with persistent eviction (SURVEY
+                                §8(f) NEXT-3, reading A35; "the
+                                higher priority job is admitted as long as its own
+                                safety condition is met ... regardless of other
+                                already-running jobs"): when FindLane fails for a
+                                queued job, idle admitted jobs of strictly lower
+                                SRTF priority are swapped out (lowest first, all or
+                                nothing) -- their persistent pages copied by the
+                                kernel to the caller's pinned host buffer
+                                (salus_set_swap) and freed -- and restored (copied
+                                back into fresh pages) when re-admitted.  SRTF only,
+                                not with SALUS_FLAG_ONLINE (else E_INVAL at open). */
 };
 
 /* salus_job.dump */
@@ -103,7 +115,13 @@ enum {
   SALUS_REC_LANE_CLOSE = 6,  /* JobFinish, ref(lane) == 0             */
   SALUS_REC_JOB_QUEUED = 7,  /* JobArrive: Q <- Q u {(P,E)}           */
   SALUS_REC_JOB_ADMIT = 8,   /* ProcessRequests assigns a lane; a = p, b = e pages */
-  SALUS_REC_JOB_FINISH = 9   /* last iteration ended; a = n, b = completion_seq    */
+  SALUS_REC_JOB_FINISH = 9,  /* last iteration ended; a = n, b = completion_seq    */
+  SALUS_REC_JOB_EVICT = 10,  /* SALUS_FLAG_EVICT: swapped out of its lane (A35);
+                                lane = the lane it left, a = p pages,
+                                b = iterations done so far                       */
+  SALUS_REC_JOB_RESTORE = 11 /* SALUS_FLAG_EVICT: a swapped-out job re-admitted;
+                                a = p, b = e pages (its first admission is
+                                JOB_ADMIT)                                       */
 };
 
 /* Physical timing of one dispatched iteration (not part of the compared log):
@@ -193,6 +211,20 @@ int salus_submit_job(salus_ctx *ctx, const salus_job *job);
  * dump area.  Valid after the last submit. */
 int salus_meta_bytes(const salus_ctx *ctx, uint64_t *bytes);
 
+/* SALUS_FLAG_EVICT: bytes of pinned host memory
+ * the swap area needs -- one fixed region per job, the size of its
+ * persistent device backing (salus_job_footprint), 0 without the flag.
+ * Valid after the last submit. */
+int salus_swap_bytes(const salus_ctx *ctx, uint64_t *bytes);
+
+/* Bind the caller-owned swap area: page-locked host memory (cudaHostAlloc /
+ * torch pin_memory; with unified addressing the kernel reads and writes it
+ * directly), >= salus_swap_bytes, 256-byte aligned, outliving the context.
+ * Before salus_prepare.  Errors: E_STATE (after prepare, or no EVICT flag),
+ * E_INVAL (alignment / not device-accessible), E_CAPACITY (too small).
+ * salus_prepare fails with E_STATE if EVICT needs a swap area and none was set. */
+int salus_set_swap(salus_ctx *ctx, void *host, uint64_t bytes);
+
 /* Bind the caller-owned device buffer `meta` (>= salus_meta_bytes, 256-byte
  * aligned) and upload the job tables on cfg.stream (host->device copies).
  * After this no more jobs can be submitted. Errors: E_STATE, E_CAPACITY, E_CUDA. */
@@ -257,6 +289,10 @@ typedef struct {
   uint64_t d2h_bytes;         /* device->host bytes read back by salus_run        */
   uint64_t sched_fence_ns;    /* part of sched_wait_ns: page-reuse fences (A30)    */
   uint64_t sched_ring_ns;     /* part of sched_wait_ns: a lane's dispatch ring full */
+  uint64_t n_swap_out, n_swap_in;   /* SALUS_FLAG_EVICT: swap records executed     */
+  uint64_t swap_bytes;        /* bytes copied by them (device <-> pinned host)     */
+  uint64_t swap_ns;           /* sum of their durations (first tile start -> last
+                                 tile end, globaltimer)                           */
 } salus_run_stats;
 
 int salus_read_run_stats(const salus_ctx *ctx, salus_run_stats *out);

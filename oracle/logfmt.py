@@ -25,12 +25,15 @@ LANE_CLOSE = 6    # lane, job (the finishing job)
 JOB_QUEUED = 7    # lane = NONE, job
 JOB_ADMIT = 8     # lane, job, a = p pages, b = e pages
 JOB_FINISH = 9    # lane, job, a = n iterations, b = completion_seq
+JOB_EVICT = 10    # lane (left), job (the victim), a = p pages, b = iterations done (A35)
+JOB_RESTORE = 11  # lane, job, a = p pages, b = e pages: a swapped job re-admitted (A35)
 
 NONE32 = 0xFFFFFFFF
 
 NAMES = {DISPATCH: "DISPATCH", LANE_OPEN: "LANE_OPEN", LANE_REUSE: "LANE_REUSE",
          LANE_RESIZE: "LANE_RESIZE", LANE_SHRINK: "LANE_SHRINK", LANE_CLOSE: "LANE_CLOSE",
-         JOB_QUEUED: "JOB_QUEUED", JOB_ADMIT: "JOB_ADMIT", JOB_FINISH: "JOB_FINISH"}
+         JOB_QUEUED: "JOB_QUEUED", JOB_ADMIT: "JOB_ADMIT", JOB_FINISH: "JOB_FINISH",
+         JOB_EVICT: "JOB_EVICT", JOB_RESTORE: "JOB_RESTORE"}
 
 DTYPE = np.dtype([("tick", "<i8"), ("kind", "<u4"), ("lane", "<u4"), ("job", "<u4"),
                   ("a", "<u4"), ("b", "<u8")])

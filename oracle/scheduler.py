@@ -32,7 +32,7 @@ POLICY_NAMES = {FIFO: "fifo", SRTF: "srtf", PACK: "pack", FAIR: "fair"}
 DEFAULT_MAX_LANES = {FIFO: 1, SRTF: 1, PACK: 64, FAIR: 1}
 MAX_LANES = 64
 
-NOT_ARRIVED, QUEUED, ADMITTED, DONE = 0, 1, 2, 3
+NOT_ARRIVED, QUEUED, ADMITTED, DONE, SWAPPED = 0, 1, 2, 3, 4
 TRAIN, INFER = 0, 1
 
 
@@ -128,17 +128,18 @@ class SimResult:
         return LG.encode(self.log)
 
 
-def _admission_key(policy, job, c):
-    # A10: SRTF orders the pending queue by remaining time n*c (the job has
-    # not run yet); A13/A14: the others by arrival.  Ties: (arrival, id).
+def _admission_key(policy, job, c, done=0):
+    # A10: SRTF orders the pending queue by remaining time (n - done)*c (n*c
+    # for a job that has not run yet; A35: a swapped-out job keeps its
+    # progress); A13/A14: the others by arrival.  Ties: (arrival, id).
     if policy == SRTF:
-        return (job.n_iters * c, job.arrival_tick, job.job_id)
+        return ((job.n_iters - done) * c, job.arrival_tick, job.job_id)
     return (job.arrival_tick, job.job_id)
 
 
 def simulate(jobs, capacity_bytes: int, policy: int, *, page_bytes: int = 65536,
              max_lanes: int = 0, switch_ticks: int = 0, literal: bool = False,
-             check_invariants: bool = False) -> SimResult:
+             check_invariants: bool = False, evict: bool = False) -> SimResult:
     """Run the whole trace.  Tick phases (A15):
 
       t  = min(busy_until of busy lanes, next arrival, next pending request)
@@ -152,7 +153,22 @@ def simulate(jobs, capacity_bytes: int, policy: int, *, page_bytes: int = 65536,
     The default runs it only on ticks where a job arrived or finished: the
     only events that change what FindLane can return (one pass is a fixpoint,
     A8); tests check the two modes produce identical logs.
+
+    `evict=True` (SRTF only, reading A35 of DESIGN.md):
+    "the higher priority job is admitted as long as its own safety condition
+    is met -- i.e., at least, it can run alone on the GPU -- regardless of
+    other already-running jobs".  When FindLane fails for a queued
+    job j, admitted jobs of strictly lower priority (larger
+    ((n-done)*c, arrival, id)) that are not mid-iteration are swapped out,
+    lowest priority first, until FindLane succeeds; if it cannot succeed,
+    nobody is evicted.  A victim leaves its lane (JobFinish's lane update,
+    A4), its P pages are freed, and it joins Q after the pass (SWAPPED) with
+    its progress kept; re-admission logs JOB_RESTORE.  Admission runs at
+    every tick with a non-empty Q (an iteration end makes its job
+    evictable).  Swap time is not modelled in logical ticks (like A16).
     """
+    if evict and policy != SRTF:
+        raise ValueError("evict applies to SRTF only")
     G = int(page_bytes)
     Cp = int(capacity_bytes) // G
     if max_lanes <= 0:
@@ -183,6 +199,7 @@ def simulate(jobs, capacity_bytes: int, policy: int, *, page_bytes: int = 65536,
     pending = {jid: 0 for jid in J}
     next_req = {jid: 0 for jid in J}
     lane_of: Dict[int, int] = {}
+    first_lane: Dict[int, int] = {}
     first_start: Dict[int, int] = {}
     admit_tick: Dict[int, int] = {}
     last_seq: Dict[int, int] = {}
@@ -217,15 +234,64 @@ def simulate(jobs, capacity_bytes: int, policy: int, *, page_bytes: int = 65536,
         assert ids == sorted(ids) and len(set(ids)) == len(ids)
         assert sumP == sum(p[r] for ln in lanes for r in ln.residents)
 
+    def prio(jid):
+        return _admission_key(policy, J[jid], c[jid], done[jid])
+
+    def lane_left(t, ln, jid):
+        """`jid` left lane `ln` (JobFinish or eviction): delete the lane if
+        ref(lane) == 0, else L = max E of the residents (A4)."""
+        if not ln.residents:
+            lanes.remove(ln)
+            del lane_by_id[ln.id]
+            log.append((t, LG.LANE_CLOSE, ln.id, jid, 0, 0))
+        else:
+            newL = max(e[r] for r in ln.residents)
+            if newL < ln.L:
+                log.append((t, LG.LANE_SHRINK, ln.id, jid, newL, ln.L))
+                ln.L = newL
+
+    def evict_for(t, jid, evicted):
+        """A35: swap out lower-priority idle residents, lowest priority
+        first, until FindLane(p_j, e_j) succeeds; all or nothing."""
+        nonlocal sumP
+        kj = prio(jid)
+        cands = [v for ln in lanes for v in ln.residents
+                 if prio(v) > kj and not (ln.busy_until is not None and ln.cur == v)]
+        cands.sort(key=prio, reverse=True)
+        hres = {ln.id: list(ln.residents) for ln in lanes}
+        hP = sumP
+        chosen = []
+        for v in cands:
+            chosen.append(v)
+            hP -= p[v]
+            hres[lane_of[v]].remove(v)
+            hl = [(ln.id, max(e[r] for r in hres[ln.id])) for ln in lanes if hres[ln.id]]
+            if find_lane(hP, hl, p[jid], e[jid], Cp, max_lanes) is not None:
+                break
+        else:
+            return None
+        for v in chosen:
+            ln = lane_by_id[lane_of[v]]
+            st[v] = SWAPPED
+            sumP -= p[v]
+            ln.residents.remove(v)
+            log.append((t, LG.JOB_EVICT, ln.id, v, p[v], done[v]))
+            lane_left(t, ln, v)
+            evicted.append(v)
+        return find_lane(sumP, [(ln.id, ln.L) for ln in lanes], p[jid], e[jid], Cp, max_lanes)
+
     def admission_pass(t, dry=False):
         nonlocal sumP, next_lane
         admitted = 0
-        order = sorted(Q, key=lambda jid: _admission_key(policy, J[jid], c[jid]))
+        order = sorted(Q, key=prio)
         busy_job = any(st[x] == ADMITTED for x in J) if policy == FIFO else False
+        evicted: List[int] = []
         for jid in order:
             if policy == FIFO and busy_job:          # A14: exclusive GPU, strict HOL
                 break
             d = find_lane(sumP, [(ln.id, ln.L) for ln in lanes], p[jid], e[jid], Cp, max_lanes)
+            if d is None and evict and not dry:
+                d = evict_for(t, jid, evicted)
             if d is None:
                 if policy == FIFO:
                     break
@@ -254,13 +320,16 @@ def simulate(jobs, capacity_bytes: int, policy: int, *, page_bytes: int = 65536,
                 svc[jid] = min((svc[r] for r in ln.residents), default=0)
             ln.residents.append(jid)
             sumP += p[jid]
+            restored = st[jid] == SWAPPED
             st[jid] = ADMITTED
-            admit_tick[jid] = t
+            admit_tick.setdefault(jid, t)
+            first_lane.setdefault(jid, ln.id)
             lane_of[jid] = ln.id
-            log.append((t, LG.JOB_ADMIT, ln.id, jid, p[jid], e[jid]))
+            log.append((t, LG.JOB_RESTORE if restored else LG.JOB_ADMIT, ln.id, jid, p[jid], e[jid]))
             Q.remove(jid)
             admitted += 1
             busy_job = True
+        Q.extend(evicted)                             # A35: victims queue after the pass
         return admitted
 
     while n_done < len(J):
@@ -269,7 +338,7 @@ def simulate(jobs, capacity_bytes: int, policy: int, *, page_bytes: int = 65536,
         if arr_ptr < len(by_arrival):
             cand.append(by_arrival[arr_ptr].arrival_tick)
         for jid in infer_ids:
-            if st[jid] in (QUEUED, ADMITTED) and next_req[jid] < J[jid].n_iters:
+            if st[jid] in (QUEUED, ADMITTED, SWAPPED) and next_req[jid] < J[jid].n_iters:
                 cand.append(J[jid].request_ticks[next_req[jid]])
         if not cand:
             raise Stuck(f"no event left with {len(J) - n_done} jobs unfinished")
@@ -291,18 +360,10 @@ def simulate(jobs, capacity_bytes: int, policy: int, *, page_bytes: int = 65536,
                 dirty = True
                 sumP -= p[jid]
                 ln.residents.remove(jid)
-                stats[jid] = JobStat(jid, lane_of[jid], admit_tick[jid], first_start[jid], t,
+                stats[jid] = JobStat(jid, first_lane[jid], admit_tick[jid], first_start[jid], t,
                                      last_seq[jid])
                 log.append((t, LG.JOB_FINISH, ln.id, jid, done[jid], last_seq[jid]))
-                if not ln.residents:                  # ref(lane) == 0: delete lane
-                    lanes.remove(ln)
-                    del lane_by_id[ln.id]
-                    log.append((t, LG.LANE_CLOSE, ln.id, jid, 0, 0))
-                else:                                 # A4: L_j = max E_i of residents
-                    newL = max(e[r] for r in ln.residents)
-                    if newL < ln.L:
-                        log.append((t, LG.LANE_SHRINK, ln.id, jid, newL, ln.L))
-                        ln.L = newL
+                lane_left(t, ln, jid)
         if check_invariants:
             invariants("P1")
 
@@ -315,7 +376,7 @@ def simulate(jobs, capacity_bytes: int, policy: int, *, page_bytes: int = 65536,
             log.append((t, LG.JOB_QUEUED, LG.NONE32, jid, 0, 0))
             dirty = True
         for jid in infer_ids:
-            if st[jid] not in (QUEUED, ADMITTED):
+            if st[jid] not in (QUEUED, ADMITTED, SWAPPED):
                 continue
             rt = J[jid].request_ticks
             k = 0
@@ -337,12 +398,20 @@ def simulate(jobs, capacity_bytes: int, policy: int, *, page_bytes: int = 65536,
                         svc[jid] = max(svc[jid], min(co))
 
         # ---- P3: ProcessRequests ------------------------------
-        if Q and (dirty or literal):
+        if Q and (dirty or literal or evict):
             admission_pass(t)
         if check_invariants:
             invariants("P3")
-            if Q:
+            if Q and not evict:
                 assert admission_pass(t, dry=True) == 0, "I7: second pass admitted a job"
+            if Q and evict:
+                # I8: the highest-priority queued job is admitted
+                # "regardless of other already-running jobs" once every
+                # admitted job has lower priority and none is mid-iteration.
+                top = min(Q, key=prio)
+                adm = [r for ln in lanes for r in ln.residents]
+                busy = any(ln.busy_until is not None for ln in lanes)
+                assert not (all(prio(r) > prio(top) for r in adm) and not busy), ("I8", t, top)
 
         # ---- P4: dispatch at iteration boundaries ----
         for ln in lanes:

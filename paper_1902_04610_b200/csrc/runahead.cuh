@@ -47,8 +47,8 @@ __device__ __forceinline__ bool take_next(Slot &sl, DispRec *rec) {
     const unsigned long long st = ld_acquire_u64q(&sl.qstate);
     if ((uint32_t)(st >> 32) != h) {
       const volatile DispRec *vr = &sl.recs[h % RQ];
-      rec->job = vr->job; rec->iter = vr->iter; rec->seq = vr->seq; rec->lane_id = vr->lane_id; rec->pad = 0;
-      rec->append_ns = vr->append_ns;
+      rec->job = vr->job; rec->iter = vr->iter; rec->seq = vr->seq; rec->lane_id = vr->lane_id; rec->kind = vr->kind;
+      rec->append_ns = vr->append_ns; rec->lseq = vr->lseq;
       st_release_u32(&sl.q_head, h + 1);
       return true;
     }
@@ -56,19 +56,25 @@ __device__ __forceinline__ bool take_next(Slot &sl, DispRec *rec) {
   }
 }
 
-// Single thread: make `rec` the slot's in-flight iteration.  Returns the first
-// stage (INIT before a job's first iteration, else GEN); the caller enqueues
-// that stage's tiles after this returns (the fence orders these writes first).
+// Single thread: make `rec` the slot's in-flight record.  Returns the first
+// stage (INIT before a job's first iteration, else GEN; the copy stage of a
+// swap record); the caller enqueues that stage's tiles after this returns
+// (the fence orders these writes first).
 __device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec) {
   sl.job = rec.job;
   sl.iter = rec.iter;
   sl.seq = rec.seq;
+  sl.lseq = rec.lseq;
+  sl.rkind = rec.kind;
   sl.lane_id = rec.lane_id;
   sl.append_ns = rec.append_ns;
   sl.start_ns = ~0ull;
   sl.end_ns = 0;
   for (uint32_t k = 0; k < MAX_STAGES + 2; k++) sl.stage_done[k] = 0;
+  if (rec.kind != REC_ITER) { sl.stage_done[STAGE_SWAP_OUT] = 0; sl.stage_done[STAGE_SWAP_IN] = 0; }
   __threadfence();
+  if (rec.kind == REC_SWAP_OUT) return STAGE_SWAP_OUT;
+  if (rec.kind == REC_SWAP_IN) return STAGE_SWAP_IN;
   return rec.iter == 0 ? 0u : 1u;
 }
 

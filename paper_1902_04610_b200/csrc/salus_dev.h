@@ -18,7 +18,8 @@ constexpr uint32_t NONE32 = 0xFFFFFFFFu;
 constexpr uint32_t TASK_EXIT = 0xFFFFFFFFu;
 
 // Job states (oracle: NOT_ARRIVED, QUEUED, ADMITTED, DONE)
-enum : uint8_t { ST_NOT_ARRIVED = 0, ST_QUEUED = 1, ST_ADMITTED = 2, ST_DONE = 3 };
+// + SWAPPED (A35, SALUS_FLAG_EVICT): admitted once, persistent pages on the host, in Q
+enum : uint8_t { ST_NOT_ARRIVED = 0, ST_QUEUED = 1, ST_ADMITTED = 2, ST_DONE = 3, ST_SWAPPED = 4 };
 
 // Static per-job descriptor, uploaded by salus_prepare.  The dense index of
 // a job is its rank in (arrival_tick, job_id) order, so every "(arrival, id)"
@@ -58,11 +59,15 @@ struct alignas(128) DevJob {   // whole cache lines: a live job's descriptor nev
 // full ring while another lane runs dry (C3: 1k+ requests per lane)
 constexpr uint32_t RQ = SALUS_RQ;
 
+// Record kinds: an iteration, or (A35) a swap of the job's persistent pages
+enum : uint32_t { REC_ITER = 0, REC_SWAP_OUT = 1, REC_SWAP_IN = 2 };
+
 struct DispRec {
   uint32_t job, iter;                  // dense job index, iteration index
-  uint64_t seq;                        // global dispatch seq
-  uint32_t lane_id, pad;               // logical lane id (for the wall log)
+  uint64_t seq;                        // physical record seq (done_seq, page fences)
+  uint32_t lane_id, kind;              // logical lane id (for the wall log), REC_*
   uint64_t append_ns;                  // globaltimer of the scheduler's append
+  uint64_t lseq;                       // logical dispatch seq (log, wall stamps)
 };
 
 // One physical lane slot.  256-B aligned.
@@ -70,13 +75,15 @@ struct alignas(256) Slot {
   // the in-flight iteration (written by whoever started it)
   uint32_t job;             // dense job index of the in-flight iteration
   uint32_t iter;            // iteration index k
-  uint64_t seq;             // global dispatch seq
+  uint64_t seq;             // physical record seq
+  uint64_t lseq;            // logical dispatch seq (REC_ITER)
+  uint32_t rkind;           // REC_*
   uint64_t start_ns;        // min globaltimer over first-stage tiles (atomicMin)
   uint64_t end_ns;          // globaltimer when the last stage completed
   uint64_t done_seq;        // seq + 1 of the last physically completed iteration (monotonic)
   uint32_t lane_id;
   uint64_t append_ns;       // when the in-flight iteration's record was appended
-  uint32_t stage_done[MAX_STAGES + 2];
+  uint32_t stage_done[32];         // per stage number (5 bits; 30, 31 = swap copies)
   // dispatch ring: qstate = records appended << 32 | running (1 while an
   // iteration is in flight or being started), one word so that append and
   // release race through single atomics
@@ -97,6 +104,7 @@ struct alignas(256) Ctrl {
   uint64_t wall_first_ns, wall_last_ns;
   uint32_t log_overflow, n_workers;
   unsigned long long n_trace;
+  unsigned long long n_swap_out, n_swap_in, swap_bytes, swap_ns;   // A35 swap records
 };
 
 struct Params {
@@ -136,7 +144,19 @@ struct Params {
   uint32_t *live;                  // mapped {n_published, closed} (SALUS_FLAG_ONLINE), else null
   int64_t switch_ticks;
   uint64_t timeout_ns;
+  // SALUS_FLAG_EVICT (A35): pinned host swap area (job j's region at
+  // pt_off * PAGE_BYTES, ap_pages pages), per-job fence of its last swap-out
+  // record (slot << 56 | seq + 1), victims of the current admission pass
+  uint8_t *swap;
+  unsigned long long *swap_fence;
+  uint16_t *evl;
 };
+
+// A35 swap records run as one stage of copy tasks (two 64 KiB pages per pair task)
+constexpr uint32_t STAGE_SWAP_OUT = 30, STAGE_SWAP_IN = 31;
+__host__ __device__ inline uint32_t stage_ntiles(const DevJob &J, uint32_t stage) {
+  return stage >= STAGE_SWAP_OUT ? (J.ap_pages + 1) / 2 : J.stage_tiles[stage];
+}
 
 // task payload: slot (6 bits) | stage (5 bits) | tile (21 bits)
 __host__ __device__ inline uint32_t task_pack(uint32_t slot, uint32_t stage, uint32_t tile) {

@@ -85,7 +85,10 @@ struct salus_ctx {
   uint64_t ring_cap = 0, log_cap = 0;
   uint64_t off_ctrl = 0, off_jobs = 0, off_req = 0, off_inf = 0, off_ppt = 0, off_lpt = 0, off_free = 0,
            off_slots = 0, off_ring = 0, off_fslot = 0, off_fseq = 0, off_pend = 0, off_log = 0, off_wall = 0, off_stats = 0, off_dump = 0, off_trace = 0,
-           total = 0;
+           off_swfence = 0, off_evl = 0, total = 0;
+  // SALUS_FLAG_EVICT (A35): caller-owned pinned host swap area
+  uint8_t *swap_dev = nullptr;
+  uint64_t swap_set_bytes = 0;
   uint64_t trace_cap = 0, n_trace = 0, h2d_bytes = 0;
   uint32_t lpt_stride = 0;
   uint32_t *host_abort = nullptr;
@@ -177,6 +180,9 @@ int salus_open(const salus_config *cfg, salus_ctx **out) {
   if (!c.arena || (reinterpret_cast<uintptr_t>(c.arena) & 255) || c.arena_bytes < Cp * c.page_bytes)
     return SALUS_E_INVAL;
   if (c.timeout_ms == 0) c.timeout_ms = 600000;
+  // A35: eviction is the SRTF admission rule of P:530, for offline traces
+  if ((c.flags & SALUS_FLAG_EVICT) && (c.policy != SALUS_SRTF || (c.flags & SALUS_FLAG_ONLINE)))
+    return SALUS_E_INVAL;
   salus_ctx *ctx = new salus_ctx();
   ctx->cfg = c;
   ctx->Cp = (uint32_t)Cp;
@@ -304,6 +310,7 @@ static void compute_layout(salus_ctx *c) {
     c->id_to_dense[j.job_id] = d;
     fill_devjob(c, h, D, req_total, ppt_total, dump_cur);
     for (uint32_t s = 0; s < D.n_stages; s++) max_tiles = std::max<uint64_t>(max_tiles, D.stage_tiles[s]);
+    if (c->cfg.flags & SALUS_FLAG_EVICT) max_tiles = std::max<uint64_t>(max_tiles, (D.ap_pages + 1) / 2);
     max_ae = std::max<uint64_t>(max_ae, D.ae_pages);
     dispatches += j.n_iters;
   }
@@ -331,7 +338,10 @@ static void compute_layout(salus_ctx *c) {
   c->log_cap = 0;
   if (c->cfg.flags & SALUS_FLAG_LOG)
     c->log_cap = c->cfg.log_capacity ? c->cfg.log_capacity
-                                     : dispatches + 6ull * n + 16 + (online ? (1ull << 20) : 0);
+                                     : dispatches + 6ull * n + 16 + (online ? (1ull << 20) : 0) +
+                                       // A35: an eviction logs <= 4 records and happens at most
+                                       // once per iteration boundary of its victim
+                                       ((c->cfg.flags & SALUS_FLAG_EVICT) ? 4 * dispatches : 0);
   uint64_t o = 0;
   auto take = [&](uint64_t bytes) { uint64_t r = o; o = align_up(o + bytes, 256); return r; };
   c->off_ctrl = take(sizeof(Ctrl));
@@ -354,6 +364,8 @@ static void compute_layout(salus_ctx *c) {
   c->off_dump = take(4 * std::max<uint64_t>(c->dump_cap, 1));
   c->trace_cap = (c->cfg.flags & SALUS_FLAG_TRACE) ? (c->cfg.trace_capacity ? c->cfg.trace_capacity : (1ull << 20)) : 0;
   c->off_trace = take(sizeof(salus_trace_rec) * std::max<uint64_t>(c->trace_cap, 1));
+  c->off_swfence = take(8 * std::max<uint64_t>(n_cap, 1));
+  c->off_evl = take(2 * std::max<uint64_t>(n_cap, 1));
   c->total = o;
 }
 
@@ -361,6 +373,34 @@ int salus_meta_bytes(const salus_ctx *ctx, uint64_t *bytes) {
   if (!ctx || !bytes) return SALUS_E_INVAL;
   compute_layout(const_cast<salus_ctx *>(ctx));
   *bytes = ctx->total;
+  return SALUS_OK;
+}
+
+int salus_swap_bytes(const salus_ctx *ctx, uint64_t *bytes) {
+  if (!ctx || !bytes) return SALUS_E_INVAL;
+  compute_layout(const_cast<salus_ctx *>(ctx));
+  // job j's region: its persistent backing pages, at pt_off pages (dense order)
+  *bytes = (ctx->cfg.flags & SALUS_FLAG_EVICT) ? ctx->ppt_used * ctx->cfg.page_bytes : 0;
+  return SALUS_OK;
+}
+
+int salus_set_swap(salus_ctx *ctx, void *host, uint64_t bytes) {
+  if (!ctx) return SALUS_E_INVAL;
+  if (ctx->state != 0) return fail(ctx, SALUS_E_STATE, "salus_set_swap after salus_prepare");
+  if (!(ctx->cfg.flags & SALUS_FLAG_EVICT)) return fail(ctx, SALUS_E_STATE, "no SALUS_FLAG_EVICT");
+  if (!host || (reinterpret_cast<uintptr_t>(host) & 255)) return fail(ctx, SALUS_E_INVAL, "swap must be 256-B aligned");
+  uint64_t need = 0;
+  salus_swap_bytes(ctx, &need);
+  if (bytes < need) return fail(ctx, SALUS_E_CAPACITY, "swap area too small");
+  cudaError_t e = cudaSetDevice(ctx->cfg.device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  void *dev = nullptr;
+  if ((e = cudaHostGetDevicePointer(&dev, host, 0)) != cudaSuccess) {
+    cudaGetLastError();
+    return fail(ctx, SALUS_E_INVAL, "swap area is not page-locked host memory the device can access");
+  }
+  ctx->swap_dev = static_cast<uint8_t *>(dev);
+  ctx->swap_set_bytes = bytes;
   return SALUS_OK;
 }
 
@@ -372,6 +412,9 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   compute_layout(ctx);
   if (!meta || (reinterpret_cast<uintptr_t>(meta) & 255)) return fail(ctx, SALUS_E_INVAL, "meta must be 256-B aligned");
   if (meta_bytes < ctx->total) return fail(ctx, SALUS_E_CAPACITY, "meta buffer too small");
+  if ((ctx->cfg.flags & SALUS_FLAG_EVICT) && ctx->ppt_used &&
+      (!ctx->swap_dev || ctx->swap_set_bytes < ctx->ppt_used * ctx->cfg.page_bytes))
+    return fail(ctx, SALUS_E_STATE, "SALUS_FLAG_EVICT needs salus_set_swap (>= salus_swap_bytes) first");
   cudaError_t e = cudaSetDevice(ctx->cfg.device);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
   int grid = 0;
@@ -455,6 +498,9 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   P.trace_cap = ctx->trace_cap;
   P.dump = reinterpret_cast<float *>(m + ctx->off_dump);
   P.host_abort = ctx->host_abort_dev;
+  P.swap = ctx->swap_dev;
+  P.swap_fence = reinterpret_cast<unsigned long long *>(m + ctx->off_swfence);
+  P.evl = reinterpret_cast<uint16_t *>(m + ctx->off_evl);
   P.n_jobs = n;
   P.n_infer = (uint32_t)inf.size();
   P.n_req = (uint32_t)req.size();
@@ -616,6 +662,7 @@ int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64
   rs.n_tasks = ctrl.n_tasks; rs.kernel_ns = (uint64_t)((double)ms * 1e6);
   rs.wall_first_ns = ctrl.wall_first_ns; rs.wall_last_ns = ctrl.wall_last_ns;
   rs.sched_wait_ns = ctrl.sched_wait_ns; rs.sched_fence_ns = ctrl.sched_fence_ns; rs.sched_ring_ns = ctrl.sched_ring_ns; rs.status = ctrl.status; rs.n_workers = ctx->grid / 2 - 1;
+  rs.n_swap_out = ctrl.n_swap_out; rs.n_swap_in = ctrl.n_swap_in; rs.swap_bytes = ctrl.swap_bytes; rs.swap_ns = ctrl.swap_ns;
   ctx->n_trace = std::min<uint64_t>(ctrl.n_trace, ctx->trace_cap);
   rs.h2d_bytes = ctx->h2d_bytes;
   rs.d2h_bytes = sizeof(Ctrl) + (stats ? sizeof(salus_job_stat) * ctx->jobs.size() : 0);

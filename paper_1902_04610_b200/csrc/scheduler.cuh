@@ -31,7 +31,9 @@ struct SchedShared {
   // lane table, index order == lane id order
   uint32_t lane_id[MAX_LANES], lane_L[MAX_LANES], lane_slot[MAX_LANES], lane_back[MAX_LANES];
   int64_t lane_busy[MAX_LANES];
-  uint64_t lane_seq[MAX_LANES];
+  uint64_t lane_seq[MAX_LANES];             // logical seq of the in-flight dispatch (log, stats)
+  uint64_t lane_pseq[MAX_LANES];            // its physical record seq (page fences)
+  uint32_t hL[MAX_LANES];                   // A35: lane sizes of a hypothetical eviction state
   uint16_t lane_cur[MAX_LANES], lane_last[MAX_LANES];
   // per job (dense index = (arrival, id) rank)
   int64_t svc[MAX_JOBS];
@@ -78,6 +80,14 @@ __device__ __forceinline__ uint64_t warp_min_u64(uint64_t v) {
   }
   return v;
 }
+__device__ __forceinline__ uint64_t warp_max_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    uint64_t w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
 __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -94,6 +104,10 @@ struct Sched {
   // warp-uniform scalar state
   int64_t t = 0;
   uint64_t seq = 0, n_log = 0, n_ticks = 0, wait_ns = 0;
+  // physical record seq: every record appended to a slot ring (iterations and
+  // A35 swap records) takes the next one; done_seq, page fences and drains
+  // count in it.  Equal to `seq` (logical dispatches) without eviction.
+  uint64_t pseq = 0;
   uint64_t wait_fence_ns = 0, wait_ring_ns = 0;     // parts of wait_ns: page fences, full dispatch ring
   uint64_t append_ns = 0;                          // SALUS_DBG_SCHED builds
   const int64_t *rq = nullptr;                     // request ticks (smem stage or global)
@@ -105,10 +119,12 @@ struct Sched {
   int64_t next_arrival = IDLE_T;
   bool dirty = false;
   bool physical = true;                      // false in SALUS_FLAG_NULL_WORK
+  bool evict_mode = false;                   // SALUS_FLAG_EVICT (A35)
   uint64_t pend_mask = 0;                    // target slots with page-reuse fences
 
   __device__ Sched(const Params &p_, SchedShared &s_)
-      : P(p_), S(s_), tid(threadIdx.x & 31), physical(!(p_.flags & SALUS_FLAG_NULL_WORK)), rq(p_.req_ticks) {}
+      : P(p_), S(s_), tid(threadIdx.x & 31), physical(!(p_.flags & SALUS_FLAG_NULL_WORK)),
+        evict_mode((p_.flags & SALUS_FLAG_EVICT) != 0), rq(p_.req_ticks) {}
 
   __device__ void fail(int32_t code, uint32_t info) {
     if (tid == 0 && err == 0) {
@@ -176,29 +192,42 @@ struct Sched {
   // condition), A2 (best match = smallest L >= E, lowest id), A3 (branch 3
   // only for L_r < E, ascending (L_r, id)), A9 (max_lanes).
   // Returns 0 = none, 1 = new, 2 = reuse, 3 = resize; *li = lane index.
-  __device__ int find_lane(uint32_t p, uint32_t e, uint32_t *li) const {
-    const int64_t S_ = (int64_t)sumP + (int64_t)sumL, Cp = P.Cp;
-    if (nl < max_lanes && S_ + p + e <= Cp) return 1;
+  // Over a lane table Ls[0..n_all) of which n_open exist (NONE32 = a lane
+  // closed in a hypothetical eviction state, A35; it matches no branch).
+  __device__ int find_lane_g(uint32_t p, uint32_t e, const uint32_t *Ls, uint32_t n_all, uint32_t n_open,
+                             int64_t S_, uint32_t *li) const {
+    const int64_t Cp = P.Cp;
+    if (n_open < max_lanes && S_ + p + e <= Cp) return 1;
     if (S_ + p <= Cp) {
       uint32_t bestL = NONE32, bi = NONE32;
-      for (uint32_t i = 0; i < nl; i++) {
-        uint32_t L = S.lane_L[i];
+      for (uint32_t i = 0; i < n_all; i++) {
+        uint32_t L = Ls[i];
         if (L >= e && L < bestL) { bestL = L; bi = i; }
       }
       if (bi != NONE32) { *li = bi; return 2; }
     }
     const int64_t thr = S_ + p + e - Cp;   // S - L + p + e <= C  <=>  L >= thr
     uint32_t bestL = NONE32, bi = NONE32;
-    for (uint32_t i = 0; i < nl; i++) {
-      uint32_t L = S.lane_L[i];
+    for (uint32_t i = 0; i < n_all; i++) {
+      uint32_t L = Ls[i];
       if (L < e && (int64_t)L >= thr && L < bestL) { bestL = L; bi = i; }
     }
     if (bi != NONE32) { *li = bi; return 3; }
     return 0;
   }
+  __device__ int find_lane(uint32_t p, uint32_t e, uint32_t *li) const {
+    return find_lane_g(p, e, S.lane_L, nl, nl, (int64_t)sumP + (int64_t)sumL, li);
+  }
 
   // ------------------------------------------------------------ helpers
   __device__ bool runnable(uint32_t j) const { return S.kind[j] == SALUS_TRAIN || S.pending[j] > 0; }
+
+  // SRTF priority (A10/A11/A35): ((n - done) * c, dense index); smaller first
+  __device__ uint64_t srtf_key(uint32_t j) const {
+    return ((uint64_t)((int64_t)(S.n[j] - S.done[j]) * S.c[j]) << KEY_BITS) | j;
+  }
+  // a job with requests or iterations still to come (arrived, not finished)
+  __device__ static bool live_state(uint8_t st) { return st == ST_QUEUED || st == ST_ADMITTED || st == ST_SWAPPED; }
 
   // min svc over admitted jobs in `slot` (excluding `skip`, optionally only
   // runnable ones); IDLE_T if none
@@ -332,7 +361,7 @@ struct Sched {
     for (uint32_t i = tid; i < nl; i += 32) m = min(m, S.lane_busy[i]);
     for (uint32_t k = tid; k < P.n_infer; k += 32) {
       uint32_t j = S.infer[k];
-      if (S.st[j] == ST_QUEUED || S.st[j] == ST_ADMITTED) m = min(m, S.nrt[j]);
+      if (live_state(S.st[j])) m = min(m, S.nrt[j]);
     }
     m = warp_min_i64(m);
     return min(m, next_arrival);
@@ -343,7 +372,8 @@ struct Sched {
       if (tid == 0) {
         S.lane_id[k] = S.lane_id[k + 1]; S.lane_L[k] = S.lane_L[k + 1]; S.lane_slot[k] = S.lane_slot[k + 1];
         S.lane_back[k] = S.lane_back[k + 1]; S.lane_busy[k] = S.lane_busy[k + 1];
-        S.lane_seq[k] = S.lane_seq[k + 1]; S.lane_cur[k] = S.lane_cur[k + 1]; S.lane_last[k] = S.lane_last[k + 1];
+        S.lane_seq[k] = S.lane_seq[k + 1]; S.lane_pseq[k] = S.lane_pseq[k + 1];
+        S.lane_cur[k] = S.lane_cur[k + 1]; S.lane_last[k] = S.lane_last[k + 1];
       }
     }
     nl--;
@@ -378,49 +408,56 @@ struct Sched {
         remove_adm(j);
         // completion_seq = seq of the final iteration = the lane's in-flight one
         emit(SALUS_REC_JOB_FINISH, S.lane_id[i], S.id[j], S.n[j], S.lane_seq[i]);
-        push_pages(job_table(j), S.ap[j], slot, S.lane_seq[i]);
-        // residents left in this lane: count, max e, max actual e
-        uint32_t cnt = 0, maxe = 0, maxae = 0;
-        for (uint32_t a = tid; a < an; a += 32) {
-          uint32_t r = S.adm[a];
-          if (S.jslot[r] == slot) { cnt++; maxe = max(maxe, S.e[r]); maxae = max(maxae, S.ae[r]); }
-        }
-        cnt = __reduce_add_sync(0xffffffffu, cnt);
-        maxe = warp_max_u32(maxe);
-        maxae = warp_max_u32(maxae);
-        if (cnt == 0) {                           // ref(lane) == 0: delete lane
-          emit(SALUS_REC_LANE_CLOSE, S.lane_id[i], S.id[j], 0, 0);
-          push_pages(lane_table(slot), S.lane_back[i], slot, S.lane_seq[i]);
-          sumL -= S.lane_L[i];
-          if (tid == 0) S.tail_seq[slot] = S.last_app[slot];
-          slot_free |= (1ull << slot);
-          remove_lane(i);
-          continue;
-        }
-        if (maxe < S.lane_L[i]) {                 // A4: L_j = max E_i of residents
-          emit(SALUS_REC_LANE_SHRINK, S.lane_id[i], S.id[j], maxe, S.lane_L[i]);
-          sumL -= S.lane_L[i] - maxe;
-          if (tid == 0) S.lane_L[i] = maxe;
-        }
-        if (maxae < S.lane_back[i]) {
-          push_pages(lane_table(slot) + maxae, S.lane_back[i] - maxae, slot, S.lane_seq[i]);
-          if (tid == 0) { S.lane_back[i] = maxae; S.tail_seq[slot] = S.last_app[slot]; }
-        }
-        __syncwarp();
+        push_pages(job_table(j), S.ap[j], slot, S.lane_pseq[i]);
+        if (lane_left(i, j, S.lane_pseq[i])) continue;
       }
       i++;
     }
   }
 
+  // Job j has left lane index i (JobFinish; eviction, A35): delete
+  // the lane if ref(lane) == 0, else L = max E of its residents (A4) and the
+  // backing shrinks to their max actual E.  Freed pages are fenced on the
+  // slot's physical record `fseq` (~0 = none).  Returns true if deleted.
+  __device__ bool lane_left(uint32_t i, uint32_t j, uint64_t fseq) {
+    const uint32_t slot = S.lane_slot[i];
+    uint32_t cnt = 0, maxe = 0, maxae = 0;
+    for (uint32_t a = tid; a < an; a += 32) {
+      uint32_t r = S.adm[a];
+      if (S.jslot[r] == slot) { cnt++; maxe = max(maxe, S.e[r]); maxae = max(maxae, S.ae[r]); }
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    maxe = warp_max_u32(maxe);
+    maxae = warp_max_u32(maxae);
+    if (cnt == 0) {                           // ref(lane) == 0: delete lane
+      emit(SALUS_REC_LANE_CLOSE, S.lane_id[i], S.id[j], 0, 0);
+      push_pages(lane_table(slot), S.lane_back[i], slot, fseq);
+      sumL -= S.lane_L[i];
+      if (tid == 0) S.tail_seq[slot] = S.last_app[slot];
+      slot_free |= (1ull << slot);
+      remove_lane(i);
+      return true;
+    }
+    if (maxe < S.lane_L[i]) {                 // A4: L_j = max E_i of residents
+      emit(SALUS_REC_LANE_SHRINK, S.lane_id[i], S.id[j], maxe, S.lane_L[i]);
+      sumL -= S.lane_L[i] - maxe;
+      if (tid == 0) S.lane_L[i] = maxe;
+    }
+    if (maxae < S.lane_back[i]) {
+      push_pages(lane_table(slot) + maxae, S.lane_back[i] - maxae, slot, fseq);
+      if (tid == 0) { S.lane_back[i] = maxae; S.tail_seq[slot] = S.last_app[slot]; }
+    }
+    __syncwarp();
+    return false;
+  }
+
   __device__ void q_insert(uint32_t j) {
     uint32_t pos = qn;
-    if (P.policy == SALUS_SRTF) {            // A10: key (n*c, arrival, id)
-      const int64_t kj = (int64_t)S.n[j] * S.c[j];
+    if (P.policy == SALUS_SRTF) {            // A10: key ((n - done)*c, arrival, id) (A35: done > 0 when swapped)
+      const uint64_t kj = srtf_key(j);
       uint32_t cnt = 0;
-      for (uint32_t q = tid; q < qn; q += 32) {
-        uint32_t r = S.Q[q];
-        if ((int64_t)S.n[r] * S.c[r] <= kj) cnt++;   // r arrived earlier: rank(r) < j
-      }
+      for (uint32_t q = tid; q < qn; q += 32)
+        if (srtf_key(S.Q[q]) < kj) cnt++;
       pos = __reduce_add_sync(0xffffffffu, cnt);
       // shift [pos, qn) right by one, high chunks first
       for (int64_t b = (int64_t)((qn - 1) & ~31u); qn > 0 && b >= (int64_t)(pos & ~31u); b -= 32) {
@@ -465,7 +502,7 @@ struct Sched {
       uint32_t j = 0, cnt = 0;
       if (k < P.n_infer) {
         j = S.infer[k];
-        if ((S.st[j] == ST_QUEUED || S.st[j] == ST_ADMITTED) && S.nrt[j] == t) {
+        if (live_state(S.st[j]) && S.nrt[j] == t) {
           const uint32_t off = S.req_off[j];
           uint32_t nr = S.next_req[j];
           int64_t nt = t;                  // == rq[off + nr] (that is why we are here)
@@ -506,6 +543,7 @@ struct Sched {
   }
 
   __device__ void admit(uint32_t j, int branch, uint32_t li) {
+    const bool restored = S.st[j] == ST_SWAPPED;         // A35: re-admission of a victim
     uint32_t slot;
     if (branch == 1) {                                   // new lane
       // any free slot will do (slots are physical, never logged): prefer
@@ -522,6 +560,7 @@ struct Sched {
       if (tid == 0) {
         S.lane_id[li] = next_lane; S.lane_L[li] = S.e[j]; S.lane_slot[li] = slot; S.lane_back[li] = 0;
         S.lane_busy[li] = IDLE_T; S.lane_cur[li] = NONE16; S.lane_last[li] = NONE16; S.lane_seq[li] = 0;
+        S.lane_pseq[li] = 0;
       }
       next_lane++; nl++; sumL += S.e[j];
       __syncwarp();
@@ -549,6 +588,12 @@ struct Sched {
       pop_pages(lane_table(slot) + S.lane_back[li], S.ae[j] - S.lane_back[li], slot);
       if (tid == 0) S.lane_back[li] = S.ae[j];
     }
+    if (restored && physical && S.ap[j] > 0) {
+      // its page-table entries are read by its swap-out record: rewrite them
+      // only once that record has completed
+      const uint64_t f = P.swap_fence[j];
+      wait_slot((uint32_t)(f >> 56), f & ((1ull << 56) - 1));
+    }
     pop_pages(job_table(j), S.ap[j], slot);
     if (P.policy == SALUS_FAIR) {                        // A12: virtual-time start
       const int64_t m = min_svc_in(slot, NONE32, false);
@@ -556,11 +601,120 @@ struct Sched {
     }
     if (tid == 0) {
       S.adm[an] = (uint16_t)j; S.jslot[j] = (uint8_t)slot; S.st[j] = ST_ADMITTED;
-      P.stats[j].admit_tick = t; P.stats[j].first_lane = S.lane_id[li];
+      if (!restored) { P.stats[j].admit_tick = t; P.stats[j].first_lane = S.lane_id[li]; }
     }
     an++; sumP += S.p[j];
     __syncwarp();
-    emit(SALUS_REC_JOB_ADMIT, S.lane_id[li], S.id[j], S.p[j], S.e[j]);
+    emit(restored ? SALUS_REC_JOB_RESTORE : SALUS_REC_JOB_ADMIT, S.lane_id[li], S.id[j], S.p[j], S.e[j]);
+    // the copy back precedes the job's next iteration in the slot's ring
+    if (restored && physical && S.ap[j] > 0) append(slot, S.lane_id[li], j, REC_SWAP_IN);
+  }
+
+  // ------------------------------------------------------------ eviction (A35)
+  // SALUS_FLAG_EVICT, SRTF: "the higher priority job is admitted as long as
+  // its own safety condition is met ... regardless of other already-running
+  // jobs".  Victims are admitted jobs with a larger SRTF key that are
+  // not mid-iteration, largest key first, until FindLane succeeds on the
+  // hypothetical state; all or nothing.
+
+  __device__ uint32_t lane_index_of_slot(uint32_t slot) const {
+    uint32_t i = 0;
+    while (i < nl && S.lane_slot[i] != slot) i++;
+    return i;
+  }
+
+  // swap out job v (its decision is final): leave the lane, free its pages
+  // behind a swap-out record in its slot's ring
+  __device__ void evict(uint32_t v) {
+    const uint32_t slot = S.jslot[v];
+    const uint32_t i = lane_index_of_slot(slot);
+    if (tid == 0) S.st[v] = ST_SWAPPED;
+    sumP -= S.p[v];
+    __syncwarp();
+    remove_adm(v);
+    emit(SALUS_REC_JOB_EVICT, S.lane_id[i], S.id[v], S.p[v], S.done[v]);
+    if (physical && S.ap[v] > 0) {
+      append(slot, S.lane_id[i], v, REC_SWAP_OUT);
+      if (err) return;
+      if (tid == 0) P.swap_fence[v] = ((unsigned long long)slot << 56) | S.last_app[slot];
+      __syncwarp();
+    }
+    // the last record of the slot (the swap-out; ~0 = none ever) fences the pages
+    const uint64_t fseq = S.last_app[slot] - 1;
+    push_pages(job_table(v), S.ap[v], slot, fseq);
+    lane_left(i, v, fseq);
+  }
+
+  __device__ bool executing(uint32_t v) const {
+    const uint32_t i = lane_index_of_slot(S.jslot[v]);
+    return i < nl && S.lane_busy[i] != IDLE_T && S.lane_cur[i] == v;
+  }
+
+  // Returns FindLane's branch for j after the evictions (0: nobody evicted).
+  // Victims are appended to P.evl[*nev..] (they join Q after the pass).
+  __device__ int evict_for(uint32_t j, uint32_t *li, uint32_t *nev) {
+    const uint64_t kj = srtf_key(j);
+    int64_t hP = sumP;
+    uint32_t nch = 0;
+    bool fits = false;
+    for (;;) {
+      uint64_t best = 0;
+      for (uint32_t a = tid; a < an; a += 32) {
+        const uint32_t v = S.adm[a];
+        if (S.st[v] != ST_ADMITTED) continue;          // chosen already in this attempt
+        const uint64_t kv = srtf_key(v);
+        if (kv > kj && kv > best && !executing(v)) best = kv;
+      }
+      best = warp_max_u64(best);
+      if (best == 0) break;                             // no candidate left
+      const uint32_t v = (uint32_t)(best & ((1u << KEY_BITS) - 1));
+      if (tid == 0) { S.st[v] = ST_SWAPPED; P.evl[*nev + nch] = (uint16_t)v; }
+      nch++;
+      hP -= S.p[v];
+      __syncwarp();
+      int64_t hS = hP;
+      uint32_t nopen = 0;
+      for (uint32_t i = 0; i < nl; i++) {               // L = max e of the remaining residents
+        uint32_t cnt = 0, mx = 0;
+        for (uint32_t a = tid; a < an; a += 32) {
+          const uint32_t r = S.adm[a];
+          if (S.st[r] == ST_ADMITTED && S.jslot[r] == S.lane_slot[i]) { cnt++; mx = max(mx, S.e[r]); }
+        }
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        mx = warp_max_u32(mx);
+        if (tid == 0) S.hL[i] = cnt ? mx : NONE32;
+        if (cnt) { hS += mx; nopen++; }
+      }
+      __syncwarp();
+      uint32_t hli;
+      if (find_lane_g(S.p[j], S.e[j], S.hL, nl, nopen, hS, &hli)) { fits = true; break; }
+    }
+    __syncwarp();
+    if (!fits) {                                        // nothing is evicted
+      for (uint32_t k = tid; k < nch; k += 32) S.st[P.evl[*nev + k]] = ST_ADMITTED;
+      __syncwarp();
+      return 0;
+    }
+    for (uint32_t k = 0; k < nch && !err; k++) evict(P.evl[*nev + k]);
+    *nev += nch;
+    return find_lane(S.p[j], S.e[j], li);
+  }
+
+  // P3 with eviction: one in-order pass over Q (sorted by SRTF key); a job
+  // FindLane rejects may evict; victims join Q after the pass (so none is
+  // re-admitted in the pass that evicted it).
+  __device__ void phase_admission_evict() {
+    uint32_t pos = 0, nev = 0;
+    while (pos < qn && !err) {
+      const uint32_t j = S.Q[pos];
+      uint32_t li = 0;
+      int br = find_lane(S.p[j], S.e[j], &li);
+      if (br == 0) br = evict_for(j, &li, &nev);
+      if (br == 0) { pos++; continue; }
+      q_remove(pos);
+      admit(j, br, li);
+    }
+    for (uint32_t k = 0; k < nev; k++) q_insert(P.evl[k]);
   }
 
   // P3: ProcessRequests — one in-order pass over Q (A5, A7, A8, A14)
@@ -615,13 +769,13 @@ struct Sched {
   // Append the dispatch to the slot's ring (A30 mode 2); if the slot is idle,
   // take the `running` token and start it here, else the worker finishing
   // the slot's current iteration will.
-  __device__ void append(uint32_t slot, uint32_t lane_id, uint32_t j) {
+  __device__ void append(uint32_t slot, uint32_t lane_id, uint32_t j, uint32_t kind = REC_ITER) {
 #if SALUS_DBG_SCHED
     const uint64_t ta_ = ptx::globaltimer();
-    append_body(slot, lane_id, j);
+    append_body(slot, lane_id, j, kind);
     append_ns += ptx::globaltimer() - ta_;
   }
-  __device__ void append_body(uint32_t slot, uint32_t lane_id, uint32_t j) {
+  __device__ void append_body(uint32_t slot, uint32_t lane_id, uint32_t j, uint32_t kind) {
 #endif
     wait_fences(slot);
     if (err) return;
@@ -651,15 +805,16 @@ struct Sched {
     uint32_t won = 0;
     if (tid == 0) {
       volatile DispRec *vr = &sl.recs[tl % RQ];
-      vr->job = j; vr->iter = S.done[j]; vr->seq = seq; vr->lane_id = lane_id; vr->pad = 0;
+      vr->job = j; vr->iter = S.done[j]; vr->seq = pseq; vr->lseq = seq; vr->lane_id = lane_id; vr->kind = kind;
       vr->append_ns = ptx::globaltimer();
       // publish (release) and learn whether the slot was idle in one atomic;
       // only the scheduler ever sets `running`, so taking it needs no CAS
       won = (atom_add_release_u64(&sl.qstate, 1ull << 32) & 1ull) == 0;
       if (won) atomicOr(&sl.qstate, 1ull);
       S.sq_tail[slot] = tl + 1;
-      S.last_app[slot] = seq + 1;
+      S.last_app[slot] = pseq + 1;
     }
+    pseq++;
     __syncwarp();
     won = __shfl_sync(0xffffffffu, won, 0);
     if (!won) return;
@@ -673,7 +828,7 @@ struct Sched {
     if (!got) return;
     first = __shfl_sync(0xffffffffu, first, 0);
     jj = __shfl_sync(0xffffffffu, jj, 0);
-    enqueue(slot, first, P.jobs[jj].stage_tiles[first]);
+    enqueue(slot, first, stage_ntiles(P.jobs[jj], first));
   }
 
   // End of the schedule: wait for every slot to drain its ring.
@@ -715,7 +870,7 @@ struct Sched {
       const int64_t pen = (last != NONE16 && last != j) ? P.switch_ticks : 0;   // A16
       if (tid == 0) {
         S.lane_busy[i] = t + pen + S.c[j];
-        S.lane_cur[i] = (uint16_t)j; S.lane_last[i] = (uint16_t)j; S.lane_seq[i] = seq;
+        S.lane_cur[i] = (uint16_t)j; S.lane_last[i] = (uint16_t)j; S.lane_seq[i] = seq; S.lane_pseq[i] = pseq;
         if (S.kind[j] == SALUS_INFER) S.pending[j] -= 1;
         salus_job_stat &st = P.stats[j];
         if (S.done[j] == 0) st.first_start_tick = t;   // a job's iterations never overlap
@@ -757,7 +912,10 @@ struct Sched {
       SALUS_PH(1, phase_completions())
       if (err) break;
       SALUS_PH(2, phase_arrivals())
-      if (qn > 0 && dirty) SALUS_PH(3, phase_admission())
+      // A35: with eviction an iteration end can make its job evictable, so
+      // the pass runs at every tick with a queued job
+      if (qn > 0 && evict_mode) SALUS_PH(3, phase_admission_evict())
+      else if (qn > 0 && dirty) SALUS_PH(3, phase_admission())
       if (P.flags & SALUS_FLAG_CHECK) check_safety();
       SALUS_PH(4, phase_dispatch())
       if ((n_ticks & 255) == 0) {

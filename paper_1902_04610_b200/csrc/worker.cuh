@@ -78,7 +78,7 @@ constexpr uint32_t WORKER_THREADS = 32 * (DONE_WARP + 1);
 constexpr uint32_t ACC_COLS = 256;
 constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;          // all of TMEM: 2 accumulators
 
-enum : uint32_t { T_EXIT = 0, T_INIT = 1, T_GEN = 2, T_GEMM = 3 };
+enum : uint32_t { T_EXIT = 0, T_INIT = 1, T_GEN = 2, T_GEMM = 3, T_COPY = 4 };
 enum : uint32_t { EPI_RELU = 0, EPI_OUT = 1, EPI_LOSS = 2, EPI_DX = 3, EPI_SGD = 4 };
 // translated pointers of a tile: bf16 output panels, Wb panels (SGD/INIT),
 // fp32 master pages, epilogue-input panels (DX mask)
@@ -99,7 +99,8 @@ struct TileDesc {
   uint32_t valid;          // this CTA's half exists (odd block counts leave the peer's empty)
   uint32_t peer_valid;     // the pair's second M block exists
   uint32_t peer_nca;       // (leader) A copies per K-chunk of the peer CTA
-  uint64_t seq, t_claim, t_ready, t_mma, t_end;   // trace stamps
+  uint64_t seq, t_claim, t_ready, t_mma, t_end;   // physical record seq, trace stamps
+  uint64_t lseq;           // logical dispatch seq (wall stamps)
   // GEMM
   uint32_t N, nk, idesc, epi, layer, ncopy_a, ncopy_b, abytes, bbytes;
   uint32_t n_ech;          // epilogue-input chunks (0 = none)
@@ -210,11 +211,11 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   const uint32_t slot = payload >> 26, stage = (payload >> 21) & 31u, tile = payload & ((1u << 21) - 1);
   const uint32_t k = sl.iter;
   const uint32_t L = J.n_layers, bp = J.bpad;
-  td.slot = slot; td.stage = stage; td.job = sl.job; td.iter = k; td.seq = sl.seq;
-  td.ntiles = J.stage_tiles[stage];
-  td.is_last = stage == last_stage(J.kind, L);
+  td.slot = slot; td.stage = stage; td.job = sl.job; td.iter = k; td.seq = sl.seq; td.lseq = sl.lseq;
+  td.ntiles = stage_ntiles(J, stage);
+  td.is_last = stage >= STAGE_SWAP_OUT || stage == last_stage(J.kind, L);
   td.next_ntiles = td.is_last ? 0 : J.stage_tiles[stage + 1];
-  td.first_stage = k == 0 ? 0u : 1u;
+  td.first_stage = stage >= STAGE_SWAP_OUT ? stage : k == 0 ? 0u : 1u;
   td.dump_off = -1;
   td.n_ech = 0;
   td.xt_mask = 0;
@@ -223,6 +224,19 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   const uint32_t *lt = P.lpt + (uint64_t)slot * P.lpt_stride;   // lane (ephemeral) space
   const uint32_t *jt = P.ppt + J.pt_off;                        // job (persistent) space
 
+  if (stage >= STAGE_SWAP_OUT) {                      // A35 swap: CTA h copies page 2 tile + h
+    td.kind = T_COPY;
+    const uint32_t pg = 2 * tile + h;
+    td.valid = pg < J.ap_pages;
+    td.m0 = pg;
+    if (td.valid) {
+      uint8_t *dev = P.arena + ((uint64_t)jt[pg] << PAGE_SHIFT);
+      uint8_t *host = P.swap + ((uint64_t)(J.pt_off + pg) << PAGE_SHIFT);
+      td.ptr[PTR_OUT] = stage == STAGE_SWAP_OUT ? host : dev;      // destination
+      td.ptr[PTR_OUT + 1] = stage == STAGE_SWAP_OUT ? dev : host;  // source
+    }
+    return;
+  }
   if (stage == 0) {                                   // INIT weights (128 x 128 blocks)
     td.kind = T_INIT;
     uint32_t t = 2 * tile + h, l = 1;
@@ -524,6 +538,22 @@ __device__ void gen_tile(const TileDesc &td, uint32_t r, uint32_t h) {
     u.z = pack_bf16x2(v[4], v[5]); u.w = pack_bf16x2(v[6], v[7]);
     *reinterpret_cast<uint4 *>((cg < 64 ? out0 : out1) + swz(r, (cg % 64) / 8)) = u;
   }
+}
+
+// A35 swap copy: one 64 KiB page between the arena and the pinned host swap
+// area (PCIe), 16 x 16 B per epilogue thread, all loads in flight before the
+// stores.  The system-scope fence makes the host-side bytes visible to the
+// SM that later copies them back (another slot's record).
+__device__ void copy_page(const TileDesc &td, uint32_t et) {
+  const uint4 *src = reinterpret_cast<const uint4 *>(td.ptr[PTR_OUT + 1]);
+  uint4 *dst = reinterpret_cast<uint4 *>(td.ptr[PTR_OUT]);
+  constexpr uint32_t PER = PAGE_BYTES / 16 / EPI_THREADS;
+  uint4 v[PER];
+#pragma unroll
+  for (uint32_t k = 0; k < PER; k++) v[k] = __ldcv(src + k * EPI_THREADS + et);
+#pragma unroll
+  for (uint32_t k = 0; k < PER; k++) __stcg(dst + k * EPI_THREADS + et, v[k]);
+  __threadfence_system();
 }
 
 // ---------------------------------------------------------------------------
@@ -840,6 +870,8 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
       }
       if (++b == 2) { b = 0; b_phase ^= 1; }
     } else if (!td.valid) {
+    } else if (td.kind == T_COPY) {
+      copy_page(td, et);
     } else if (td.kind == T_INIT) {
       init_tile(td, r, h);
     } else {
@@ -890,24 +922,31 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
       Slot &sl = P.slots[td.slot];
       const uint32_t old = ptx::atom_add_acqrel_u32(&sl.stage_done[td.stage], 1u);
       if (old + 1 == 2 * td.ntiles) {
-        if (td.is_last) {                      // the iteration is physically complete
+        if (td.is_last) {                      // the record is physically complete
           const uint64_t end = ptx::globaltimer(), start = sl.start_ns;
           sl.end_ns = end;
           const DevJob &J = P.jobs[td.job];
-          if ((P.flags & SALUS_FLAG_LOG) && td.seq < P.log_cap) {
-            salus_wall_rec w;
-            w.seq = td.seq; w.lane = sl.lane_id; w.job = J.job_id; w.start_ns = start; w.end_ns = end;
-            w.append_ns = sl.append_ns;
-            P.wall[td.seq] = w;
+          if (td.kind == T_COPY) {             // A35 swap record
+            __threadfence_system();
+            atomicAdd(td.stage == STAGE_SWAP_OUT ? &P.ctrl->n_swap_out : &P.ctrl->n_swap_in, 1ull);
+            atomicAdd(&P.ctrl->swap_bytes, (unsigned long long)J.ap_pages << PAGE_SHIFT);
+            atomicAdd(&P.ctrl->swap_ns, (unsigned long long)(end - start));
+          } else {
+            if ((P.flags & SALUS_FLAG_LOG) && td.lseq < P.log_cap) {
+              salus_wall_rec w;
+              w.seq = td.lseq; w.lane = sl.lane_id; w.job = J.job_id; w.start_ns = start; w.end_ns = end;
+              w.append_ns = sl.append_ns;
+              P.wall[td.lseq] = w;
+            }
+            if (td.iter == 0) P.stats[td.job].wall_start_ns = start;
+            if (td.iter + 1 == J.n_iters) P.stats[td.job].wall_end_ns = end;
           }
-          if (td.iter == 0) P.stats[td.job].wall_start_ns = start;
-          if (td.iter + 1 == J.n_iters) P.stats[td.job].wall_end_ns = end;
           ptx::st_release_u64(&sl.done_seq, td.seq + 1);
           // run-ahead: start the slot's next queued iteration right here
           DispRec rec;
           if (take_next(sl, &rec)) {
             pst = begin_iteration(sl, rec);
-            pub = 1; ps = td.slot; pn = P.jobs[rec.job].stage_tiles[pst];
+            pub = 1; ps = td.slot; pn = stage_ntiles(P.jobs[rec.job], pst);
             pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)pn);
           }
         } else {

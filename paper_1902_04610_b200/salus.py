@@ -19,7 +19,7 @@ LIB_PATH = os.environ.get("SALUS_LIB", os.path.join(HERE, "libsalus.so"))
 
 FIFO, SRTF, PACK, FAIR = 0, 1, 2, 3
 TRAIN, INFER = 0, 1
-FLAG_LOG, FLAG_NULL_WORK, FLAG_CHECK, FLAG_TRACE, FLAG_ONLINE = 1, 2, 4, 8, 16
+FLAG_LOG, FLAG_NULL_WORK, FLAG_CHECK, FLAG_TRACE, FLAG_ONLINE, FLAG_EVICT = 1, 2, 4, 8, 16, 32
 DUMP_OUTPUTS, DUMP_WEIGHTS = 1, 2
 WEIGHTS = 0xFFFFFFFF
 
@@ -62,7 +62,9 @@ class RunStats(C.Structure):
                 ("n_tasks", C.c_uint64), ("kernel_ns", C.c_uint64), ("wall_first_ns", C.c_uint64),
                 ("wall_last_ns", C.c_uint64), ("sched_wait_ns", C.c_uint64), ("status", C.c_int32),
                 ("n_workers", C.c_uint32), ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64),
-                ("sched_fence_ns", C.c_uint64), ("sched_ring_ns", C.c_uint64)]
+                ("sched_fence_ns", C.c_uint64), ("sched_ring_ns", C.c_uint64),
+                ("n_swap_out", C.c_uint64), ("n_swap_in", C.c_uint64), ("swap_bytes", C.c_uint64),
+                ("swap_ns", C.c_uint64)]
 
 
 WALL_DTYPE = np.dtype([("seq", "<u8"), ("lane", "<u4"), ("job", "<u4"), ("start_ns", "<u8"),
@@ -75,7 +77,8 @@ LOG_DTYPE = np.dtype([("tick", "<i8"), ("kind", "<u4"), ("lane", "<u4"), ("job",
 EXPORTS = ["salus_open", "salus_job_footprint", "salus_submit_job", "salus_meta_bytes",
            "salus_prepare", "salus_run", "salus_read_run_stats", "salus_read_log",
            "salus_read_wall", "salus_read_trace", "salus_read_layers", "salus_last_error", "salus_close",
-           "salus_run_async", "salus_submit_live", "salus_end_submissions", "salus_wait"]
+           "salus_run_async", "salus_submit_live", "salus_end_submissions", "salus_wait",
+           "salus_swap_bytes", "salus_set_swap"]
 
 _lib = None
 
@@ -108,6 +111,8 @@ def lib():
         L.salus_submit_live.argtypes = [P, C.POINTER(JobDesc)]
         L.salus_end_submissions.argtypes = [P]
         L.salus_wait.argtypes = [P, C.POINTER(JobStat), C.c_uint64, C.POINTER(C.c_uint64)]
+        L.salus_swap_bytes.argtypes = [P, C.POINTER(C.c_uint64)]
+        L.salus_set_swap.argtypes = [P, P, C.c_uint64]
         for name in EXPORTS:
             if name != "salus_last_error":
                 getattr(L, name).restype = C.c_int
@@ -155,7 +160,8 @@ class Context:
                  max_lanes: int = 0, switch_ticks: int = 0, log: bool = True, null_work: bool = False,
                  check: bool = False, dump: Optional[Dict[int, int]] = None, n_workers: int = 0,
                  timeout_ms: int = 0, page_bytes: int = 65536, trace: bool = False,
-                 trace_capacity: int = 0, online: bool = False, max_jobs: int = 0, dump_bytes: int = 0):
+                 trace_capacity: int = 0, online: bool = False, max_jobs: int = 0, dump_bytes: int = 0,
+                 evict: bool = False):
         import torch
         self._torch = torch
         self.L = lib()
@@ -177,7 +183,7 @@ class Context:
         cfg.max_jobs = max(1, len(self.jobs), max_jobs)
         cfg.flags = ((FLAG_LOG if log else 0) | (FLAG_NULL_WORK if null_work else 0) |
                      (FLAG_CHECK if check else 0) | (FLAG_TRACE if trace else 0) |
-                     (FLAG_ONLINE if online else 0))
+                     (FLAG_ONLINE if online else 0) | (FLAG_EVICT if evict else 0))
         cfg.switch_ticks = switch_ticks
         cfg.n_workers = n_workers
         cfg.timeout_ms = timeout_ms
@@ -190,6 +196,15 @@ class Context:
         for j in self.jobs:
             d, keep = job_desc(j, dump.get(j.job_id, 0))
             self._check(self.L.salus_submit_job(self.ctx, C.byref(d)), f"submit {j.job_id}")
+        self.swap = None
+        if evict:                    # A35: caller-owned pinned host swap area
+            sb = C.c_uint64()
+            self._check(self.L.salus_swap_bytes(self.ctx, C.byref(sb)), "swap_bytes")
+            if sb.value:
+                self.swap = torch.empty(sb.value + 256, dtype=torch.uint8, pin_memory=True)
+                base = self.swap.data_ptr()
+                self._check(self.L.salus_set_swap(self.ctx, C.c_void_p((base + 255) // 256 * 256), sb.value),
+                            "set_swap")
         mb = C.c_uint64()
         self._check(self.L.salus_meta_bytes(self.ctx, C.byref(mb)), "meta_bytes")
         self.meta = torch.empty(max(256, mb.value), dtype=torch.uint8, device=f"cuda:{device}")

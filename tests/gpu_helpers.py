@@ -32,12 +32,13 @@ def first_diff(a: bytes, b: bytes, context=3):
     return f"length differs: gpu {len(ra)} oracle {len(rb)} records"
 
 
-def assert_schedule_parity(jobs, cap, policy, max_lanes=0, switch_ticks=0, null_work=True, **kw):
+def assert_schedule_parity(jobs, cap, policy, max_lanes=0, switch_ticks=0, null_work=True, evict=False,
+                           **kw):
     """Byte-identical canonical log and identical per-job stats (north star:
     'run order, lane ids, per-job completion iteration ... bit-exactly')."""
-    ref = OS.simulate(jobs, cap, policy, max_lanes=max_lanes, switch_ticks=switch_ticks)
+    ref = OS.simulate(jobs, cap, policy, max_lanes=max_lanes, switch_ticks=switch_ticks, evict=evict)
     ctx, stats = run_gpu(jobs, cap, policy, max_lanes=max_lanes, switch_ticks=switch_ticks,
-                         null_work=null_work, log=True, **kw)
+                         null_work=null_work, log=True, evict=evict, **kw)
     try:
         got = ctx.log_bytes()
         want = ref.log_bytes()

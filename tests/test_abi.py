@@ -34,7 +34,7 @@ def test_exports_every_declared_symbol(L):
 
 def test_struct_sizes_match_header_layout():
     assert C.sizeof(S.JobStat) == 64
-    assert C.sizeof(S.RunStats) == 104
+    assert C.sizeof(S.RunStats) == 136
     assert S.LOG_DTYPE.itemsize == 32 and S.WALL_DTYPE.itemsize == 40
 
 
