@@ -243,6 +243,43 @@ def c4_jct(S, device):
     return out
 
 
+def c4e_evict(S, device):
+    """SURVEY §8(f) NEXT-3 (reading A35): the C4 trace with 8x the
+    declared persistent memory (C4e), so SRTF admission runs into the safety
+    condition.  SRTF without and with eviction, every iteration executed:
+    logical average JCT (bit-identical to the oracle's log), and the swap
+    records the kernel executed -- persistent pages copied to pinned host
+    memory and back -- with their measured bandwidth."""
+    from oracle import metrics as OM, scheduler as OS
+    from workloads import c4_trace
+    jobs, cap = c4_trace(p_scale=8.0)
+    out = {"config": "C4e: C4 with declared P x8 (0.89-6.6 GB), SRTF, 1 lane, 16 GiB"}
+    for name, ev in (("srtf", False), ("srtf_evict", True)):
+        ctx = S.Context(jobs, cap, S.SRTF, device=device, log=True, evict=ev)
+        try:
+            st = ctx.run()
+            rs = ctx.run_stats()
+            log = ctx.log_bytes()
+        finally:
+            ctx.close()
+        ref = OS.simulate(jobs, cap, OS.SRTF, evict=ev)
+
+        class _St:
+            def __init__(self, d):
+                self.__dict__.update(d)
+        m = OM.summarize(jobs, {k: _St(v) for k, v in st.items()})
+        r = {"avg_jct_ticks": m["avg_jct"], "makespan_ticks": m["makespan"],
+             "log_matches_oracle": log == ref.log_bytes(), "kernel_ms": rs["kernel_ns"] / 1e6}
+        if ev:
+            r.update({"n_swap_out": rs["n_swap_out"], "n_swap_in": rs["n_swap_in"],
+                      "swap_gib": rs["swap_bytes"] / 2**30,
+                      "swap_gbs": rs["swap_bytes"] / max(1, rs["swap_ns"]),
+                      "swap_ms_total": rs["swap_ns"] / 1e6})
+        out[name] = r
+    out["srtf_over_evict_avg_jct"] = out["srtf"]["avg_jct_ticks"] / out["srtf_evict"]["avg_jct_ticks"]
+    return out
+
+
 def c2b_tensor(S, device, n_jobs=8, n_iters=20):
     """C2b: the compute-heavy sweep member, MLP [4096]^4
     B=2048 training (AI 683 flop/B, tensor-bound), n_jobs packed into one
@@ -429,6 +466,7 @@ SIDE_SECTIONS = {
     "jct": ("jct_physical", lambda S, d, jobs, cap: jct_physical(S, d, jobs, cap)),
     "c4": ("c4_jct", lambda S, d, jobs, cap: c4_jct(S, d)),
     "c2b": ("c2b_tensor", lambda S, d, jobs, cap: c2b_tensor(S, d)),
+    "evict": ("c4e_evict", lambda S, d, jobs, cap: c4e_evict(S, d)),
     "online": ("online_submission", lambda S, d, jobs, cap: online_submission(S, d)),
 }
 
@@ -451,7 +489,7 @@ def main():
     ap.add_argument("--impl", default="salus", choices=["salus", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--only", default="",
-                    help="comma list of side sections to run alone and print (c1,c2b,c3,c4,jct,online,overhead)")
+                    help="comma list of side sections to run alone and print (c1,c2b,c3,c4,evict,jct,online,overhead)")
     args = ap.parse_args()
     rank, world, local = dist_env()
 

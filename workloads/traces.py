@@ -237,12 +237,16 @@ def _loguniform(rng, lo, hi):
 
 
 def c4_trace(n_jobs: int = 100, seed: int = 4, load: float = 1.2, burst: bool = False,
-             rate_scale: float = 1.0, job_id_base: int = 0) -> Tuple[List[Job], int]:
+             rate_scale: float = 1.0, job_id_base: int = 0, p_scale: float = 1.0) -> Tuple[List[Job], int]:
     """C4: mixed training trace (stand-in for the unpublished Gandiva
     distribution).  n log-uniform [10, 2000]; width {256..4096} x
     depth {2,3,4} x B {64..1024}; declared P log-uniform [110.9 MB, 822.2 MB]
     (P:159), E log-uniform up to 13.8 GB - P; Poisson arrivals at
-    offered load `load` of one lane.  C = 16 GiB."""
+    offered load `load` of one lane.  C = 16 GiB.
+
+    `p_scale` multiplies the declared P (C4e, the eviction config of
+    SURVEY §8(f) NEXT-3: p_scale 8 -> P in [0.89, 6.6] GB, so admitted jobs'
+    persistent memory fills the GPU and SRTF admission has to evict)."""
     rng = np.random.default_rng(seed)
     widths = [256, 512, 1024, 2048, 4096]
     batches = [64, 128, 256, 512, 1024]
@@ -254,7 +258,7 @@ def c4_trace(n_jobs: int = 100, seed: int = 4, load: float = 1.2, burst: bool = 
         n = int(round(_loguniform(rng, 10, 2000)))
         dims = (w,) * (depth + 1)
         p_act, e_act = footprint_bytes(TRAIN, dims, b)
-        P = max(p_act, int(_loguniform(rng, 110.9e6, 822.2e6)))
+        P = max(p_act, int(p_scale * _loguniform(rng, 110.9e6, 822.2e6)))
         e_lo = max(e_act, 64 * MIB)
         e_hi = max(e_lo + 1, int(13.8e9) - P)
         E = max(e_act, int(_loguniform(rng, e_lo, e_hi)))
