@@ -8,6 +8,7 @@ gloo in the CPU tests).  Host logic only — marshalling, no method arithmetic.
 """
 from __future__ import annotations
 
+import heapq
 from typing import Dict, Iterable
 
 import numpy as np
@@ -48,6 +49,24 @@ def gather_stats(stats: Dict[int, dict], rank: int, world: int, device=None) -> 
     return merged
 
 
-def partition_jobs(jobs: Iterable, world: int, rank: int):
-    from workloads import partition
-    return partition(list(jobs), world, rank)
+def partition_jobs(jobs: Iterable, world: int, rank: int, placement: str = "mod"):
+    """This rank's jobs.  placement "mod": the k-th job in (arrival, id)
+    order goes to GPU k mod G.  "lpt" (NEXT-4, reading A36):
+    longest logical work n*c first, each to the least-loaded GPU so far
+    (ties: lowest rank) -- balances heterogeneous traces such as C5, where
+    mod-G leaves one GPU with far more work than the others.  Either way the
+    rank's jobs are returned in (arrival, id) order."""
+    jobs = list(jobs)
+    if placement == "mod":
+        from workloads import partition
+        return partition(jobs, world, rank)
+    if placement != "lpt":
+        raise ValueError(f"unknown placement {placement!r}")
+    heap = [(0, r) for r in range(world)]       # (work so far, rank)
+    mine = []
+    for j in sorted(jobs, key=lambda j: (-(j.n_iters * j.iter_ticks), j.arrival_tick, j.job_id)):
+        w, r = heapq.heappop(heap)
+        if r == rank:
+            mine.append(j)
+        heapq.heappush(heap, (w + j.n_iters * j.iter_ticks, r))
+    return sorted(mine, key=lambda j: (j.arrival_tick, j.job_id))

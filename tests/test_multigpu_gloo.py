@@ -71,3 +71,65 @@ def test_gloo_world2_allgather_matches_per_partition_oracle():
             assert g["rank"] == r
             assert (g["completion_tick"], g["completion_seq"], g["first_lane"]) == \
                 (s.completion_tick, s.completion_seq, s.first_lane)
+
+
+# ---------------------------------------------------------------- NEXT-4 placement
+
+def _tiny_jobs(ws, arr=None):
+    from workloads import make_job, TRAIN
+    return [make_job(i, TRAIN, 0 if arr is None else arr[i], (128, 128), 128, n, iter_ticks=c)
+            for i, (n, c) in enumerate(ws)]
+
+
+def test_lpt_placement_equals_oracle_rule():
+    """The product's heap-based LPT gives the oracle's plain-loop placement."""
+    import numpy as np
+    from oracle import placement as OP
+    rng = np.random.default_rng(3)
+    for trial in range(60):
+        n = int(rng.integers(1, 40))
+        G = int(rng.integers(1, 9))
+        ws = [(int(rng.integers(1, 20)), int(rng.integers(1, 5)) * 10) for _ in range(n)]
+        jobs = _tiny_jobs(ws, arr=[int(x) for x in rng.integers(0, 5, size=n)])
+        ref = OP.place_lpt(jobs, G)
+        for r in range(G):
+            assert [j.job_id for j in MG.partition_jobs(jobs, G, r, "lpt")] == [j.job_id for j in ref[r]]
+        refm = OP.place_mod(jobs, G)
+        for r in range(G):
+            assert [j.job_id for j in MG.partition_jobs(jobs, G, r, "mod")] == [j.job_id for j in refm[r]]
+
+
+def test_lpt_graham_bound_against_brute_force():
+    """Pin of the oracle rule: LPT's max load <= (4/3 - 1/(3G)) OPT (Graham
+    1969), OPT by enumerating every assignment of <= 8 jobs to <= 3 GPUs;
+    and with identical works LPT is a balanced round robin."""
+    import itertools
+    import numpy as np
+    from oracle import placement as OP
+    rng = np.random.default_rng(11)
+    for trial in range(150):
+        n = int(rng.integers(1, 9))
+        G = int(rng.integers(1, 4))
+        ws = [(int(rng.integers(1, 12)), 1) for _ in range(n)]
+        jobs = _tiny_jobs(ws)
+        w = [a * b for a, b in ws]
+        opt = min(max(sum(w[i] for i in range(n) if a[i] == g) for g in range(G))
+                  for a in itertools.product(range(G), repeat=n))
+        got = max(OP.loads(OP.place_lpt(jobs, G)))
+        assert got * 3 * G <= (4 * G - 1) * opt, (ws, G, got, opt)
+        assert sum(OP.loads(OP.place_lpt(jobs, G))) == sum(w)
+    same = _tiny_jobs([(5, 10)] * 13)
+    sizes = [len(p) for p in OP.place_lpt(same, 4)]
+    assert max(sizes) - min(sizes) <= 1
+
+
+def test_lpt_balances_c5_better_than_mod():
+    from oracle import placement as OP
+    from workloads import c5_trace
+    jobs, cap = c5_trace()
+    for G in (2, 4, 8):
+        lm = OP.loads(OP.place_mod(jobs, G))
+        ll = OP.loads(OP.place_lpt(jobs, G))
+        assert sum(lm) == sum(ll)
+        assert max(ll) <= max(lm)
+        assert max(ll) <= 1.01 * sum(ll) / G      # near-perfect balance on 2000 jobs
