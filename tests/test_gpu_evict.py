@@ -102,3 +102,42 @@ def test_evict_flag_validation():
     for pol in (S.FIFO, S.PACK, S.FAIR):
         with pytest.raises(S.SalusError):
             S.Context(jobs, 1 << 26, pol, evict=True)
+
+
+def test_c4e_schedule_parity():
+    """C4e (the bench's eviction config, 13 evictions) with the allocator and
+    dispatch only: byte-identical log."""
+    from workloads import c4_trace
+    jobs, cap = c4_trace(p_scale=8.0)
+    ctx, ref, stats = assert_schedule_parity(jobs, cap, OS.SRTF, evict=True)
+    assert _n_evicts(ref) >= 10
+    ctx.close()
+
+
+def test_c4e_real_work_swaps_do_not_change_math():
+    """Full size: C4e executed with eviction (the [4096]^5 B=1024 job 49 is
+    swapped out and back 11 times, 0.5 GB each way) and without it must give
+    bit-identical final weights for every evicted job -- the kernel's math is
+    deterministic per job, so any byte lost or misplaced by a swap round trip
+    would show (the oracle cannot follow 1583 iterations of this job)."""
+    from paper_1902_04610_b200 import salus as S
+    from workloads import c4_trace
+    jobs, cap = c4_trace(p_scale=8.0)
+    ref = OS.simulate(jobs, cap, OS.SRTF, evict=True)
+    victims = sorted({r[3] for r in ref.log if r[1] == LG.JOB_EVICT})
+    assert victims
+    dump = {v: S.DUMP_WEIGHTS for v in victims}
+    out = {}
+    for ev in (True, False):
+        ctx, r2, stats = assert_schedule_parity(jobs, cap, OS.SRTF, evict=ev, null_work=False, dump=dump,
+                                                timeout_ms=300000)
+        try:
+            out[ev] = {v: ctx.layers(v, S.WEIGHTS).copy() for v in victims}
+            if ev:
+                rs = ctx.run_stats()
+                assert rs["n_swap_out"] == _n_evicts(ref) == rs["n_swap_in"]
+        finally:
+            ctx.close()
+    for v in victims:
+        assert np.isfinite(out[True][v]).all()
+        assert np.array_equal(out[True][v], out[False][v]), v
