@@ -205,7 +205,26 @@ __device__ __forceinline__ void named_bar(uint32_t id, uint32_t n) {
 // ---------------------------------------------------------------------------
 // A task is a pair task: CTA h takes block 2t + h of INIT / GEN, and M block
 // 2 mp + h of a GEMM super-tile (the N block is shared).
-__device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, const Slot &sl,
+// The slot's in-flight record as the decoder sees it (two vector loads).
+struct SlotHead { uint32_t job, iter; uint64_t seq, lseq; };
+
+__device__ __forceinline__ SlotHead load_slot_head(const Slot &sl) {
+  static_assert(offsetof(Slot, job) == 0 && offsetof(Slot, iter) == 4 && offsetof(Slot, seq) == 8 &&
+                offsetof(Slot, lseq) == 16, "Slot head layout");
+  uint4 a;
+  uint2 b;
+  asm volatile("ld.relaxed.gpu.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(a.x), "=r"(a.y), "=r"(a.z), "=r"(a.w) : "l"(&sl) : "memory");
+  asm volatile("ld.relaxed.gpu.global.v2.u32 {%0, %1}, [%2];"
+               : "=r"(b.x), "=r"(b.y) : "l"(reinterpret_cast<const uint8_t *>(&sl) + 16) : "memory");
+  SlotHead hd;
+  hd.job = a.x; hd.iter = a.y;
+  hd.seq = ((uint64_t)a.w << 32) | a.z;
+  hd.lseq = ((uint64_t)b.y << 32) | b.x;
+  return hd;
+}
+
+__device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, const SlotHead &sl,
                             TileDesc &td, uint32_t h) {
   td.payload = payload;
   const uint32_t slot = payload >> 26, stage = (payload >> 21) & 31u, tile = payload & ((1u << 21) - 1);
@@ -582,6 +601,7 @@ __device__ __forceinline__ void release_desc(WorkerSmem &W, uint32_t d, uint32_t
 
 __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint32_t h) {
   uint32_t d = 0, d_phase = 0;
+  uint32_t cached_job = NONE32;               // dense index of the DevJob in W.job_cache
   for (;;) {
     TileDesc &td = W.desc[d];
     uint32_t payload = TASK_EXIT;
@@ -621,13 +641,17 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint
       }
       break;
     }
-    const Slot &sl = P.slots[payload >> 26];
-    const uint32_t j = *(volatile const uint32_t *)&sl.job;
-    const uint32_t *src = reinterpret_cast<const uint32_t *>(P.jobs + j);
-    for (uint32_t x = lane; x < sizeof(DevJob) / 4; x += 32) W.job_cache[x] = src[x];
+    SlotHead head;
+    if (lane == 0) head = load_slot_head(P.slots[payload >> 26]);
+    const uint32_t j = __shfl_sync(0xffffffffu, head.job, 0);
+    if (j != cached_job) {            // descriptors are static while a job has tasks in flight
+      const uint32_t *src = reinterpret_cast<const uint32_t *>(P.jobs + j);
+      for (uint32_t x = lane; x < sizeof(DevJob) / 4; x += 32) W.job_cache[x] = src[x];
+      cached_job = j;
+    }
     __syncwarp();
     if (lane == 0) {
-      decode_task(P, payload, *reinterpret_cast<const DevJob *>(W.job_cache), sl, td, h);
+      decode_task(P, payload, *reinterpret_cast<const DevJob *>(W.job_cache), head, td, h);
       td.t_claim = t_claim;
     }
     __syncwarp();
@@ -907,7 +931,9 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
     uint32_t pub = 0, ps = 0, pst = 0, pn = 0;
     unsigned long long pb = 0;
     if (lane == 0) {
-      __threadfence();
+      // The epilogue's stores happen-before this thread's acq_rel stage-counter
+      // atomic (CTA-scope mbarrier handoff after a named barrier); its release
+      // at gpu scope is cumulative over them, so no separate fence is needed.
       if ((P.flags & SALUS_FLAG_TRACE) && td.valid) {
         const unsigned long long i = atomicAdd(&P.ctrl->n_trace, 1ull);
         if (i < P.trace_cap) {
