@@ -634,6 +634,20 @@ def main():
         }
         for k in SIDE_SECTIONS:
             line[SIDE_SECTIONS[k][0]] = side_section(k, S, local, jobs, cap)
+        # the paper's figures (2x P100, TF 1.5, private traces) beside ours: context only
+        try:
+            line["paper_context"] = {
+                "avg_jct_fifo_over_srtf": {"ours_c4": line["c4_jct"]["fifo_over_srtf_avg_jct"], "paper": 3.19},
+                "sweep_fifo_over_salus": {"ours_c2a_physical_makespan":
+                                          line["jct_physical"]["fifo_over_pack_makespan"],
+                                          "paper_makespan": "2.38 (superres_128) / 1.07 (resnet50_50)"},
+                "inference_models_on_one_gpu": {"ours_c3": line["c3_switch"]["models_coresident"],
+                                                "ours_switch_from_ready_p99_us":
+                                                    line["c3_switch"]["switch_from_ready_us"]["p99"],
+                                                "paper": "42 (42x consolidation)"},
+                "paper_hardware": "2x Tesla P100 16 GB, TensorFlow 1.5, fp32 (P:594-597)"}
+        except Exception as exc:  # noqa: BLE001
+            line["paper_context"] = {"error": str(exc)[:200]}
         if not args.no_cpu_baseline and world == 1:
             line["cpu_baseline"] = cpu_baseline(jobs, cap)
         print(json.dumps(line), flush=True)
