@@ -274,6 +274,16 @@ int salus_submit_live(salus_ctx *ctx, const salus_job *job);
 int salus_end_submissions(salus_ctx *ctx);
 int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats);
 
+/* Streaming statistics: while a salus_run_async is in
+ * flight, copy the per-job records as they stand (host `stats`, submit
+ * order, like salus_run) over a private non-blocking stream, concurrently
+ * with the running kernel.  *n_done (may be NULL) = jobs whose last
+ * iteration has physically completed (wall_end_ns != 0); their records are
+ * final.  Records of unfinished jobs are partial (-1 / 0 where not yet set).
+ * Errors: E_STATE (nothing running), E_CUDA. */
+int salus_poll_stats(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats,
+                     uint64_t *n_done);
+
 /* Whole-run counters of the last salus_run. */
 typedef struct {
   uint64_t n_dispatch;        /* iterations executed                              */

@@ -687,6 +687,36 @@ int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64
   return SALUS_OK;
 }
 
+int salus_poll_stats(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats,
+                     uint64_t *n_done) {
+  if (!ctx) return SALUS_E_INVAL;
+  if (!ctx->running) return fail(ctx, SALUS_E_STATE, "no run in flight (salus_run_async first)");
+  cudaError_t e = cudaSetDevice(ctx->cfg.device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  if (!ctx->side && (e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)))
+    return cuda_fail(ctx, e, "side stream");
+  uint32_t n;
+  {
+    std::lock_guard<std::mutex> g(ctx->live_mu);     // live submissions grow the table
+    n = (uint32_t)ctx->jobs.size();
+  }
+  std::vector<salus_job_stat> dense(n);
+  if (n && ((e = cudaMemcpyAsync(dense.data(), ctx->meta + ctx->off_stats, sizeof(salus_job_stat) * n,
+                                 cudaMemcpyDeviceToHost, ctx->side)) ||
+            (e = cudaStreamSynchronize(ctx->side))))
+    return cuda_fail(ctx, e, "poll stats");
+  uint64_t done = 0;
+  for (uint32_t d = 0; d < n; d++) done += dense[d].wall_end_ns != 0;
+  if (n_done) *n_done = done;
+  const uint64_t k = stats ? std::min<uint64_t>(max_stats, n) : 0;
+  for (uint32_t d = 0; d < n && stats; d++) {
+    const uint32_t s = d < ctx->dense_to_submit.size() ? ctx->dense_to_submit[d] : d;
+    if (s < k) stats[s] = dense[d];
+  }
+  if (n_stats) *n_stats = k;
+  return SALUS_OK;
+}
+
 int salus_read_run_stats(const salus_ctx *ctx, salus_run_stats *out) {
   if (!ctx || !out) return SALUS_E_INVAL;
   if (!ctx->ran) return SALUS_E_STATE;

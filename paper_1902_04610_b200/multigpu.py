@@ -70,3 +70,17 @@ def partition_jobs(jobs: Iterable, world: int, rank: int, placement: str = "mod"
             mine.append(j)
         heapq.heappush(heap, (w + j.n_iters * j.iter_ticks, r))
     return sorted(mine, key=lambda j: (j.arrival_tick, j.job_id))
+
+
+def progress(ctx, world: int, device=None):
+    """Streaming stats across GPUs (NEXT-4): jobs physically finished on all
+    ranks so far, while every rank's salus_run_async is in flight -- each
+    rank polls its own instance (salus_poll_stats) and one all_reduce sums
+    the counts.  Collective: every rank must call it the same number of times."""
+    import torch
+    import torch.distributed as dist
+    _, done = ctx.poll_stats()
+    t = torch.tensor([done], dtype=torch.int64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return int(t.item())

@@ -78,7 +78,7 @@ EXPORTS = ["salus_open", "salus_job_footprint", "salus_submit_job", "salus_meta_
            "salus_prepare", "salus_run", "salus_read_run_stats", "salus_read_log",
            "salus_read_wall", "salus_read_trace", "salus_read_layers", "salus_last_error", "salus_close",
            "salus_run_async", "salus_submit_live", "salus_end_submissions", "salus_wait",
-           "salus_swap_bytes", "salus_set_swap"]
+           "salus_swap_bytes", "salus_set_swap", "salus_poll_stats"]
 
 _lib = None
 
@@ -113,6 +113,8 @@ def lib():
         L.salus_wait.argtypes = [P, C.POINTER(JobStat), C.c_uint64, C.POINTER(C.c_uint64)]
         L.salus_swap_bytes.argtypes = [P, C.POINTER(C.c_uint64)]
         L.salus_set_swap.argtypes = [P, P, C.c_uint64]
+        L.salus_poll_stats.argtypes = [P, C.POINTER(JobStat), C.c_uint64, C.POINTER(C.c_uint64),
+                                       C.POINTER(C.c_uint64)]
         for name in EXPORTS:
             if name != "salus_last_error":
                 getattr(L, name).restype = C.c_int
@@ -246,6 +248,16 @@ class Context:
     def wait(self) -> Dict[int, dict]:
         """Wait for the run to finish; returns {job_id: stat dict}."""
         return self._stats(self.L.salus_wait, "wait")
+
+    def poll_stats(self):
+        """Streaming stats (NEXT-4) while run_async is in flight:
+        ({job_id: stat dict as it stands}, number of jobs physically done)."""
+        n = max(1, len(self.jobs))
+        arr = (JobStat * n)()
+        cnt, done = C.c_uint64(), C.c_uint64()
+        self._check(self.L.salus_poll_stats(self.ctx, arr, n, C.byref(cnt), C.byref(done)), "poll_stats")
+        return ({s.job_id: {k: getattr(s, k) for k, _ in JobStat._fields_} for s in arr[:cnt.value]},
+                int(done.value))
 
     def run_stats(self) -> dict:
         rs = RunStats()

@@ -137,3 +137,37 @@ def test_live_submission_errors():
         assert sorted(stats) == [5, 7]
     finally:
         ctx.close()
+
+
+def test_poll_stats_streams_completions():
+    """NEXT-4 streaming stats: while the kernel runs, salus_poll_stats sees
+    jobs finish one by one (monotone done count, partial progress observed),
+    and every record it reports as done equals salus_wait's final record."""
+    import time
+    from paper_1902_04610_b200 import build, salus as S
+    from workloads import TRAIN, make_job
+    build.build()
+    jobs = [make_job(k, TRAIN, 0, (1024, 1024, 1024), 256, 30 + 10 * k, lr=1e-3, seed=k) for k in range(24)]
+    ctx = S.Context(jobs, 1 << 28, S.SRTF, log=False)      # one lane: jobs finish one after another
+    try:
+        ctx.run_async()
+        seen, last, snaps = [], -1, []
+        t0 = time.time()
+        while time.time() - t0 < 60:
+            st, done = ctx.poll_stats()
+            assert done >= last
+            last = done
+            seen.append(done)
+            snaps.append(st)
+            if done == len(jobs):
+                break
+            time.sleep(0.0005)
+        final = ctx.wait()
+    finally:
+        ctx.close()
+    assert last == len(jobs)
+    assert any(0 < d < len(jobs) for d in seen), seen[:20]
+    for st in snaps:
+        for jid, s in st.items():
+            if s["wall_end_ns"]:
+                assert s == final[jid], jid

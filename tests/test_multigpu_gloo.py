@@ -40,6 +40,40 @@ def _worker(rank, world, port, out):
         dist.destroy_process_group()
 
 
+class _FakeCtx:
+    def __init__(self, done):
+        self.done = done
+
+    def poll_stats(self):
+        return {}, self.done
+
+
+def _progress_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        out[rank] = [MG.progress(_FakeCtx(3 * k + rank), world) for k in range(3)]
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world2_streaming_progress():
+    """NEXT-4 streaming stats: per-rank done counts summed across ranks."""
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as m:
+        out = m.dict()
+        procs = [ctx.Process(target=_progress_worker, args=(r, world, port, out)) for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(120)
+            assert p.exitcode == 0
+        got = [list(out[r]) for r in range(world)]
+    assert got[0] == got[1] == [1, 7, 13]
+
+
 def test_partition_is_exact_cover():
     jobs, cap = c4_trace(n_jobs=61, seed=9)
     parts = [MG.partition_jobs(jobs, 4, r) for r in range(4)]
