@@ -87,7 +87,13 @@ enum {
 /* salus_job.dump */
 enum {
   SALUS_DUMP_OUTPUTS = 1,    /* keep fp32 A_L of every iteration / request       */
-  SALUS_DUMP_WEIGHTS = 2     /* keep fp32 master weights after the last iteration */
+  SALUS_DUMP_WEIGHTS = 2,    /* keep fp32 master weights after the last iteration */
+  SALUS_DUMP_STATE = 4       /* migration: when the job
+                                finishes, the kernel copies its persistent device
+                                state (the opaque image salus_read_state returns)
+                                to its region of the swap area; another context,
+                                e.g. on another GPU, resumes it from that image
+                                (salus_job.resume_state)                          */
 };
 
 /* ---------------------------------------------------------------------
@@ -194,6 +200,17 @@ typedef struct {
   uint64_t seed;             /* data generator seed (A29)                          */
   const int64_t *request_ticks; /* host; INFER: n_iters non-decreasing ticks
                                    >= arrival_tick; copied at submit              */
+  /* Migration (NEXT-4): resume a job another context ran for resume_iter
+   * iterations.  resume_state (host, copied at submit) is the image that
+   * context's salus_read_state returned for a job of identical kind, dims and
+   * batch (resume_bytes must equal it); it replaces the weight
+   * initialisation, and this context's iteration k is the job's iteration
+   * resume_iter + k (data generation, A29).  NULL = a fresh job.  Needs a
+   * swap area (salus_set_swap). */
+  const void *resume_state;
+  uint64_t resume_bytes;
+  uint32_t resume_iter;
+  uint32_t _reserved;
 } salus_job;
 
 /* Footprint of a job in the device layout, so a
@@ -211,19 +228,27 @@ int salus_submit_job(salus_ctx *ctx, const salus_job *job);
  * dump area.  Valid after the last submit. */
 int salus_meta_bytes(const salus_ctx *ctx, uint64_t *bytes);
 
-/* SALUS_FLAG_EVICT: bytes of pinned host memory
- * the swap area needs -- one fixed region per job, the size of its
- * persistent device backing (salus_job_footprint), 0 without the flag.
+/* Bytes of pinned host memory the swap area needs -- one fixed region per
+ * job, the size of its persistent device backing (salus_job_footprint) --
+ * when the context uses one: SALUS_FLAG_EVICT, or
+ * a job with SALUS_DUMP_STATE or resume_state (migration, NEXT-4); else 0.
  * Valid after the last submit. */
 int salus_swap_bytes(const salus_ctx *ctx, uint64_t *bytes);
 
 /* Bind the caller-owned swap area: page-locked host memory (cudaHostAlloc /
  * torch pin_memory; with unified addressing the kernel reads and writes it
  * directly), >= salus_swap_bytes, 256-byte aligned, outliving the context.
- * Before salus_prepare.  Errors: E_STATE (after prepare, or no EVICT flag),
+ * Before salus_prepare.  Errors: E_STATE (after prepare, or no swap area needed),
  * E_INVAL (alignment / not device-accessible), E_CAPACITY (too small).
  * salus_prepare fails with E_STATE if EVICT needs a swap area and none was set. */
 int salus_set_swap(salus_ctx *ctx, void *host, uint64_t bytes);
+
+/* Migration (NEXT-4): after a run, copy the persistent state image of a job
+ * submitted with SALUS_DUMP_STATE (as it stood when its last iteration
+ * ended) into buf (host); *n = bytes (the job's persistent backing; pass
+ * buf = NULL to query).  Errors: E_STATE (no run yet), E_INVAL (unknown job,
+ * no SALUS_DUMP_STATE), E_CAPACITY (cap_bytes too small). */
+int salus_read_state(salus_ctx *ctx, uint32_t job_id, void *buf, uint64_t cap_bytes, uint64_t *n);
 
 /* Bind the caller-owned device buffer `meta` (>= salus_meta_bytes, 256-byte
  * aligned) and upload the job tables on cfg.stream (host->device copies).

@@ -60,7 +60,7 @@ __device__ __forceinline__ bool take_next(Slot &sl, DispRec *rec) {
 // stage (INIT before a job's first iteration, else GEN; the copy stage of a
 // swap record); the caller enqueues that stage's tiles after this returns
 // (the fence orders these writes first).
-__device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec) {
+__device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec, const DevJob *jobs) {
   sl.job = rec.job;
   sl.iter = rec.iter;
   sl.seq = rec.seq;
@@ -75,7 +75,9 @@ __device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec
   __threadfence();
   if (rec.kind == REC_SWAP_OUT) return STAGE_SWAP_OUT;
   if (rec.kind == REC_SWAP_IN) return STAGE_SWAP_IN;
-  return rec.iter == 0 ? 0u : 1u;
+  // a job's first iteration initialises its weights -- unless it resumes a
+  // migrated state (NEXT-4), whose swap-in record already put them in place
+  return (rec.iter == 0 && !(jobs[rec.job].dump & DUMP_INTERNAL_RESUME)) ? 0u : 1u;
 }
 
 }  // namespace salus

@@ -46,7 +46,12 @@ struct alignas(128) DevJob {   // whole cache lines: a live job's descriptor nev
   uint32_t act_off[MAX_LAYERS + 1], g_off[2];
   uint32_t n_stages;                      // stages of a non-first iteration path
   uint32_t stage_tiles[MAX_STAGES];       // tiles per stage
+  uint32_t iter_base;                     // migration (NEXT-4): global index of local iteration 0
 };
+
+// DevJob.dump bit set by the host: the job resumes from a state image
+// (its first iteration copies the image in instead of initialising weights)
+constexpr uint32_t DUMP_INTERNAL_RESUME = 1u << 31;
 
 // Run-ahead execution (A30 mode 2): the scheduler appends dispatch records to
 // a per-slot ring; the thread that completes an iteration starts the slot's

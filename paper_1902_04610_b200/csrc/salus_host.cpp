@@ -60,6 +60,7 @@ Footprint footprint(const salus_job &j) {
 struct HostJob {
   salus_job j;
   std::vector<int64_t> req;
+  std::vector<uint8_t> resume;        // migration: the persistent image to resume from
   Footprint fp;
   uint32_t submit_idx;
 };
@@ -86,8 +87,9 @@ struct salus_ctx {
   uint64_t off_ctrl = 0, off_jobs = 0, off_req = 0, off_inf = 0, off_ppt = 0, off_lpt = 0, off_free = 0,
            off_slots = 0, off_ring = 0, off_fslot = 0, off_fseq = 0, off_pend = 0, off_log = 0, off_wall = 0, off_stats = 0, off_dump = 0, off_trace = 0,
            off_swfence = 0, off_evl = 0, total = 0;
-  // SALUS_FLAG_EVICT (A35): caller-owned pinned host swap area
-  uint8_t *swap_dev = nullptr;
+  // caller-owned pinned host swap area: SALUS_FLAG_EVICT (A35) and migration
+  // (SALUS_DUMP_STATE / resume_state, NEXT-4); job j's region at pt_off pages
+  uint8_t *swap_dev = nullptr, *swap_host = nullptr;
   uint64_t swap_set_bytes = 0;
   uint64_t trace_cap = 0, n_trace = 0, h2d_bytes = 0;
   uint32_t lpt_stride = 0;
@@ -148,6 +150,17 @@ int validate_job(const salus_job *j, bool null_work, std::string *why) {
   Footprint f = footprint(*j);
   if (!null_work && (j->persistent_bytes < f.p || j->ephemeral_bytes < f.e)) {
     *why = "declared persistent/ephemeral bytes below the device footprint (salus_job_footprint)";
+    return SALUS_E_INVAL;
+  }
+  if (j->resume_state) {                 // migration: an image of this very layout
+    const uint64_t img = (f.p + PAGE_BYTES - 1) / PAGE_BYTES * PAGE_BYTES;
+    if (j->resume_bytes != img || null_work) {
+      *why = "resume_bytes must equal the job's persistent backing (salus_read_state), real work only";
+      return SALUS_E_INVAL;
+    }
+    if ((uint64_t)j->resume_iter + j->n_iters > 0xFFFFu) { *why = "resume_iter + n_iters must be < 65536"; return SALUS_E_INVAL; }
+  } else if (j->resume_iter) {
+    *why = "resume_iter without resume_state";
     return SALUS_E_INVAL;
   }
   return SALUS_OK;
@@ -211,6 +224,11 @@ int salus_submit_job(salus_ctx *ctx, const salus_job *job) {
   h.j = *job;
   if (job->kind == SALUS_INFER) h.req.assign(job->request_ticks, job->request_ticks + job->n_iters);
   h.j.request_ticks = nullptr;
+  if (job->resume_state) {
+    const uint8_t *r = static_cast<const uint8_t *>(job->resume_state);
+    h.resume.assign(r, r + job->resume_bytes);
+  }
+  h.j.resume_state = nullptr;
   h.fp = footprint(*job);
   h.submit_idx = (uint32_t)ctx->jobs.size();
   ctx->dump_floats += df;
@@ -238,7 +256,8 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
       D.dims[l] = l <= L ? j.dims[l] : 0;
       D.dpad[l] = l <= L ? (uint32_t)pad128(j.dims[l]) : 0;
     }
-    D.lr = j.lr; D.dump = j.dump; D.seed = j.seed;
+    D.lr = j.lr; D.dump = j.dump | (h.resume.empty() ? 0u : DUMP_INTERNAL_RESUME); D.seed = j.seed;
+    D.iter_base = j.resume_iter;
     D.req_off = (uint32_t)req_total;
     if (j.kind == SALUS_INFER) req_total += j.n_iters;
     D.pt_off = (uint32_t)ppt_total;
@@ -376,18 +395,25 @@ int salus_meta_bytes(const salus_ctx *ctx, uint64_t *bytes) {
   return SALUS_OK;
 }
 
+static bool needs_swap(const salus_ctx *ctx) {
+  if (ctx->cfg.flags & SALUS_FLAG_EVICT) return true;
+  for (const HostJob &h : ctx->jobs)
+    if ((h.j.dump & SALUS_DUMP_STATE) || !h.resume.empty()) return true;
+  return false;
+}
+
 int salus_swap_bytes(const salus_ctx *ctx, uint64_t *bytes) {
   if (!ctx || !bytes) return SALUS_E_INVAL;
   compute_layout(const_cast<salus_ctx *>(ctx));
   // job j's region: its persistent backing pages, at pt_off pages (dense order)
-  *bytes = (ctx->cfg.flags & SALUS_FLAG_EVICT) ? ctx->ppt_used * ctx->cfg.page_bytes : 0;
+  *bytes = needs_swap(ctx) ? ctx->ppt_used * ctx->cfg.page_bytes : 0;
   return SALUS_OK;
 }
 
 int salus_set_swap(salus_ctx *ctx, void *host, uint64_t bytes) {
   if (!ctx) return SALUS_E_INVAL;
   if (ctx->state != 0) return fail(ctx, SALUS_E_STATE, "salus_set_swap after salus_prepare");
-  if (!(ctx->cfg.flags & SALUS_FLAG_EVICT)) return fail(ctx, SALUS_E_STATE, "no SALUS_FLAG_EVICT");
+  if (!needs_swap(ctx)) return fail(ctx, SALUS_E_STATE, "no swap area needed (no EVICT flag, DUMP_STATE or resume)");
   if (!host || (reinterpret_cast<uintptr_t>(host) & 255)) return fail(ctx, SALUS_E_INVAL, "swap must be 256-B aligned");
   uint64_t need = 0;
   salus_swap_bytes(ctx, &need);
@@ -400,6 +426,7 @@ int salus_set_swap(salus_ctx *ctx, void *host, uint64_t bytes) {
     return fail(ctx, SALUS_E_INVAL, "swap area is not page-locked host memory the device can access");
   }
   ctx->swap_dev = static_cast<uint8_t *>(dev);
+  ctx->swap_host = static_cast<uint8_t *>(host);
   ctx->swap_set_bytes = bytes;
   return SALUS_OK;
 }
@@ -412,9 +439,9 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   compute_layout(ctx);
   if (!meta || (reinterpret_cast<uintptr_t>(meta) & 255)) return fail(ctx, SALUS_E_INVAL, "meta must be 256-B aligned");
   if (meta_bytes < ctx->total) return fail(ctx, SALUS_E_CAPACITY, "meta buffer too small");
-  if ((ctx->cfg.flags & SALUS_FLAG_EVICT) && ctx->ppt_used &&
+  if (needs_swap(ctx) && ctx->ppt_used &&
       (!ctx->swap_dev || ctx->swap_set_bytes < ctx->ppt_used * ctx->cfg.page_bytes))
-    return fail(ctx, SALUS_E_STATE, "SALUS_FLAG_EVICT needs salus_set_swap (>= salus_swap_bytes) first");
+    return fail(ctx, SALUS_E_STATE, "SALUS_FLAG_EVICT / DUMP_STATE / resume need salus_set_swap (>= salus_swap_bytes) first");
   cudaError_t e = cudaSetDevice(ctx->cfg.device);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
   int grid = 0;
@@ -542,6 +569,14 @@ int salus_run_async(salus_ctx *ctx) {
       (e = cudaMemsetAsync(m + ctx->off_pend, 0, 8ull * MAX_LANES * MAX_LANES, st)))
     return cuda_fail(ctx, e, "reset");
   *reinterpret_cast<volatile uint32_t *>(ctx->host_abort) = 0;
+  // migration: every run starts from the resume images (a DUMP_STATE job's
+  // region is overwritten with its final state by the previous run)
+  for (uint32_t d = 0; d < (uint32_t)ctx->djobs.size() && d < ctx->n_pre; d++) {
+    const HostJob &h = ctx->jobs[ctx->dense_to_submit[d]];
+    if (!h.resume.empty())
+      std::memcpy(ctx->swap_host + (uint64_t)ctx->djobs[d].pt_off * ctx->cfg.page_bytes, h.resume.data(),
+                  h.resume.size());
+  }
   if ((e = cudaEventRecord(ctx->ev0, st))) return cuda_fail(ctx, e, "event");
   if (ctx->live) {
     std::lock_guard<std::mutex> g(ctx->live_mu);
@@ -584,6 +619,8 @@ int salus_submit_live(salus_ctx *ctx, const salus_job *job) {
   if (!ctx->running || ctx->ended) return fail(ctx, SALUS_E_STATE, "no live run accepting submissions");
   if (ctx->id_to_submit.count(job->job_id)) return fail(ctx, SALUS_E_DUPLICATE, "duplicate job id");
   if (job->kind != SALUS_TRAIN) return fail(ctx, SALUS_E_INVAL, "live submission takes TRAIN jobs");
+  if (job->resume_state || (job->dump & SALUS_DUMP_STATE))
+    return fail(ctx, SALUS_E_INVAL, "migration state (resume / DUMP_STATE) is for jobs submitted before the run");
   if (!ctx->jobs.empty() && job->job_id <= ctx->max_id)
     return fail(ctx, SALUS_E_INVAL, "live job ids must increase");
   std::string why;
@@ -714,6 +751,21 @@ int salus_poll_stats(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, 
     if (s < k) stats[s] = dense[d];
   }
   if (n_stats) *n_stats = k;
+  return SALUS_OK;
+}
+
+int salus_read_state(salus_ctx *ctx, uint32_t job_id, void *buf, uint64_t cap_bytes, uint64_t *n) {
+  if (!ctx || !n) return SALUS_E_INVAL;
+  if (!ctx->ran) return fail(ctx, SALUS_E_STATE, "no run yet");
+  auto it = ctx->id_to_dense.find(job_id);
+  if (it == ctx->id_to_dense.end()) return fail(ctx, SALUS_E_INVAL, "unknown job");
+  const DevJob &D = ctx->djobs[it->second];
+  if (!(D.dump & SALUS_DUMP_STATE)) return fail(ctx, SALUS_E_INVAL, "job was not submitted with SALUS_DUMP_STATE");
+  const uint64_t bytes = (uint64_t)D.ap_pages * ctx->cfg.page_bytes;
+  *n = bytes;
+  if (!buf) return SALUS_OK;
+  if (cap_bytes < bytes) return fail(ctx, SALUS_E_CAPACITY, "buffer too small");
+  std::memcpy(buf, ctx->swap_host + (uint64_t)D.pt_off * ctx->cfg.page_bytes, bytes);
   return SALUS_OK;
 }
 

@@ -408,8 +408,16 @@ struct Sched {
         remove_adm(j);
         // completion_seq = seq of the final iteration = the lane's in-flight one
         emit(SALUS_REC_JOB_FINISH, S.lane_id[i], S.id[j], S.n[j], S.lane_seq[i]);
-        push_pages(job_table(j), S.ap[j], slot, S.lane_pseq[i]);
-        if (lane_left(i, j, S.lane_pseq[i])) continue;
+        uint64_t fseq = S.lane_pseq[i];
+        if (physical && S.ap[j] > 0 && (P.jobs[j].dump & SALUS_DUMP_STATE)) {
+          // migration (NEXT-4): copy the final persistent state to the job's
+          // swap region behind its last iteration; its pages wait for the copy
+          append(slot, S.lane_id[i], j, REC_SWAP_OUT);
+          if (err) return;
+          fseq = S.last_app[slot] - 1;
+        }
+        push_pages(job_table(j), S.ap[j], slot, fseq);
+        if (lane_left(i, j, fseq)) continue;
       }
       i++;
     }
@@ -606,8 +614,10 @@ struct Sched {
     an++; sumP += S.p[j];
     __syncwarp();
     emit(restored ? SALUS_REC_JOB_RESTORE : SALUS_REC_JOB_ADMIT, S.lane_id[li], S.id[j], S.p[j], S.e[j]);
-    // the copy back precedes the job's next iteration in the slot's ring
-    if (restored && physical && S.ap[j] > 0) append(slot, S.lane_id[li], j, REC_SWAP_IN);
+    // the copy back precedes the job's next iteration in the slot's ring; a
+    // migrated job (NEXT-4) is copied in before its first iteration
+    if (physical && S.ap[j] > 0 && (restored || (P.jobs[j].dump & DUMP_INTERNAL_RESUME) && S.done[j] == 0))
+      append(slot, S.lane_id[li], j, REC_SWAP_IN);
   }
 
   // ------------------------------------------------------------ eviction (A35)
@@ -822,7 +832,7 @@ struct Sched {
     if (tid == 0) {
       DispRec r;
       got = take_next(sl, &r);
-      if (got) { first = begin_iteration(sl, r); jj = r.job; }
+      if (got) { first = begin_iteration(sl, r, P.jobs); jj = r.job; }
     }
     got = __shfl_sync(0xffffffffu, got, 0);
     if (!got) return;

@@ -228,13 +228,14 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
                             TileDesc &td, uint32_t h) {
   td.payload = payload;
   const uint32_t slot = payload >> 26, stage = (payload >> 21) & 31u, tile = payload & ((1u << 21) - 1);
-  const uint32_t k = sl.iter;
+  const uint32_t k = sl.iter;                         // this context's iteration index
+  const uint32_t kg = k + J.iter_base;                // the job's own (migration, NEXT-4)
   const uint32_t L = J.n_layers, bp = J.bpad;
   td.slot = slot; td.stage = stage; td.job = sl.job; td.iter = k; td.seq = sl.seq; td.lseq = sl.lseq;
   td.ntiles = stage_ntiles(J, stage);
   td.is_last = stage >= STAGE_SWAP_OUT || stage == last_stage(J.kind, L);
   td.next_ntiles = td.is_last ? 0 : J.stage_tiles[stage + 1];
-  td.first_stage = stage >= STAGE_SWAP_OUT ? stage : k == 0 ? 0u : 1u;
+  td.first_stage = stage >= STAGE_SWAP_OUT ? stage : (k == 0 && !(J.dump & DUMP_INTERNAL_RESUME)) ? 0u : 1u;
   td.dump_off = -1;
   td.n_ech = 0;
   td.xt_mask = 0;
@@ -285,7 +286,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     td.rows_valid = J.batch; td.cols_valid = J.dims[0];
     for (uint32_t q = 0; q < 2; q++)
       defer(td, PTR_OUT + q, lt, J.act_off[0] + (2 * cb + q) * bp * 128u + mb * 16384u);
-    td.key = gen_key(J.seed, J.job_id, GEN_X, 0, k);
+    td.key = gen_key(J.seed, J.job_id, GEN_X, 0, kg);
     return;
   }
   td.kind = T_GEMM;
@@ -296,14 +297,14 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     td.peer_valid = (mb | 1u) < bp / 128;
     td.layer = l; td.N = N; td.nk = J.dpad[l - 1] / 64;
     td.a = OpDesc{lt, J.act_off[l - 1], bp, mb * 128, 0};
-    td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * N + h * (N / 2), 0};
+    td.b = OpDesc{jt, J.wb_off[l - 1][kg & 1], J.dpad[l], nb * N + h * (N / 2), 0};
     td.m0 = mb * 128; td.n0 = nb * N;
     td.rows_valid = J.batch; td.cols_valid = J.dims[l]; td.ld_logical = J.dims[l];
     uint32_t out_off;
     if (l < L) { td.epi = EPI_RELU; out_off = J.act_off[l]; }
     else if (J.kind == SALUS_TRAIN) {
       td.epi = EPI_LOSS; out_off = J.g_off[0];
-      td.key = gen_key(J.seed, J.job_id, GEN_T, L, k);
+      td.key = gen_key(J.seed, J.job_id, GEN_T, L, kg);
     } else { td.epi = EPI_OUT; out_off = J.act_off[L]; }
     if (td.valid) {
       if (l == L && (J.dump & SALUS_DUMP_OUTPUTS))
@@ -334,7 +335,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
         for (uint32_t q = 0; q < N / 128; q++) defer(td, PTR_W32 + q, jt, w32 + q * 65536u);
         td.n_ech = N / 64;
         for (uint32_t q = 0; q < N / 64; q++)
-          defer(td, PTR_AUX + q, jt, J.wb_off[l - 1][(k + 1) & 1] + (td.n0 / 64 + q) * J.dpad[l] * 128u + mb * 16384u);
+          defer(td, PTR_AUX + q, jt, J.wb_off[l - 1][(kg + 1) & 1] + (td.n0 / 64 + q) * J.dpad[l] * 128u + mb * 16384u);
       }
       if (td.valid && (J.dump & SALUS_DUMP_WEIGHTS) && k + 1 == J.n_iters) {
         uint64_t base = J.dump_w_off;
@@ -347,7 +348,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
       td.peer_valid = (mb | 1u) < bp / 128;
       td.epi = EPI_DX; td.nk = J.dpad[l] / 64;
       td.a = OpDesc{lt, gin, bp, mb * 128, 0};
-      td.b = OpDesc{jt, J.wb_off[l - 1][k & 1], J.dpad[l], nb * N + h * (N / 2), 1};
+      td.b = OpDesc{jt, J.wb_off[l - 1][kg & 1], J.dpad[l], nb * N + h * (N / 2), 1};
       td.m0 = mb * 128; td.n0 = nb * N;
       td.rows_valid = J.batch; td.cols_valid = J.dims[l - 1];
       if (td.valid) {
@@ -971,7 +972,7 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
           // run-ahead: start the slot's next queued iteration right here
           DispRec rec;
           if (take_next(sl, &rec)) {
-            pst = begin_iteration(sl, rec);
+            pst = begin_iteration(sl, rec, P.jobs);
             pub = 1; ps = td.slot; pn = stage_ntiles(P.jobs[rec.job], pst);
             pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)pn);
           }

@@ -20,7 +20,7 @@ LIB_PATH = os.environ.get("SALUS_LIB", os.path.join(HERE, "libsalus.so"))
 FIFO, SRTF, PACK, FAIR = 0, 1, 2, 3
 TRAIN, INFER = 0, 1
 FLAG_LOG, FLAG_NULL_WORK, FLAG_CHECK, FLAG_TRACE, FLAG_ONLINE, FLAG_EVICT = 1, 2, 4, 8, 16, 32
-DUMP_OUTPUTS, DUMP_WEIGHTS = 1, 2
+DUMP_OUTPUTS, DUMP_WEIGHTS, DUMP_STATE = 1, 2, 4
 WEIGHTS = 0xFFFFFFFF
 
 ERRORS = {-1: "E_INVAL", -2: "E_DUPLICATE", -3: "E_UNSCHEDULABLE", -4: "E_STATE",
@@ -47,7 +47,9 @@ class JobDesc(C.Structure):
                 ("persistent_bytes", C.c_uint64), ("ephemeral_bytes", C.c_uint64),
                 ("n_iters", C.c_uint32), ("n_layers", C.c_uint32), ("iter_ticks", C.c_uint64),
                 ("dims", C.c_uint32 * 9), ("batch", C.c_uint32), ("lr", C.c_float),
-                ("dump", C.c_uint32), ("seed", C.c_uint64), ("request_ticks", C.POINTER(C.c_int64))]
+                ("dump", C.c_uint32), ("seed", C.c_uint64), ("request_ticks", C.POINTER(C.c_int64)),
+                ("resume_state", C.c_void_p), ("resume_bytes", C.c_uint64), ("resume_iter", C.c_uint32),
+                ("_reserved", C.c_uint32)]
 
 
 class JobStat(C.Structure):
@@ -78,7 +80,7 @@ EXPORTS = ["salus_open", "salus_job_footprint", "salus_submit_job", "salus_meta_
            "salus_prepare", "salus_run", "salus_read_run_stats", "salus_read_log",
            "salus_read_wall", "salus_read_trace", "salus_read_layers", "salus_last_error", "salus_close",
            "salus_run_async", "salus_submit_live", "salus_end_submissions", "salus_wait",
-           "salus_swap_bytes", "salus_set_swap", "salus_poll_stats"]
+           "salus_swap_bytes", "salus_set_swap", "salus_poll_stats", "salus_read_state"]
 
 _lib = None
 
@@ -113,6 +115,7 @@ def lib():
         L.salus_wait.argtypes = [P, C.POINTER(JobStat), C.c_uint64, C.POINTER(C.c_uint64)]
         L.salus_swap_bytes.argtypes = [P, C.POINTER(C.c_uint64)]
         L.salus_set_swap.argtypes = [P, P, C.c_uint64]
+        L.salus_read_state.argtypes = [P, C.c_uint32, P, C.c_uint64, C.POINTER(C.c_uint64)]
         L.salus_poll_stats.argtypes = [P, C.POINTER(JobStat), C.c_uint64, C.POINTER(C.c_uint64),
                                        C.POINTER(C.c_uint64)]
         for name in EXPORTS:
@@ -122,7 +125,7 @@ def lib():
     return _lib
 
 
-def job_desc(job, dump: int = 0):
+def job_desc(job, dump: int = 0, resume=None):
     """Marshal a workloads.Job-like object into a salus_job; returns (desc, keepalive)."""
     d = JobDesc()
     d.job_id = job.job_id
@@ -143,6 +146,13 @@ def job_desc(job, dump: int = 0):
     if job.kind == INFER:
         keep = (C.c_int64 * len(job.request_ticks))(*job.request_ticks)
         d.request_ticks = C.cast(keep, C.POINTER(C.c_int64))
+    if resume is not None:                       # migration (NEXT-4): (state image, iterations done)
+        img, it = resume
+        img = np.ascontiguousarray(img, dtype=np.uint8)
+        d.resume_state = C.c_void_p(img.ctypes.data)
+        d.resume_bytes = img.nbytes
+        d.resume_iter = int(it)
+        keep = (keep, img)
     return d, keep
 
 
@@ -163,7 +173,7 @@ class Context:
                  check: bool = False, dump: Optional[Dict[int, int]] = None, n_workers: int = 0,
                  timeout_ms: int = 0, page_bytes: int = 65536, trace: bool = False,
                  trace_capacity: int = 0, online: bool = False, max_jobs: int = 0, dump_bytes: int = 0,
-                 evict: bool = False):
+                 evict: bool = False, resume: Optional[Dict[int, tuple]] = None):
         import torch
         self._torch = torch
         self.L = lib()
@@ -195,18 +205,19 @@ class Context:
         self.ctx = C.c_void_p()
         self._check(self.L.salus_open(C.byref(cfg), C.byref(self.ctx)), "open")
         dump = dump or {}
+        resume = resume or {}
         for j in self.jobs:
-            d, keep = job_desc(j, dump.get(j.job_id, 0))
+            d, keep = job_desc(j, dump.get(j.job_id, 0), resume.get(j.job_id))
             self._check(self.L.salus_submit_job(self.ctx, C.byref(d)), f"submit {j.job_id}")
         self.swap = None
-        if evict:                    # A35: caller-owned pinned host swap area
-            sb = C.c_uint64()
-            self._check(self.L.salus_swap_bytes(self.ctx, C.byref(sb)), "swap_bytes")
-            if sb.value:
-                self.swap = torch.empty(sb.value + 256, dtype=torch.uint8, pin_memory=True)
-                base = self.swap.data_ptr()
-                self._check(self.L.salus_set_swap(self.ctx, C.c_void_p((base + 255) // 256 * 256), sb.value),
-                            "set_swap")
+        # caller-owned pinned host swap area: eviction (A35) and migration state (NEXT-4)
+        sb = C.c_uint64()
+        self._check(self.L.salus_swap_bytes(self.ctx, C.byref(sb)), "swap_bytes")
+        if sb.value:
+            self.swap = torch.empty(sb.value + 256, dtype=torch.uint8, pin_memory=True)
+            base = self.swap.data_ptr()
+            self._check(self.L.salus_set_swap(self.ctx, C.c_void_p((base + 255) // 256 * 256), sb.value),
+                        "set_swap")
         mb = C.c_uint64()
         self._check(self.L.salus_meta_bytes(self.ctx, C.byref(mb)), "meta_bytes")
         self.meta = torch.empty(max(256, mb.value), dtype=torch.uint8, device=f"cuda:{device}")
@@ -248,6 +259,16 @@ class Context:
     def wait(self) -> Dict[int, dict]:
         """Wait for the run to finish; returns {job_id: stat dict}."""
         return self._stats(self.L.salus_wait, "wait")
+
+    def read_state(self, job_id: int) -> np.ndarray:
+        """Migration (NEXT-4): the persistent state image of a DUMP_STATE job
+        after the run -- resume it elsewhere with Context(resume={id: (img, iters)})."""
+        n = C.c_uint64()
+        self._check(self.L.salus_read_state(self.ctx, job_id, None, 0, C.byref(n)), "state size")
+        out = np.empty(n.value, dtype=np.uint8)
+        self._check(self.L.salus_read_state(self.ctx, job_id, C.c_void_p(out.ctypes.data), n.value, C.byref(n)),
+                    "state")
+        return out
 
     def poll_stats(self):
         """Streaming stats (NEXT-4) while run_async is in flight:
