@@ -290,6 +290,34 @@ def c4e_evict(S, device):
     return out
 
 
+def sched_rate(S, device):
+    """SURVEY §8(d) C1 row "scheduler ns/event": the device scheduler alone
+    (SALUS_FLAG_NULL_WORK: admission, lanes, pages, dispatch, no tiles) on
+    C2a, C3 and C4, against the CPU oracle's simulation of the same trace
+    (one host core, Python)."""
+    from oracle import scheduler as OS
+    from workloads import c4_trace
+    out = {}
+    for name, (jobs, cap), pol, ml in (("c2a_pack", c2_trace("a"), S.PACK, 0),
+                                       ("c3_fair8", c3_trace(), S.FAIR, 8),
+                                       ("c4_srtf", c4_trace(), S.SRTF, 0)):
+        ctx = S.Context(jobs, cap, pol, device=device, max_lanes=ml, null_work=True, log=False)
+        try:
+            ctx.run()
+            ctx.run()
+            rs = ctx.run_stats()
+        finally:
+            ctx.close()
+        t0 = time.perf_counter()
+        ref = OS.simulate(jobs, cap, pol, max_lanes=ml)
+        t_cpu = time.perf_counter() - t0
+        out[name] = {"ticks": int(rs["n_ticks"]), "dispatches": int(rs["n_dispatch"]),
+                     "device_ns_per_tick": rs["kernel_ns"] / rs["n_ticks"],
+                     "device_ns_per_dispatch": rs["kernel_ns"] / rs["n_dispatch"],
+                     "oracle_ns_per_tick": t_cpu * 1e9 / ref.n_ticks}
+    return out
+
+
 def c2b_tensor(S, device, n_jobs=8, n_iters=20):
     """C2b: the compute-heavy sweep member, MLP [4096]^4
     B=2048 training (AI 683 flop/B, tensor-bound), n_jobs packed into one
@@ -477,6 +505,7 @@ SIDE_SECTIONS = {
     "c4": ("c4_jct", lambda S, d, jobs, cap: c4_jct(S, d)),
     "c2b": ("c2b_tensor", lambda S, d, jobs, cap: c2b_tensor(S, d)),
     "evict": ("c4e_evict", lambda S, d, jobs, cap: c4e_evict(S, d)),
+    "sched": ("scheduler_only", lambda S, d, jobs, cap: sched_rate(S, d)),
     "online": ("online_submission", lambda S, d, jobs, cap: online_submission(S, d)),
 }
 
@@ -499,7 +528,7 @@ def main():
     ap.add_argument("--impl", default="salus", choices=["salus", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--only", default="",
-                    help="comma list of side sections to run alone and print (c1,c2b,c3,c4,evict,jct,online,overhead)")
+                    help="comma list of side sections to run alone and print (c1,c2b,c3,c4,evict,jct,online,overhead,sched)")
     args = ap.parse_args()
     rank, world, local = dist_env()
 
