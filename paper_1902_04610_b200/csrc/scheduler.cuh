@@ -391,9 +391,28 @@ struct Sched {
   }
 
   // P1: iteration completions and JobFinish (A4)
+  // Lanes whose iteration ends at t are found 32 at a time with a ballot and
+  // processed in lane-id order; a deleted lane shifts the later entries down
+  // by one, so original index o sits at o - (lanes deleted before it).
   __device__ void phase_completions() {
-    for (uint32_t i = 0; i < nl;) {
-      if (S.lane_busy[i] != t) { i++; continue; }
+    const uint32_t nl0 = nl;
+    uint32_t removed = 0;
+    for (uint32_t b = 0; b < nl0 && !err; b += 32) {
+      const uint32_t o = b + tid;
+      uint32_t m = __ballot_sync(0xffffffffu, o < nl0 && S.lane_busy[o - removed] == t);
+      while (m) {
+        const uint32_t i = b + (uint32_t)(__ffs(m) - 1) - removed;
+        m &= m - 1;
+        if (complete_lane(i)) removed++;
+        if (err) return;
+      }
+    }
+  }
+
+  // the in-flight iteration of lane index i ended at t; JobFinish if it was
+  // the job's last.  Returns true if the lane was deleted.
+  __device__ bool complete_lane(uint32_t i) {
+    {
       const uint32_t slot = S.lane_slot[i];
       const uint32_t j = S.lane_cur[i];
       if (tid == 0) { S.done[j] += 1; S.svc[j] += S.c[j]; S.lane_busy[i] = IDLE_T; }
@@ -413,14 +432,14 @@ struct Sched {
           // migration (NEXT-4): copy the final persistent state to the job's
           // swap region behind its last iteration; its pages wait for the copy
           append(slot, S.lane_id[i], j, REC_SWAP_OUT);
-          if (err) return;
+          if (err) return false;
           fseq = S.last_app[slot] - 1;
         }
         push_pages(job_table(j), S.ap[j], slot, fseq);
-        if (lane_left(i, j, fseq)) continue;
+        return lane_left(i, j, fseq);
       }
-      i++;
     }
+    return false;
   }
 
   // Job j has left lane index i (JobFinish; eviction, A35): delete
@@ -852,9 +871,9 @@ struct Sched {
     // one pass over the residents: the minimum key of each slot (a lane owns
     // one slot and a job one lane, so dispatching on one lane never changes
     // another lane's minimum)
-    uint32_t idle = 0;
-    for (uint32_t i = 0; i < nl; i++) idle |= (S.lane_busy[i] == IDLE_T) ? 1u : 0u;
-    if (!idle) return;
+    bool idle = false;
+    for (uint32_t i = tid; i < nl; i += 32) idle |= S.lane_busy[i] == IDLE_T;
+    if (!__any_sync(0xffffffffu, idle)) return;
     for (uint32_t i = tid; i < nl; i += 32) S.slot_key[S.lane_slot[i]] = ~0ull;
     __syncwarp();
     for (uint32_t a = tid; a < an; a += 32) {
@@ -870,11 +889,22 @@ struct Sched {
       atomicMin(&S.slot_key[S.jslot[j]], (unsigned long long)key);
     }
     __syncwarp();
-    for (uint32_t i = 0; i < nl; i++) {
-      if (S.lane_busy[i] != IDLE_T) continue;
+    // idle lanes with a runnable resident, 32 at a time, in lane-id order
+    for (uint32_t b = 0; b < nl && !err; b += 32) {
+      const uint32_t k = b + tid;
+      uint32_t m = __ballot_sync(0xffffffffu, k < nl && S.lane_busy[k] == IDLE_T && S.slot_key[S.lane_slot[k]] != ~0ull);
+      while (m && !err) {
+        const uint32_t i = b + (uint32_t)(__ffs(m) - 1);
+        m &= m - 1;
+        dispatch_lane(i);
+      }
+    }
+  }
+
+  __device__ void dispatch_lane(uint32_t i) {
+    {
       const uint32_t slot = S.lane_slot[i];
       const uint64_t best = S.slot_key[slot];
-      if (best == ~0ull) continue;
       const uint32_t j = (uint32_t)(best & ((1u << KEY_BITS) - 1));
       const uint16_t last = S.lane_last[i];
       const int64_t pen = (last != NONE16 && last != j) ? P.switch_ticks : 0;   // A16
