@@ -290,6 +290,33 @@ def c4e_evict(S, device):
     return out
 
 
+def c3_rate_sweep(S, device):
+    """the request-rate sweep {20, 100, 1k, 10k} req/s
+    per model (42 models, PACK: one lane each; FAIR over 8 lanes), every
+    request executed.  Logical request latency (A17 cost model; end of the
+    serving iteration - request tick, from the oracle-identical log) shows
+    where the lanes saturate; requests/s is the device's physical rate."""
+    out = {}
+    for lam in (20, 100, 1000, 10000):
+        jobs, cap = c3_trace(rate_per_s=float(lam))
+        J = {j.job_id: j for j in jobs}
+        for name, pol, ml in (("pack", S.PACK, 0), ("fair8", S.FAIR, 8)):
+            ctx = S.Context(jobs, cap, pol, device=device, max_lanes=ml, log=True)
+            try:
+                ctx.run()
+                rs = ctx.run_stats()
+                log = np.frombuffer(ctx.log_bytes(), dtype=S.LOG_DTYPE)
+            finally:
+                ctx.close()
+            d = log[log["kind"] == 1]
+            lat = np.array([int(r["tick"]) + J[int(r["job"])].iter_ticks - J[int(r["job"])].request_ticks[int(r["a"])]
+                            for r in d], dtype=np.float64) / 1e3
+            out[f"{name}_lambda{lam}"] = {"latency_logical_us": {"avg": float(lat.mean()),
+                                                                 "p99": float(np.percentile(lat, 99))},
+                                          "requests_per_s_device": rs["n_dispatch"] / (rs["kernel_ns"] / 1e9)}
+    return out
+
+
 def sched_rate(S, device):
     """SURVEY §8(d) C1 row "scheduler ns/event": the device scheduler alone
     (SALUS_FLAG_NULL_WORK: admission, lanes, pages, dispatch, no tiles) on
@@ -506,6 +533,7 @@ SIDE_SECTIONS = {
     "c2b": ("c2b_tensor", lambda S, d, jobs, cap: c2b_tensor(S, d)),
     "evict": ("c4e_evict", lambda S, d, jobs, cap: c4e_evict(S, d)),
     "sched": ("scheduler_only", lambda S, d, jobs, cap: sched_rate(S, d)),
+    "c3rate": ("c3_rate_sweep", lambda S, d, jobs, cap: c3_rate_sweep(S, d)),
     "online": ("online_submission", lambda S, d, jobs, cap: online_submission(S, d)),
 }
 
@@ -528,7 +556,7 @@ def main():
     ap.add_argument("--impl", default="salus", choices=["salus", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--only", default="",
-                    help="comma list of side sections to run alone and print (c1,c2b,c3,c4,evict,jct,online,overhead,sched)")
+                    help="comma list of side sections to run alone and print (c1,c2b,c3,c3rate,c4,evict,jct,online,overhead,sched)")
     args = ap.parse_args()
     rank, world, local = dist_env()
 
