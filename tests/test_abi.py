@@ -114,3 +114,55 @@ def test_whole_configs_validate(L):
             keep.append(k)
             assert L.salus_submit_job(ctx, C.byref(d)) == 0, j.job_id
         L.salus_close(ctx)
+
+
+def test_evict_swap_and_migration_validation(L):
+    """NEXT-3 / NEXT-4 entry points, host-side checks only (no GPU):
+    SALUS_FLAG_EVICT is SRTF-only; the swap area is needed exactly when
+    EVICT, DUMP_STATE or a resume image is present; a resume image must have
+    the job's persistent-backing size; poll / read_state need a run."""
+    import numpy as np
+    G = PAGE_BYTES
+    cfg = S.Config()
+    cfg.arena = 1 << 20
+    cfg.capacity_bytes = cfg.arena_bytes = 64 * G
+    cfg.max_jobs = 4
+    ctx = C.c_void_p()
+    for pol in (S.FIFO, S.PACK, S.FAIR):
+        cfg.policy, cfg.flags = pol, S.FLAG_EVICT
+        assert L.salus_open(C.byref(cfg), C.byref(ctx)) == -1
+    cfg.policy, cfg.flags = S.SRTF, S.FLAG_EVICT | S.FLAG_ONLINE
+    assert L.salus_open(C.byref(cfg), C.byref(ctx)) == -1
+
+    # no swap needed: 0 bytes, salus_set_swap refuses
+    rc, ctx = _open(L, cap=64 * G)
+    j = make_job(1, TRAIN, 0, (128, 256, 128), 128, 2, iter_ticks=5)
+    d, _ = S.job_desc(j)
+    assert L.salus_submit_job(ctx, C.byref(d)) == 0
+    n = C.c_uint64(7)
+    assert L.salus_swap_bytes(ctx, C.byref(n)) == 0 and n.value == 0
+    buf = np.zeros(1 << 20, dtype=np.uint8)
+    assert L.salus_set_swap(ctx, C.c_void_p(buf.ctypes.data), buf.nbytes) == -4
+    assert L.salus_poll_stats(ctx, None, 0, None, None) == -4          # nothing running
+    assert L.salus_read_state(ctx, 1, None, 0, C.byref(n)) == -4        # no run yet
+    L.salus_close(ctx)
+
+    # DUMP_STATE: one region = the job's persistent backing (8 pages here)
+    rc, ctx = _open(L, cap=64 * G)
+    d, _ = S.job_desc(j, S.DUMP_STATE)
+    assert L.salus_submit_job(ctx, C.byref(d)) == 0
+    assert L.salus_swap_bytes(ctx, C.byref(n)) == 0 and n.value == 8 * G
+    L.salus_close(ctx)
+
+    # resume: the image must have exactly that size; resume_iter needs an image
+    rc, ctx = _open(L, cap=64 * G)
+    d, keep = S.job_desc(j, 0, (np.zeros(8 * G - 1, dtype=np.uint8), 3))
+    assert L.salus_submit_job(ctx, C.byref(d)) == -1
+    d, keep = S.job_desc(j, 0, (np.zeros(8 * G, dtype=np.uint8), 3))
+    assert L.salus_submit_job(ctx, C.byref(d)) == 0
+    assert L.salus_swap_bytes(ctx, C.byref(n)) == 0 and n.value == 8 * G
+    j2 = make_job(2, TRAIN, 0, (128, 256, 128), 128, 2, iter_ticks=5)
+    d, _ = S.job_desc(j2)
+    d.resume_iter = 4
+    assert L.salus_submit_job(ctx, C.byref(d)) == -1
+    L.salus_close(ctx)
