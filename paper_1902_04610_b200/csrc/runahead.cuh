@@ -71,13 +71,16 @@ __device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec
   sl.start_ns = ~0ull;
   sl.end_ns = 0;
   for (uint32_t k = 0; k < MAX_STAGES + 2; k++) sl.stage_done[k] = 0;
-  if (rec.kind != REC_ITER) { sl.stage_done[STAGE_SWAP_OUT] = 0; sl.stage_done[STAGE_SWAP_IN] = 0; }
+  const uint32_t kind = rec.kind & REC_KIND_MASK;
+  if (kind != REC_ITER) { sl.stage_done[STAGE_SWAP_OUT] = 0; sl.stage_done[STAGE_SWAP_IN] = 0; }
   __threadfence();
-  if (rec.kind == REC_SWAP_OUT) return STAGE_SWAP_OUT;
-  if (rec.kind == REC_SWAP_IN) return STAGE_SWAP_IN;
+  if (kind == REC_SWAP_OUT) return STAGE_SWAP_OUT;
+  if (kind == REC_SWAP_IN) return STAGE_SWAP_IN;
   // a job's first iteration initialises its weights -- unless it resumes a
-  // migrated state (NEXT-4), whose swap-in record already put them in place
-  return (rec.iter == 0 && !(jobs[rec.job].dump & DUMP_INTERNAL_RESUME)) ? 0u : 1u;
+  // migrated state (NEXT-4), whose swap-in record already put them in place;
+  // a GEN-prefetch job's X is already there (stage 1 skipped)
+  if (rec.iter == 0 && !(jobs[rec.job].dump & DUMP_INTERNAL_RESUME)) return 0u;
+  return (rec.kind & REC_FLAG_XPRE) ? 2u : 1u;
 }
 
 }  // namespace salus

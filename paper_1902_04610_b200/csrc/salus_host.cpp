@@ -126,6 +126,24 @@ uint32_t default_max_lanes(uint32_t policy) {
   }
 }
 
+// Persistent backing pages of a job: its footprint, plus two X buffers for
+// the GEN prefetch when the declared P leaves room for them (and the
+// SALUS_XPRE environment variable is not "0"); never more than declared.
+uint32_t backing_pages(const salus_job &j, const Footprint &fp, bool null_work, uint32_t *xpre,
+                       uint64_t *xbytes) {
+  const uint64_t G = PAGE_BYTES;
+  const uint64_t p_pages = (j.persistent_bytes + G - 1) / G;
+  const uint64_t xb = 2ull * pad128(j.batch) * pad128(j.dims[0]);
+  static const bool enabled = [] { const char *e = getenv("SALUS_XPRE"); return !(e && e[0] == '0'); }();
+  *xpre = 0;
+  *xbytes = xb;
+  if (!null_work && enabled && p_pages * G >= fp.p + 2 * xb) {
+    *xpre = 1;
+    return (uint32_t)((fp.p + 2 * xb + G - 1) / G);
+  }
+  return (uint32_t)std::min<uint64_t>((fp.p + G - 1) / G, p_pages);
+}
+
 int validate_job(const salus_job *j, bool null_work, std::string *why) {
   if (j->kind > SALUS_INFER) { *why = "kind"; return SALUS_E_INVAL; }
   if (j->n_layers < 1 || j->n_layers > MAX_LAYERS) { *why = "n_layers must be 1..8"; return SALUS_E_INVAL; }
@@ -153,7 +171,9 @@ int validate_job(const salus_job *j, bool null_work, std::string *why) {
     return SALUS_E_INVAL;
   }
   if (j->resume_state) {                 // migration: an image of this very layout
-    const uint64_t img = (f.p + PAGE_BYTES - 1) / PAGE_BYTES * PAGE_BYTES;
+    uint32_t xpre;
+    uint64_t xb;
+    const uint64_t img = (uint64_t)backing_pages(*j, f, null_work, &xpre, &xb) * PAGE_BYTES;
     if (j->resume_bytes != img || null_work) {
       *why = "resume_bytes must equal the job's persistent backing (salus_read_state), real work only";
       return SALUS_E_INVAL;
@@ -248,7 +268,10 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
     // backing pages: the device footprint (<= declared, so the pool of Cp pages
     // can never run dry under the safety condition); in NULL_WORK mode the
     // allocator still runs, bounded by the declared sizes
-    D.ap_pages = (uint32_t)std::min<uint64_t>((h.fp.p + G - 1) / G, D.p_pages);
+    uint64_t xbytes = 0;
+    D.ap_pages = backing_pages(j, h.fp, (c->cfg.flags & SALUS_FLAG_NULL_WORK) != 0, &D.xpre, &xbytes);
+    D.x_off[0] = D.xpre ? (uint32_t)h.fp.p : 0;
+    D.x_off[1] = D.xpre ? (uint32_t)(h.fp.p + xbytes) : 0;
     D.ae_pages = (uint32_t)std::min<uint64_t>((h.fp.e + G - 1) / G, D.e_pages);
     D.bpad = (uint32_t)pad128(j.batch);
     const uint32_t L = j.n_layers;
@@ -293,6 +316,10 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
     D.stage_tiles[0] = pairs(ti);
     D.stage_tiles[1] = pairs((D.bpad / 128) * (D.dpad[0] / 128));
     for (uint32_t l = 1; l <= L; l++) D.stage_tiles[1 + l] = pairs(D.bpad / 128) * (D.dpad[l] / ntile_for(D.dpad[l]));
+    if (D.xpre) {                    // INIT and F_1 also generate X (GEN prefetch)
+      D.stage_tiles[0] += D.stage_tiles[1];
+      D.stage_tiles[2] += D.stage_tiles[1];
+    }
     if (j.kind == SALUS_TRAIN) {
       for (uint32_t l = L; l >= 1; l--) {
         const uint32_t s = L + 2 + (L - l), nt = ntile_for(D.dpad[l - 1]);

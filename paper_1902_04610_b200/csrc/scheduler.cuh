@@ -45,6 +45,7 @@ struct SchedShared {
   uint16_t Q[MAX_JOBS];
   uint16_t adm[MAX_JOBS];                   // admitted, unfinished
   uint8_t st[MAX_JOBS], jslot[MAX_JOBS], kind[MAX_JOBS];
+  uint8_t xpre[MAX_JOBS];                   // DevJob.xpre (GEN prefetch), tagged on its records
   // run-ahead: records appended per physical slot, last appended seq + 1
   uint32_t sq_tail[MAX_LANES];
   uint64_t last_app[MAX_LANES];
@@ -278,6 +279,7 @@ struct Sched {
     S.svc[j] = 0; S.c[j] = J.iter_ticks; S.done[j] = 0; S.pending[j] = 0; S.next_req[j] = 0;
     S.n[j] = J.n_iters; S.p[j] = J.p_pages; S.e[j] = J.e_pages; S.ap[j] = J.ap_pages; S.ae[j] = J.ae_pages;
     S.id[j] = J.job_id; S.st[j] = ST_NOT_ARRIVED; S.jslot[j] = 0xFF; S.kind[j] = (uint8_t)J.kind;
+    S.xpre[j] = (uint8_t)J.xpre;
     S.nrt[j] = J.kind == SALUS_INFER ? rq[J.req_off] : IDLE_T;
     S.req_off[j] = J.req_off;
     salus_job_stat &st = P.stats[j];
@@ -834,7 +836,8 @@ struct Sched {
     uint32_t won = 0;
     if (tid == 0) {
       volatile DispRec *vr = &sl.recs[tl % RQ];
-      vr->job = j; vr->iter = S.done[j]; vr->seq = pseq; vr->lseq = seq; vr->lane_id = lane_id; vr->kind = kind;
+      vr->job = j; vr->iter = S.done[j]; vr->seq = pseq; vr->lseq = seq; vr->lane_id = lane_id;
+      vr->kind = kind | ((kind == REC_ITER && S.xpre[j]) ? REC_FLAG_XPRE : 0u);
       vr->append_ns = ptx::globaltimer();
       // publish (release) and learn whether the slot was idle in one atomic;
       // only the scheduler ever sets `running`, so taking it needs no CAS

@@ -95,7 +95,7 @@ struct OpDesc {
 
 
 struct TileDesc {
-  uint32_t kind, payload, slot, stage, job, iter, ntiles, next_ntiles, is_last, first_stage;
+  uint32_t kind, payload, slot, stage, job, iter, ntiles, next_ntiles, is_last, first_stage, next_stage;
   uint32_t valid;          // this CTA's half exists (odd block counts leave the peer's empty)
   uint32_t peer_valid;     // the pair's second M block exists
   uint32_t peer_nca;       // (leader) A copies per K-chunk of the peer CTA
@@ -224,6 +224,20 @@ __device__ __forceinline__ SlotHead load_slot_head(const Slot &sl) {
   return hd;
 }
 
+// A GEN tile: CTA h generates 128 x 128 block 2 tile + h of X_kx (A29) into
+// the panels at byte offset `off` of the space `table` translates.
+__device__ __forceinline__ void decode_gen(TileDesc &td, const DevJob &J, uint32_t tile, uint32_t h,
+                                           const uint32_t *table, uint32_t off, uint32_t kx) {
+  td.kind = T_GEN;
+  const uint32_t bp = J.bpad;
+  const uint32_t ncb = J.dpad[0] / 128, blk = 2 * tile + h, mb = blk / ncb, cb = blk % ncb;
+  if (mb >= bp / 128) { td.valid = 0; return; }
+  td.m0 = mb * 128; td.n0 = cb * 128;
+  td.rows_valid = J.batch; td.cols_valid = J.dims[0];
+  for (uint32_t q = 0; q < 2; q++) defer(td, PTR_OUT + q, table, off + (2 * cb + q) * bp * 128u + mb * 16384u);
+  td.key = gen_key(J.seed, J.job_id, GEN_X, 0, kx);
+}
+
 __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, const SlotHead &sl,
                             TileDesc &td, uint32_t h) {
   td.payload = payload;
@@ -234,8 +248,10 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   td.slot = slot; td.stage = stage; td.job = sl.job; td.iter = k; td.seq = sl.seq; td.lseq = sl.lseq;
   td.ntiles = stage_ntiles(J, stage);
   td.is_last = stage >= STAGE_SWAP_OUT || stage == last_stage(J.kind, L);
-  td.next_ntiles = td.is_last ? 0 : J.stage_tiles[stage + 1];
-  td.first_stage = stage >= STAGE_SWAP_OUT ? stage : (k == 0 && !(J.dump & DUMP_INTERNAL_RESUME)) ? 0u : 1u;
+  td.next_stage = td.is_last ? 0 : next_stage(J, stage);
+  td.next_ntiles = td.is_last ? 0 : J.stage_tiles[td.next_stage];
+  td.first_stage = stage >= STAGE_SWAP_OUT ? stage
+                   : (k == 0 && !(J.dump & DUMP_INTERNAL_RESUME)) ? 0u : (J.xpre ? 2u : 1u);
   td.dump_off = -1;
   td.n_ech = 0;
   td.xt_mask = 0;
@@ -255,6 +271,13 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
       td.ptr[PTR_OUT] = stage == STAGE_SWAP_OUT ? host : dev;      // destination
       td.ptr[PTR_OUT + 1] = stage == STAGE_SWAP_OUT ? dev : host;  // source
     }
+    return;
+  }
+  // GEN-prefetch jobs: the INIT stage (X_k) and the F_1 stage (X_{k+1}) end
+  // with the GEN tiles of stage 1's shape, into the per-job X buffers
+  if (J.xpre && (stage == 0 || stage == 2) && tile >= J.stage_tiles[stage] - J.stage_tiles[1]) {
+    const uint32_t kx = stage == 0 ? kg : kg + 1;
+    decode_gen(td, J, tile - (J.stage_tiles[stage] - J.stage_tiles[1]), h, jt, J.x_off[kx & 1], kx);
     return;
   }
   if (stage == 0) {                                   // INIT weights (128 x 128 blocks)
@@ -279,16 +302,12 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     return;
   }
   if (stage == 1) {                                   // GEN input batch X (128 x 128 blocks)
-    td.kind = T_GEN;
-    const uint32_t ncb = J.dpad[0] / 128, blk = 2 * tile + h, mb = blk / ncb, cb = blk % ncb;
-    if (mb >= bp / 128) { td.valid = 0; return; }
-    td.m0 = mb * 128; td.n0 = cb * 128;
-    td.rows_valid = J.batch; td.cols_valid = J.dims[0];
-    for (uint32_t q = 0; q < 2; q++)
-      defer(td, PTR_OUT + q, lt, J.act_off[0] + (2 * cb + q) * bp * 128u + mb * 16384u);
-    td.key = gen_key(J.seed, J.job_id, GEN_X, 0, kg);
+    decode_gen(td, J, tile, h, lt, J.act_off[0], kg);
     return;
   }
+  // where X_k is read from: the lane (GEN stage) or the job's prefetch buffer
+  const uint32_t *xt = J.xpre ? jt : lt;
+  const uint32_t xo = J.xpre ? J.x_off[kg & 1] : J.act_off[0];
   td.kind = T_GEMM;
   if (stage <= L + 1) {                               // forward F_l
     const uint32_t l = stage - 1, N = ntile_for(J.dpad[l]), ntn = J.dpad[l] / N;
@@ -296,7 +315,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     td.valid = mb < bp / 128;
     td.peer_valid = (mb | 1u) < bp / 128;
     td.layer = l; td.N = N; td.nk = J.dpad[l - 1] / 64;
-    td.a = OpDesc{lt, J.act_off[l - 1], bp, mb * 128, 0};
+    td.a = l == 1 ? OpDesc{xt, xo, bp, mb * 128, 0} : OpDesc{lt, J.act_off[l - 1], bp, mb * 128, 0};
     td.b = OpDesc{jt, J.wb_off[l - 1][kg & 1], J.dpad[l], nb * N + h * (N / 2), 0};
     td.m0 = mb * 128; td.n0 = nb * N;
     td.rows_valid = J.batch; td.cols_valid = J.dims[l]; td.ld_logical = J.dims[l];
@@ -324,7 +343,8 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
       td.peer_valid = (mb | 1u) < J.dpad[l] / 128;
       td.epi = EPI_SGD; td.nk = bp / 64;
       td.a = OpDesc{lt, gin, bp, mb * 128, 1};
-      td.b = OpDesc{lt, J.act_off[l - 1], bp, nb * N + h * (N / 2), 1};
+      td.b = l == 1 ? OpDesc{xt, xo, bp, nb * N + h * (N / 2), 1}
+                    : OpDesc{lt, J.act_off[l - 1], bp, nb * N + h * (N / 2), 1};
       td.m0 = mb * 128; td.n0 = nb * N;
       td.rows_valid = J.dims[l]; td.cols_valid = J.dims[l - 1]; td.ld_logical = J.dims[l];
       td.lr = J.lr;
@@ -977,7 +997,7 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
             pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)pn);
           }
         } else {
-          pub = 1; ps = td.slot; pst = td.stage + 1; pn = td.next_ntiles;
+          pub = 1; ps = td.slot; pst = td.next_stage; pn = td.next_ntiles;
           pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)pn);
         }
       }

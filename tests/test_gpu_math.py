@@ -181,3 +181,25 @@ def test_max_sizes():
         _check_math(ctx, jobs)
     finally:
         ctx.close()
+
+
+@pytest.mark.parametrize("kind", [TRAIN, INFER])
+@pytest.mark.parametrize("dims,batch", [((128, 256, 128), 128), ((200, 256, 72), 300), ((384, 128, 256, 128), 100)])
+def test_gen_prefetch_jobs(kind, dims, batch):
+    """Jobs whose declared P leaves room for two X buffers take the GEN-
+    prefetch path (X_{k+1} generated by extra tiles of iteration k's F_1
+    stage, X_0 by INIT): same schedule, same math as the oracle."""
+    from paper_1902_04610_b200 import salus as S
+    from workloads import footprint_bytes
+    jobs = []
+    for jid in range(2):
+        p, e = footprint_bytes(kind, dims, batch)
+        jobs.append(make_job(jid, kind, 0, dims, batch, 4, lr=1e-2, seed=60 + jid,
+                             persistent_bytes=p + (8 << 20), ephemeral_bytes=e,
+                             request_ticks=(0, 1, 2, 3) if kind == INFER else ()))
+    dump = {j.job_id: S.DUMP_OUTPUTS | (S.DUMP_WEIGHTS if kind == TRAIN else 0) for j in jobs}
+    ctx, ref, stats = assert_schedule_parity(jobs, 1 << 30, OS.PACK, null_work=False, dump=dump)
+    try:
+        _check_math(ctx, jobs)
+    finally:
+        ctx.close()

@@ -35,11 +35,15 @@ def _run(jobs, dump, policy=OS.PACK, resume=None, cap=1 << 30):
         raise
 
 
-@pytest.mark.parametrize("k", [1, 2, 5])
-def test_split_run_equals_straight_run(k):
+@pytest.mark.parametrize("k,slack", [(1, 0), (2, 0), (5, 0), (2, 8 << 20)])
+def test_split_run_equals_straight_run(k, slack):
+    """slack > 0: the declared P leaves room for the GEN-prefetch X buffers,
+    which then travel inside the state image."""
     from paper_1902_04610_b200 import salus as S
+    from workloads import footprint_bytes
     n = 6
-    full = make_job(7, TRAIN, 0, (256, 512, 256), 200, n, lr=1e-2, seed=41)
+    full = make_job(7, TRAIN, 0, (256, 512, 256), 200, n, lr=1e-2, seed=41,
+                    persistent_bytes=footprint_bytes(TRAIN, (256, 512, 256), 200)[0] + slack)
     ctx = _run([full], {7: S.DUMP_WEIGHTS | S.DUMP_OUTPUTS})
     W_straight = ctx.layers(7, S.WEIGHTS).copy()
     out_straight = [ctx.layers(7, i).copy() for i in range(n)]
@@ -78,8 +82,8 @@ def test_resumed_job_under_eviction():
     from paper_1902_04610_b200 import salus as S
     G = 1 << 16
     n, k = 8, 3
-    full = make_job(0, TRAIN, 0, (128, 256, 128), 128, n, iter_ticks=100, persistent_bytes=8 * G,
-                    ephemeral_bytes=6 * G, lr=1e-2, seed=11)
+    full = make_job(0, TRAIN, 0, (128, 256, 128), 128, n, iter_ticks=100, persistent_bytes=10 * G,
+                    ephemeral_bytes=6 * G, lr=1e-2, seed=11)      # 8 + 2 X-buffer pages: GEN prefetch
     ctx = _run([full], {0: S.DUMP_WEIGHTS})
     W_straight = ctx.layers(0, S.WEIGHTS).copy()
     ctx.close()
@@ -87,12 +91,13 @@ def test_resumed_job_under_eviction():
     img = ctx.read_state(0)
     ctx.close()
     rest = dataclasses.replace(full, n_iters=n - k)
-    short = make_job(1, TRAIN, 150, (128, 256, 128), 128, 1, iter_ticks=100, persistent_bytes=8 * G,
+    short = make_job(1, TRAIN, 150, (128, 256, 128), 128, 1, iter_ticks=100, persistent_bytes=10 * G,
                      ephemeral_bytes=6 * G, lr=1e-2, seed=12)
     from paper_1902_04610_b200 import build
     build.build()
-    ref = OS.simulate([rest, short], 20 * G, OS.SRTF, evict=True)
-    ctx = S.Context([rest, short], 20 * G, S.SRTF, evict=True, dump={0: S.DUMP_WEIGHTS},
+    ref = OS.simulate([rest, short], 24 * G, OS.SRTF, evict=True)
+    assert sum(1 for r in ref.log if r[1] == 10) == 1
+    ctx = S.Context([rest, short], 24 * G, S.SRTF, evict=True, dump={0: S.DUMP_WEIGHTS},
                     resume={0: (img, k)}, log=True)
     try:
         ctx.run()
