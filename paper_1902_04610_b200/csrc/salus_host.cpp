@@ -134,12 +134,13 @@ uint32_t backing_pages(const salus_job &j, const Footprint &fp, bool null_work, 
   const uint64_t G = PAGE_BYTES;
   const uint64_t p_pages = (j.persistent_bytes + G - 1) / G;
   const uint64_t xb = 2ull * pad128(j.batch) * pad128(j.dims[0]);
+  const uint64_t tb = j.kind == SALUS_TRAIN ? 2ull * pad128(j.batch) * pad128(j.dims[j.n_layers]) : 0;
   static const bool enabled = [] { const char *e = getenv("SALUS_XPRE"); return !(e && e[0] == '0'); }();
   *xpre = 0;
   *xbytes = xb;
-  if (!null_work && enabled && p_pages * G >= fp.p + 2 * xb) {
+  if (!null_work && enabled && p_pages * G >= fp.p + 2 * xb + 2 * tb) {
     *xpre = 1;
-    return (uint32_t)((fp.p + 2 * xb + G - 1) / G);
+    return (uint32_t)((fp.p + 2 * xb + 2 * tb + G - 1) / G);
   }
   return (uint32_t)std::min<uint64_t>((fp.p + G - 1) / G, p_pages);
 }
@@ -272,6 +273,10 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
     D.ap_pages = backing_pages(j, h.fp, (c->cfg.flags & SALUS_FLAG_NULL_WORK) != 0, &D.xpre, &xbytes);
     D.x_off[0] = D.xpre ? (uint32_t)h.fp.p : 0;
     D.x_off[1] = D.xpre ? (uint32_t)(h.fp.p + xbytes) : 0;
+    const uint64_t tbytes = 2ull * pad128(j.batch) * pad128(j.dims[j.n_layers]);
+    const bool tpre = D.xpre && j.kind == SALUS_TRAIN;
+    D.t_off[0] = tpre ? (uint32_t)(h.fp.p + 2 * xbytes) : 0;
+    D.t_off[1] = tpre ? (uint32_t)(h.fp.p + 2 * xbytes + tbytes) : 0;
     D.ae_pages = (uint32_t)std::min<uint64_t>((h.fp.e + G - 1) / G, D.e_pages);
     D.bpad = (uint32_t)pad128(j.batch);
     const uint32_t L = j.n_layers;
@@ -316,9 +321,10 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
     D.stage_tiles[0] = pairs(ti);
     D.stage_tiles[1] = pairs((D.bpad / 128) * (D.dpad[0] / 128));
     for (uint32_t l = 1; l <= L; l++) D.stage_tiles[1 + l] = pairs(D.bpad / 128) * (D.dpad[l] / ntile_for(D.dpad[l]));
-    if (D.xpre) {                    // INIT and F_1 also generate X (GEN prefetch)
-      D.stage_tiles[0] += D.stage_tiles[1];
-      D.stage_tiles[2] += D.stage_tiles[1];
+    D.t_gen_tiles = (D.xpre && j.kind == SALUS_TRAIN) ? pairs((D.bpad / 128) * (D.dpad[L] / 128)) : 0;
+    if (D.xpre) {                    // INIT and F_1 also generate X and T (GEN prefetch)
+      D.stage_tiles[0] += D.stage_tiles[1] + D.t_gen_tiles;
+      D.stage_tiles[2] += D.stage_tiles[1] + D.t_gen_tiles;
     }
     if (j.kind == SALUS_TRAIN) {
       for (uint32_t l = L; l >= 1; l--) {

@@ -224,18 +224,19 @@ __device__ __forceinline__ SlotHead load_slot_head(const Slot &sl) {
   return hd;
 }
 
-// A GEN tile: CTA h generates 128 x 128 block 2 tile + h of X_kx (A29) into
-// the panels at byte offset `off` of the space `table` translates.
+// A GEN tile: CTA h generates 128 x 128 block 2 tile + h of X_kx (or, with
+// `targets`, of the MSE targets T_kx; A29) into the panels at byte offset
+// `off` of the space `table` translates.
 __device__ __forceinline__ void decode_gen(TileDesc &td, const DevJob &J, uint32_t tile, uint32_t h,
-                                           const uint32_t *table, uint32_t off, uint32_t kx) {
+                                           const uint32_t *table, uint32_t off, uint32_t kx, bool targets = false) {
   td.kind = T_GEN;
-  const uint32_t bp = J.bpad;
-  const uint32_t ncb = J.dpad[0] / 128, blk = 2 * tile + h, mb = blk / ncb, cb = blk % ncb;
+  const uint32_t bp = J.bpad, L = J.n_layers, d = targets ? L : 0;
+  const uint32_t ncb = J.dpad[d] / 128, blk = 2 * tile + h, mb = blk / ncb, cb = blk % ncb;
   if (mb >= bp / 128) { td.valid = 0; return; }
   td.m0 = mb * 128; td.n0 = cb * 128;
-  td.rows_valid = J.batch; td.cols_valid = J.dims[0];
+  td.rows_valid = J.batch; td.cols_valid = J.dims[d];
   for (uint32_t q = 0; q < 2; q++) defer(td, PTR_OUT + q, table, off + (2 * cb + q) * bp * 128u + mb * 16384u);
-  td.key = gen_key(J.seed, J.job_id, GEN_X, 0, kx);
+  td.key = targets ? gen_key(J.seed, J.job_id, GEN_T, L, kx) : gen_key(J.seed, J.job_id, GEN_X, 0, kx);
 }
 
 __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, const SlotHead &sl,
@@ -275,10 +276,11 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   }
   // GEN-prefetch jobs: the INIT stage (X_k) and the F_1 stage (X_{k+1}) end
   // with the GEN tiles of stage 1's shape, into the per-job X buffers
-  if (J.xpre && (stage == 0 || stage == 2) && tile >= J.stage_tiles[stage] - J.stage_tiles[1]) {
+  if (J.xpre && (stage == 0 || stage == 2)) {
+    const uint32_t ngx = J.stage_tiles[1], base = J.stage_tiles[stage] - ngx - J.t_gen_tiles;
     const uint32_t kx = stage == 0 ? kg : kg + 1;
-    decode_gen(td, J, tile - (J.stage_tiles[stage] - J.stage_tiles[1]), h, jt, J.x_off[kx & 1], kx);
-    return;
+    if (tile >= base + ngx) { decode_gen(td, J, tile - base - ngx, h, jt, J.t_off[kx & 1], kx, true); return; }
+    if (tile >= base) { decode_gen(td, J, tile - base, h, jt, J.x_off[kx & 1], kx); return; }
   }
   if (stage == 0) {                                   // INIT weights (128 x 128 blocks)
     td.kind = T_INIT;
@@ -324,6 +326,11 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     else if (J.kind == SALUS_TRAIN) {
       td.epi = EPI_LOSS; out_off = J.g_off[0];
       td.key = gen_key(J.seed, J.job_id, GEN_T, L, kg);
+      if (J.t_gen_tiles && td.valid) {               // prefetched T_k: 2 target panels per input chunk
+        for (uint32_t q = 0; q < N / 64; q++)
+          defer(td, PTR_EPI + q, jt, J.t_off[kg & 1] + (nb * N / 64 + q) * bp * 128u + mb * 16384u);
+        td.n_ech = N / 128;
+      }
     } else { td.epi = EPI_OUT; out_off = J.act_off[L]; }
     if (td.valid) {
       if (l == L && (J.dump & SALUS_DUMP_OUTPUTS))
@@ -495,6 +502,22 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
       } else if (td.epi == EPI_OUT) {
 #pragma unroll
         for (int x = 0; x < 32; x++) v[x] = row_ok ? v[x] : 0.f;
+      } else if (buf) {  // EPI_LOSS with T prefetched (bf16 panels, exact: A29 values are bf16)
+        const float inv_b = 1.0f / (float)td.rows_valid;
+        const int ncol = row_ok ? (int)td.cols_valid - (int)col0 : 0;
+        const uint8_t *tp = buf + ((cc - ccb) >> 1) * 16384u;
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const uint4 m = *reinterpret_cast<const uint4 *>(tp + swz(r, ch0 + q));
+          const uint32_t w[4] = {m.x, m.y, m.z, m.w};
+#pragma unroll
+          for (int hh = 0; hh < 4; hh++) {
+            const int x0 = 8 * q + 2 * hh;
+            const float t0 = __uint_as_float(w[hh] << 16), t1 = __uint_as_float(w[hh] & 0xFFFF0000u);
+            v[x0] = x0 < ncol ? (v[x0] - t0) * inv_b : 0.f;
+            v[x0 + 1] = x0 + 1 < ncol ? (v[x0 + 1] - t1) * inv_b : 0.f;
+          }
+        }
       } else {  // EPI_LOSS: G_L = (A_L - T) / B  (MSE)
         // branch-free so the 32 independent hash chains interleave (ILP)
         const float inv_b = 1.0f / (float)td.rows_valid;
