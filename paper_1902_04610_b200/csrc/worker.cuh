@@ -122,6 +122,7 @@ struct WorkerSmem {
   TileDesc desc[NDESC];
   uint64_t full[PIPE], empty[PIPE];
   uint64_t desc_full[NDESC], desc_empty[NDESC];
+  uint64_t desc_ptrs[NDESC];          // the descriptor's translated pointers are in place
   uint64_t acc_full[2], acc_empty[2];
   uint64_t epi_full[EBUF], epi_empty[EBUF];
   uint64_t epi_done[NDESC];           // epilogue -> completion warp
@@ -682,6 +683,7 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint
         td.kind = T_EXIT;
         td.payload = TASK_EXIT;
         ptx::mbar_arrive(&W.desc_full[d]);
+        ptx::mbar_arrive(&W.desc_ptrs[d]);
       }
       break;
     }
@@ -699,14 +701,17 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint
       td.t_claim = t_claim;
     }
     __syncwarp();
-    if (lane < NPTR && ((td.xt_mask >> lane) & 1u)) td.ptr[lane] = xlate(P, td.xt_table[lane], td.xt_off[lane]);
-    __syncwarp();
+    // the operand loader and the MMA need no translated pointers: hand them
+    // the descriptor first, translate the epilogue's pointers meanwhile
     if (lane == 0) {
       if (h == 0 && td.stage == td.first_stage)
         atomicMin((unsigned long long *)&P.slots[td.slot].start_ns, (unsigned long long)ptx::globaltimer());
       ptx::fence_proxy_async_global();
       ptx::mbar_arrive(&W.desc_full[d]);
     }
+    if (lane < NPTR && ((td.xt_mask >> lane) & 1u)) td.ptr[lane] = xlate(P, td.xt_table[lane], td.xt_off[lane]);
+    __syncwarp();
+    if (lane == 0) ptx::mbar_arrive(&W.desc_ptrs[d]);
     __syncwarp();
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
@@ -807,6 +812,7 @@ __device__ void epi_loader(const Params &P, WorkerSmem &W, uint32_t h) {
     ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
     const TileDesc &td = W.desc[d];
     if (td.kind == T_EXIT) break;
+    ptx::mbar_wait_abortable(&W.desc_ptrs[d], d_phase, &P.ctrl->abort);
     if (td.kind == T_GEMM) {
       const uint32_t n = td.n_ech;
       const bool sgd = td.epi == EPI_SGD;
@@ -903,6 +909,7 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
     ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
     const TileDesc &td = W.desc[d];
     if (td.kind == T_EXIT) break;
+    ptx::mbar_wait_abortable(&W.desc_ptrs[d], d_phase, &P.ctrl->abort);
     if (td.valid) my_tasks++;
     const uint64_t t_ready = ptx::globaltimer();
     uint64_t t_mma = t_ready;
@@ -1058,6 +1065,7 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
     // completion warp (after the epilogue is done)
     for (uint32_t d = 0; d < NDESC; d++) {
       ptx::mbar_init(&W.desc_full[d], 1);
+      ptx::mbar_init(&W.desc_ptrs[d], 1);
       ptx::mbar_init(&W.desc_empty[d], 4);
       ptx::mbar_init(&W.epi_done[d], 1);
       ptx::mbar_init(&W.mail_full[d], 1);
