@@ -32,7 +32,13 @@ def _small(job_id, seed, n_iters=6):
     w = int(rng.choice([128, 256, 384]))
     depth = int(rng.integers(1, 4))
     batch = int(rng.choice([64, 128, 200]))
-    return make_job(job_id, TRAIN, 0, (w,) * (depth + 1), batch, n_iters, lr=1e-2, seed=seed)
+    # odd seeds declare 4 MiB of persistent slack: those jobs take the GEN /
+    # target prefetch path (their X, T live in per-job buffers)
+    from workloads import footprint_bytes
+    dims = (w,) * (depth + 1)
+    slack = (4 << 20) if seed % 2 else 0
+    return make_job(job_id, TRAIN, 0, dims, batch, n_iters, lr=1e-2, seed=seed,
+                    persistent_bytes=footprint_bytes(TRAIN, dims, batch)[0] + slack)
 
 
 def _run_online(policy, pre, live, cap, delays_s, null_work, max_lanes=0):
