@@ -1,3 +1,8 @@
+#!/bin/bash
+# A/B of the GEN/target prefetch: C4 under SRTF and PACK with
+# SALUS_XPRE=1 (default) and =0, two interleaved rounds, plus C2a / C1 sanity
+# (their jobs declare no persistent slack, so they never take the path).
+# usage (on the GPU box): bash tools/ab_xpre.sh
 for r in 1 2; do
 for x in 1 0; do
   echo "== SALUS_XPRE=$x round $r"
