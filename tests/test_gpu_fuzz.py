@@ -38,7 +38,7 @@ def _trace(seed, n_jobs=7):
     return jobs, int(need * 2.2) * G
 
 
-@pytest.mark.parametrize("seed", range(4))
+@pytest.mark.parametrize("seed", range(8))
 @pytest.mark.parametrize("policy,max_lanes,evict", [(OS.PACK, 0, False), (OS.FAIR, 3, False),
                                                     (OS.SRTF, 1, True), (OS.FIFO, 0, False)])
 def test_random_real_work(seed, policy, max_lanes, evict):
