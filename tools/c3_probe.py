@@ -1,4 +1,9 @@
-import sys; sys.path.insert(0,'/root/repo')
+"""What bounds C3 (42 inference models): per policy, kernel time, scheduler
+wait (and its fence / ring parts), and the physical busy time of each lane
+from the wall stamps -- the busiest lane bounds a run whose scheduler waits.
+usage: python tools/c3_probe.py"""
+import os, sys
+sys.path.insert(0, os.path.join(os.path.dirname(os.path.abspath(__file__)), '..'))
 from paper_1902_04610_b200 import build, salus as S
 from workloads import c3_trace
 import numpy as np
