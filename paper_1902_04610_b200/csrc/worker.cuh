@@ -340,11 +340,16 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
         defer(td, PTR_OUT + q, lt, out_off + (td.n0 / 64 + q) * bp * 128u + mb * 16384u);
     }
   } else {                                            // backward B_l
+    const uint32_t tile_in = tile;
     const uint32_t l = L - (stage - (L + 2));
     const uint32_t N = ntile_for(J.dpad[l - 1]), ntn = J.dpad[l - 1] / N;
     const uint32_t nW = ((J.dpad[l] / 128 + 1) / 2) * ntn;     // dW pair tasks
     const uint32_t gin = J.g_off[(L - l) & 1], gout = J.g_off[(L - l + 1) & 1];
     td.layer = l; td.N = N;
+    // the long-K dX tiles take the stage's first task indices, so they are
+    // claimed first (longest first within the stage)
+    const uint32_t nX = J.stage_tiles[stage] - nW;
+    const uint32_t tile = tile_in < nX ? nW + tile_in : tile_in - nX;
     if (tile < nW) {                                  // dW_l^T = G_l^T A_{l-1}; SGD
       const uint32_t mb = 2 * (tile / ntn) + h, nb = tile % ntn;
       td.valid = mb < J.dpad[l] / 128;
