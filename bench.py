@@ -158,9 +158,12 @@ def switch_latency(S, device):
     def pct(a):
         return {"n": len(a), "p50": float(np.median(a)) if a else None,
                 "p99": float(np.percentile(a, 99)) if a else None}
+    byts = sum(j.n_iters * algorithmic_bytes(j.kind, j.dims, j.batch) for j in jobs)
+    flops = sum(j.n_iters * algorithmic_flops(j.kind, j.dims, j.batch) for j in jobs)
     return {"config": "C3: 42 inference models (14 archs x 3), FAIR, 8 lanes, 16 GiB",
             "models_coresident": len(jobs), "requests": int(rs["n_dispatch"]),
             "requests_per_s": rs["n_dispatch"] / (rs["kernel_ns"] / 1e9),
+            "algorithmic_gbs": byts / rs["kernel_ns"], "algorithmic_tflops": flops / rs["kernel_ns"] / 1e3,
             "switch_us": pct(sw), "switch_from_ready_us": pct(rdy),
             "same_job_gap_us": pct(gap),
             "request_latency_logical_us": {"avg": float(np.mean(req_lat)) / 1e3,
