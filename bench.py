@@ -30,7 +30,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from workloads import (TRAIN, algorithmic_bytes, algorithmic_flops, c2_trace,  # noqa: E402
-                       c3_trace, partition)
+                       c3_trace)
 
 METRIC = "aggregate iters/s at 1-8 B200; job-switch µs; avg JCT vs FIFO baseline"
 UNIT = "iters/s"

@@ -304,7 +304,10 @@ int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64
  * order, like salus_run) over a private non-blocking stream, concurrently
  * with the running kernel.  *n_done (may be NULL) = jobs whose last
  * iteration has physically completed (wall_end_ns != 0); their records are
- * final.  Records of unfinished jobs are partial (-1 / 0 where not yet set).
+ * final.  Records of unfinished jobs are partial (-1 / 0 where not yet set);
+ * salus_run_async resets every record to that state on cfg.stream before the
+ * kernel starts, and the poll's copy is ordered after that reset, so a poll
+ * never returns a previous run's records.
  * Errors: E_STATE (nothing running), E_CUDA. */
 int salus_poll_stats(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats,
                      uint64_t *n_done);
@@ -320,7 +323,8 @@ typedef struct {
   uint64_t sched_wait_ns;     /* scheduler time spent waiting for iterations      */
   int32_t  status;            /* SALUS_OK or the device error code               */
   uint32_t n_workers;         /* worker CTA pairs                                 */
-  uint64_t h2d_bytes;         /* host->device bytes of salus_prepare (job tables) */
+  uint64_t h2d_bytes;         /* host->device bytes of salus_prepare (job tables)
+                                 plus this run's reset image of the per-job records */
   uint64_t d2h_bytes;         /* device->host bytes read back by salus_run        */
   uint64_t sched_fence_ns;    /* part of sched_wait_ns: page-reuse fences (A30)    */
   uint64_t sched_ring_ns;     /* part of sched_wait_ns: a lane's dispatch ring full */
@@ -365,7 +369,12 @@ int salus_read_trace(salus_ctx *ctx, salus_trace_rec *buf, uint64_t cap_recs, ui
 
 const char *salus_last_error(const salus_ctx *ctx);
 
-/* Release the host context (NULL-safe).  Never frees caller buffers. */
+/* Release the host context (NULL-safe).  Never frees caller buffers.
+ * Returns SALUS_E_TIMEOUT without freeing anything if a salus_wait found the
+ * kernel still running 20 s after the abort request (the context is
+ * "poisoned": the kernel may still touch the mapped flags and the caller's
+ * arena/meta/swap, so the caller must keep those alive too and reset the
+ * device). */
 int salus_close(salus_ctx *ctx);
 
 #ifdef __cplusplus

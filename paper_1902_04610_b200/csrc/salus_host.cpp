@@ -106,6 +106,12 @@ struct salus_ctx {
   uint64_t ppt_used = 0, ppt_cap = 0, ring_tiles = 0, dump_cur = 0, dump_cap = 0;
   uint32_t max_id = 0, n_pre = 0;
   bool t_out = false;
+  // the kernel ignored the abort flag past the grace period: buffers it may
+  // still touch (mapped flags, caller arena/meta/swap) must never be freed
+  bool poisoned = false;
+  uint32_t n_cap = 0;                              // stats records reserved (max_jobs when online)
+  uint64_t run_h2d = 0;                            // per-run H2D bytes (stats reset image)
+  std::vector<salus_job_stat> stats_img;           // host source of that copy (outlives it)
   std::chrono::steady_clock::time_point t0;
 };
 
@@ -138,7 +144,9 @@ uint32_t backing_pages(const salus_job &j, const Footprint &fp, bool null_work, 
   static const bool enabled = [] { const char *e = getenv("SALUS_XPRE"); return !(e && e[0] == '0'); }();
   *xpre = 0;
   *xbytes = xb;
-  if (!null_work && enabled && p_pages * G >= fp.p + 2 * xb + 2 * tb) {
+  // DevJob byte offsets inside a job's persistent space are 32-bit: the
+  // prefetch buffers go past the footprint, so they need it to stay < 4 GiB
+  if (!null_work && enabled && p_pages * G >= fp.p + 2 * xb + 2 * tb && fp.p + 2 * xb + 2 * tb <= 0xFFFFFFFFull) {
     *xpre = 1;
     return (uint32_t)((fp.p + 2 * xb + 2 * tb + G - 1) / G);
   }
@@ -372,6 +380,7 @@ static void compute_layout(salus_ctx *c) {
   c->dump_cur = dump_cur;
   c->n_pre = n;
   uint32_t n_cap = n;
+  c->n_cap = n;
   if (online) {
     // room for live jobs: descriptors and stats up to max_jobs, page-table
     // entries for 4 x C of persistent memory over the run, lanes up to C,
@@ -380,6 +389,7 @@ static void compute_layout(salus_ctx *c) {
     max_ae = std::max<uint64_t>(max_ae, c->Cp);
     max_tiles = std::max<uint64_t>(max_tiles, 4096);
     n_cap = c->cfg.max_jobs;
+    c->n_cap = n_cap;
   }
   c->ring_tiles = max_tiles;
   c->lpt_stride = (uint32_t)max_ae;
@@ -423,7 +433,9 @@ static void compute_layout(salus_ctx *c) {
 
 int salus_meta_bytes(const salus_ctx *ctx, uint64_t *bytes) {
   if (!ctx || !bytes) return SALUS_E_INVAL;
-  compute_layout(const_cast<salus_ctx *>(ctx));
+  // the layout is frozen at prepare (live jobs only consume reserved space):
+  // recomputing it afterwards would move the offsets Params already holds
+  if (ctx->state == 0) compute_layout(const_cast<salus_ctx *>(ctx));
   *bytes = ctx->total;
   return SALUS_OK;
 }
@@ -437,7 +449,7 @@ static bool needs_swap(const salus_ctx *ctx) {
 
 int salus_swap_bytes(const salus_ctx *ctx, uint64_t *bytes) {
   if (!ctx || !bytes) return SALUS_E_INVAL;
-  compute_layout(const_cast<salus_ctx *>(ctx));
+  if (ctx->state == 0) compute_layout(const_cast<salus_ctx *>(ctx));
   // job j's region: its persistent backing pages, at pt_off pages (dense order)
   *bytes = needs_swap(ctx) ? ctx->ppt_used * ctx->cfg.page_bytes : 0;
   return SALUS_OK;
@@ -590,6 +602,7 @@ int salus_run_async(salus_ctx *ctx) {
   if (!ctx) return SALUS_E_INVAL;
   if (ctx->state != 1) return fail(ctx, SALUS_E_STATE, "salus_prepare first");
   if (ctx->running) return fail(ctx, SALUS_E_STATE, "already running");
+  if (ctx->poisoned) return fail(ctx, SALUS_E_STATE, "context poisoned by a kernel that ignored the abort");
   if ((ctx->cfg.flags & SALUS_FLAG_ONLINE) && ctx->ran) return fail(ctx, SALUS_E_STATE, "an online context runs once");
   cudaError_t e = cudaSetDevice(ctx->cfg.device);
   if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
@@ -601,6 +614,22 @@ int salus_run_async(salus_ctx *ctx) {
       (e = cudaMemsetAsync(m + ctx->off_fseq, 0, 8ull * ctx->Cp, st)) ||
       (e = cudaMemsetAsync(m + ctx->off_pend, 0, 8ull * MAX_LANES * MAX_LANES, st)))
     return cuda_fail(ctx, e, "reset");
+  // per-job records start as "nothing yet" (job id, -1 ticks, 0 stamps) before
+  // ev0, so a salus_poll_stats ordered after ev0 never sees a previous run's
+  // records or uninitialised memory; the device's init_job rewrites the same
+  {
+    std::vector<salus_job_stat> img(std::max<uint32_t>(ctx->n_cap, 1));
+    for (auto &r : img) {
+      r.job_id = NONE32; r.first_lane = NONE32; r.admit_tick = -1; r.first_start_tick = -1;
+      r.completion_tick = -1; r.completion_seq = ~0ull; r.wall_start_ns = 0; r.wall_end_ns = 0; r.wall_arrive_ns = 0;
+    }
+    for (uint32_t d = 0; d < (uint32_t)ctx->djobs.size() && d < img.size(); d++) img[d].job_id = ctx->djobs[d].job_id;
+    ctx->stats_img.swap(img);
+    if ((e = cudaMemcpyAsync(m + ctx->off_stats, ctx->stats_img.data(), sizeof(salus_job_stat) * ctx->stats_img.size(),
+                             cudaMemcpyHostToDevice, st)))
+      return cuda_fail(ctx, e, "reset stats");
+    ctx->run_h2d = sizeof(salus_job_stat) * ctx->stats_img.size();
+  }
   *reinterpret_cast<volatile uint32_t *>(ctx->host_abort) = 0;
   // migration: every run starts from the resume images (a DUMP_STATE job's
   // region is overwritten with its final state by the previous run)
@@ -716,8 +745,11 @@ int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64
       timed_out = true;
     }
     if (timed_out && ms > ctx->cfg.timeout_ms + 20000.0) {
+      // the kernel may still read/write the mapped flags and the caller's
+      // buffers: never free them (salus_close leaks them); reset the device
       ctx->running = false;
-      return fail(ctx, SALUS_E_TIMEOUT, "kernel did not exit after abort");
+      ctx->poisoned = true;
+      return fail(ctx, SALUS_E_TIMEOUT, "kernel did not exit after abort (context poisoned: reset the device)");
     }
     std::this_thread::sleep_for(std::chrono::microseconds(20));
   }
@@ -734,7 +766,7 @@ int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64
   rs.sched_wait_ns = ctrl.sched_wait_ns; rs.sched_fence_ns = ctrl.sched_fence_ns; rs.sched_ring_ns = ctrl.sched_ring_ns; rs.status = ctrl.status; rs.n_workers = ctx->grid / 2 - 1;
   rs.n_swap_out = ctrl.n_swap_out; rs.n_swap_in = ctrl.n_swap_in; rs.swap_bytes = ctrl.swap_bytes; rs.swap_ns = ctrl.swap_ns;
   ctx->n_trace = std::min<uint64_t>(ctrl.n_trace, ctx->trace_cap);
-  rs.h2d_bytes = ctx->h2d_bytes;
+  rs.h2d_bytes = ctx->h2d_bytes + ctx->run_h2d;
   rs.d2h_bytes = sizeof(Ctrl) + (stats ? sizeof(salus_job_stat) * ctx->jobs.size() : 0);
   ctx->ran = true;
   const uint32_t n = (uint32_t)ctx->jobs.size();
@@ -766,11 +798,15 @@ int salus_poll_stats(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, 
   if (!ctx->side && (e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)))
     return cuda_fail(ctx, e, "side stream");
   uint32_t n;
+  std::vector<uint32_t> d2s;
   {
     std::lock_guard<std::mutex> g(ctx->live_mu);     // live submissions grow the table
     n = (uint32_t)ctx->jobs.size();
+    d2s = ctx->dense_to_submit;
   }
   std::vector<salus_job_stat> dense(n);
+  // never overtake run_async's reset of the records (recorded before ev0)
+  if ((e = cudaStreamWaitEvent(ctx->side, ctx->ev0, 0))) return cuda_fail(ctx, e, "poll order");
   if (n && ((e = cudaMemcpyAsync(dense.data(), ctx->meta + ctx->off_stats, sizeof(salus_job_stat) * n,
                                  cudaMemcpyDeviceToHost, ctx->side)) ||
             (e = cudaStreamSynchronize(ctx->side))))
@@ -780,7 +816,7 @@ int salus_poll_stats(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, 
   if (n_done) *n_done = done;
   const uint64_t k = stats ? std::min<uint64_t>(max_stats, n) : 0;
   for (uint32_t d = 0; d < n && stats; d++) {
-    const uint32_t s = d < ctx->dense_to_submit.size() ? ctx->dense_to_submit[d] : d;
+    const uint32_t s = d < d2s.size() ? d2s[d] : d;
     if (s < k) stats[s] = dense[d];
   }
   if (n_stats) *n_stats = k;
@@ -871,6 +907,7 @@ const char *salus_last_error(const salus_ctx *ctx) { return ctx ? ctx->err.c_str
 
 int salus_close(salus_ctx *ctx) {
   if (!ctx) return SALUS_OK;
+  if (ctx->poisoned) return SALUS_E_TIMEOUT;   // leak: a hung kernel may still use the mapped buffers
   if (ctx->running) {                      // never free under a live kernel
     if (ctx->live && !ctx->ended) salus_end_submissions(ctx);
     salus_wait(ctx, nullptr, 0, nullptr);

@@ -2,7 +2,7 @@
 
 Jobs are independent units, so the path shards with no data-path
 collective: the k-th job in (arrival, id) order goes to GPU k mod G
-(`workloads.partition`).  The only collective is one all_gather of fixed-size
+(`partition_jobs`; tests hold it to oracle/placement.py).  The only collective is one all_gather of fixed-size
 per-GPU completion records after the run (NCCL over NVLink on the GPU box,
 gloo in the CPU tests).  Host logic only — marshalling, no method arithmetic.
 """
@@ -58,8 +58,8 @@ def partition_jobs(jobs: Iterable, world: int, rank: int, placement: str = "mod"
     rank's jobs are returned in (arrival, id) order."""
     jobs = list(jobs)
     if placement == "mod":
-        from workloads import partition
-        return partition(jobs, world, rank)
+        order = sorted(jobs, key=lambda j: (j.arrival_tick, j.job_id))
+        return [j for k, j in enumerate(order) if k % world == rank]
     if placement != "lpt":
         raise ValueError(f"unknown placement {placement!r}")
     heap = [(0, r) for r in range(world)]       # (work so far, rank)

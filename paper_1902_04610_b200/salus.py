@@ -83,6 +83,7 @@ EXPORTS = ["salus_open", "salus_job_footprint", "salus_submit_job", "salus_meta_
            "salus_swap_bytes", "salus_set_swap", "salus_poll_stats", "salus_read_state"]
 
 _lib = None
+_POISONED: List[tuple] = []   # buffers of poisoned contexts, kept alive for the process
 
 
 def lib():
@@ -317,7 +318,10 @@ class Context:
 
     def close(self):
         if getattr(self, "ctx", None):
-            self.L.salus_close(self.ctx)
+            if self.L.salus_close(self.ctx) != 0:
+                # poisoned context (salus.h): a kernel that ignored the abort may
+                # still touch the arena / meta / swap -- never free them
+                _POISONED.append(tuple(getattr(self, k, None) for k in ("arena", "meta", "swap")))
             self.ctx = None
 
     def __del__(self):

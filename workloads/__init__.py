@@ -9,6 +9,6 @@ from .traces import (  # noqa: F401
     Job, TRAIN, INFER, PAGE_BYTES,
     pad128, footprint_bytes, algorithmic_flops, algorithmic_bytes, iter_ticks_for,
     make_job, c1_trace, c1_tie_trace, c2_trace, c3_trace, c4_trace, c5_trace,
-    partition, random_sched_trace, tiny_math_trace,
+    random_sched_trace, tiny_math_trace,
     to_jsonl, from_jsonl, trace_sha256,
 )

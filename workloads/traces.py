@@ -284,12 +284,6 @@ def c5_trace(n_jobs: int = 2000, seed: int = 5, burst: bool = True,
     return c4_trace(n_jobs=n_jobs, seed=seed, burst=burst, rate_scale=float(gpus))
 
 
-def partition(jobs: Sequence[Job], gpus: int, rank: int) -> List[Job]:
-    """the k-th job in (arrival, id) order goes to GPU k mod G."""
-    order = sorted(jobs, key=lambda j: (j.arrival_tick, j.job_id))
-    return [j for k, j in enumerate(order) if k % gpus == rank]
-
-
 # --------------------------------------------------------------------------
 # Small generators for property / parity tests
 # --------------------------------------------------------------------------
