@@ -33,6 +33,7 @@ from workloads import (TRAIN, algorithmic_bytes, algorithmic_flops, c2_trace,  #
                        c3_trace)
 
 METRIC = "aggregate iters/s at 1-8 B200; job-switch µs; avg JCT vs FIFO baseline"
+S_PACK = 2          # salus.h SALUS_PACK (the oracle uses the same numbering)
 UNIT = "iters/s"
 N_JOBS, N_ITERS = 300, 100
 
@@ -62,6 +63,89 @@ def peaks():
         return p["hbm_gbs"], p["bf16_tflops"], "measured"
     except Exception:  # noqa: BLE001
         return 6650.0, 1590.0, "fallback"
+
+
+def roofline_frac(jobs, seconds, gpus=1):
+    """SURVEY §8(d) reported fraction: the ideal perfectly-packed time,
+    sum over iterations of max(flops / tensor peak, bytes / HBM peak), over
+    the measured device time (peaks x G for G GPUs).  Peaks: the measured
+    burst figures of MEASURED_PEAKS.json."""
+    hbm, bf16, _ = peaks()
+    ideal = sum(j.n_iters * max(algorithmic_flops(j.kind, j.dims, j.batch) / (bf16 * 1e12),
+                                algorithmic_bytes(j.kind, j.dims, j.batch) / (hbm * 1e9)) for j in jobs)
+    return ideal / (seconds * gpus)
+
+
+def c5_section(S, local, rank, world, with_cpu_baseline):
+    """BASELINE configs[4] (C5): the 2000-job trace (burst, PACK, 16 GiB per
+    GPU) partitioned k mod N over the N ranks -- STRONG scaling, one
+    independent Salus instance per GPU, no data-path collective -- then one
+    NCCL all_gather of every job's completion record.  One
+    timed run: barrier + CUDA events on each rank, max over ranks.
+    Collective: every rank calls it."""
+    import torch
+    import torch.distributed as dist
+    from paper_1902_04610_b200 import metrics as PM, multigpu as MG
+    from workloads import c5_trace
+    jobs_all, cap = c5_trace()
+    mine = MG.partition_jobs(jobs_all, world, rank)
+    dev = f"cuda:{local}"
+    ctx = S.Context(mine, cap, S.PACK, device=local, log=False)
+    try:
+        stream = torch.cuda.current_stream(local)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        stats = ctx.run()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        rs = ctx.run_stats()
+    finally:
+        ctx.close()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    per_rank = [torch.zeros_like(t) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(per_rank, t)
+    else:
+        per_rank = [t]
+    per_rank = [float(x.item()) for x in per_rank]
+    ms_max = max(per_rank)
+    torch.cuda.synchronize()
+    ta = time.perf_counter()
+    merged = MG.gather_stats(stats, rank, world, device=dev, t0_ns=rs["wall_first_ns"])
+    torch.cuda.synchronize()
+    allgather_us = (time.perf_counter() - ta) * 1e6
+    # the FIFO baseline of the same partition: schedule only (logical ticks
+    # do not depend on the work executed), records gathered the same way
+    cf = S.Context(mine, cap, S.FIFO, device=local, log=False, null_work=True)
+    try:
+        fifo_merged = MG.gather_stats(cf.run(), rank, world, device=dev)
+    finally:
+        cf.close()
+    if rank != 0:
+        return None
+    iters = sum(j.n_iters for j in jobs_all)
+    logical = PM.summarize(jobs_all, merged)
+    fifo = PM.summarize(jobs_all, fifo_merged)
+    phys = [merged[j.job_id]["wall_end_rel_ns"] / 1e6 for j in jobs_all]
+    out = {"config": f"C5: {len(jobs_all)} jobs (C4 generator, seed 5, burst), PACK, 16 GiB per GPU, "
+                     f"partitioned k mod {world} (strong scaling)",
+           "gpus": world, "jobs": len(jobs_all), "iterations": iters,
+           "makespan_ms": ms_max, "per_rank_ms": per_rank,
+           "iters_per_s": iters / (ms_max / 1e3),
+           "roofline_frac": roofline_frac(jobs_all, ms_max / 1e3, world),
+           "avg_jct_ms": float(np.mean(phys)), "p95_jct_ms": float(np.percentile(phys, 95)),
+           **logical, "fifo_avg_jct_ticks": fifo["avg_jct_ticks"],
+           "avg_jct_fifo_over_pack": fifo["avg_jct_ticks"] / logical["avg_jct_ticks"],
+           "stats_allgathered": len(merged), "allgather_us": allgather_us,
+           "kernel_launches": world}
+    if with_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(jobs_all, cap, S_PACK, budget_s=10.0, iters_per_job=1)
+    return out
 
 
 class ClockSampler:
@@ -220,37 +304,27 @@ def c4_jct(S, device):
     arrivals, varied footprints, 16 GiB): the paper's headline "avg JCT vs
     FIFO" (PAPER.md tab:exp11; 3.19x on its private trace) as the
     device scheduler computes it, every iteration's GEMM work executed.  The
-    JCTs are logical (A17's iteration-cost model, bit-identical to the
-    oracle's; `log_matches_oracle` re-checks it here); the physical columns
-    are the measured kernel time of the whole trace under each policy."""
-    from oracle import metrics as OM, scheduler as OS
+    JCTs are logical (A17's iteration-cost model; the GPU tests hold the same
+    log byte-identical to the oracle's); the physical columns are the measured
+    kernel time of the whole trace under each policy."""
+    from paper_1902_04610_b200 import metrics as PM
     from workloads import c4_trace
     jobs, cap = c4_trace()
     flops = sum(j.n_iters * algorithmic_flops(j.kind, j.dims, j.batch) for j in jobs)
     byts = sum(j.n_iters * algorithmic_bytes(j.kind, j.dims, j.batch) for j in jobs)
-    hbm, bf16, _ = peaks()
     out = {"config": "C4: 100 jobs, widths 256-4096, depth 2-4, B 64-1024, n 10-2000, Poisson rho~1.2, 16 GiB",
            "iterations": sum(j.n_iters for j in jobs)}
     for name, pol in (("fifo", S.FIFO), ("srtf", S.SRTF), ("pack", S.PACK), ("fair", S.FAIR)):
-        ctx = S.Context(jobs, cap, pol, device=device, log=True)
+        ctx = S.Context(jobs, cap, pol, device=device, log=False)
         try:
             st = ctx.run()
             rs = ctx.run_stats()
-            log = ctx.log_bytes()
         finally:
             ctx.close()
-        ref = OS.simulate(jobs, cap, pol)
-
-        class _St:  # summarize() reads attributes
-            def __init__(self, d):
-                self.__dict__.update(d)
-        m = OM.summarize(jobs, {k: _St(v) for k, v in st.items()})
+        m = PM.summarize(jobs, st)
         ks = rs["kernel_ns"] / 1e9
-        out[name] = {"avg_jct_ticks": m["avg_jct"], "makespan_ticks": m["makespan"],
-                     "avg_queuing_ticks": m["avg_queuing"], "p95_jct_ticks": m["p95_jct"],
-                     "log_matches_oracle": log == ref.log_bytes(), "kernel_ms": ks * 1e3,
-                     "iters_per_s": rs["n_dispatch"] / ks,
-                     "roofline_frac": max(flops / (bf16 * 1e12), byts / (hbm * 1e9)) / ks}
+        out[name] = {**m, "kernel_ms": ks * 1e3, "iters_per_s": rs["n_dispatch"] / ks,
+                     "roofline_frac": roofline_frac(jobs, ks)}
     out["fifo_over_srtf_avg_jct"] = out["fifo"]["avg_jct_ticks"] / out["srtf"]["avg_jct_ticks"]
     out["paper_context"] = "3.19x avg JCT FIFO/SRTF on the paper's 100-job trace, 2x P100 (P:612-629)"
     return out
@@ -260,29 +334,23 @@ def c4e_evict(S, device):
     """SURVEY §8(f) NEXT-3 (reading A35): the C4 trace with 8x the
     declared persistent memory (C4e), so SRTF admission runs into the safety
     condition.  SRTF without and with eviction, every iteration executed:
-    logical average JCT (bit-identical to the oracle's log), and the swap
-    records the kernel executed -- persistent pages copied to pinned host
-    memory and back -- with their measured bandwidth."""
-    from oracle import metrics as OM, scheduler as OS
+    logical average JCT from the device's records, and the swap records the
+    kernel executed -- persistent pages copied to pinned host memory and
+    back -- with their measured bandwidth."""
+    from paper_1902_04610_b200 import metrics as PM
     from workloads import c4_trace
     jobs, cap = c4_trace(p_scale=8.0)
     out = {"config": "C4e: C4 with declared P x8 (0.89-6.6 GB), SRTF, 1 lane, 16 GiB"}
     for name, ev in (("srtf", False), ("srtf_evict", True)):
-        ctx = S.Context(jobs, cap, S.SRTF, device=device, log=True, evict=ev)
+        ctx = S.Context(jobs, cap, S.SRTF, device=device, log=False, evict=ev)
         try:
             st = ctx.run()
             rs = ctx.run_stats()
-            log = ctx.log_bytes()
         finally:
             ctx.close()
-        ref = OS.simulate(jobs, cap, OS.SRTF, evict=ev)
-
-        class _St:
-            def __init__(self, d):
-                self.__dict__.update(d)
-        m = OM.summarize(jobs, {k: _St(v) for k, v in st.items()})
-        r = {"avg_jct_ticks": m["avg_jct"], "makespan_ticks": m["makespan"],
-             "log_matches_oracle": log == ref.log_bytes(), "kernel_ms": rs["kernel_ns"] / 1e6}
+        m = PM.summarize(jobs, st)
+        r = {"avg_jct_ticks": m["avg_jct_ticks"], "makespan_ticks": m["makespan_ticks"],
+             "kernel_ms": rs["kernel_ns"] / 1e6}
         if ev:
             r.update({"n_swap_out": rs["n_swap_out"], "n_swap_in": rs["n_swap_in"],
                       "swap_gib": rs["swap_bytes"] / 2**30,
@@ -323,9 +391,7 @@ def c3_rate_sweep(S, device):
 def sched_rate(S, device):
     """SURVEY §8(d) C1 row "scheduler ns/event": the device scheduler alone
     (SALUS_FLAG_NULL_WORK: admission, lanes, pages, dispatch, no tiles) on
-    C2a, C3 and C4, against the CPU oracle's simulation of the same trace
-    (one host core, Python)."""
-    from oracle import scheduler as OS
+    C2a, C3 and C4 (the oracle's simulation speed is in cpu_baseline)."""
     from workloads import c4_trace
     out = {}
     for name, (jobs, cap), pol, ml in (("c2a_pack", c2_trace("a"), S.PACK, 0),
@@ -338,13 +404,9 @@ def sched_rate(S, device):
             rs = ctx.run_stats()
         finally:
             ctx.close()
-        t0 = time.perf_counter()
-        ref = OS.simulate(jobs, cap, pol, max_lanes=ml)
-        t_cpu = time.perf_counter() - t0
         out[name] = {"ticks": int(rs["n_ticks"]), "dispatches": int(rs["n_dispatch"]),
                      "device_ns_per_tick": rs["kernel_ns"] / rs["n_ticks"],
-                     "device_ns_per_dispatch": rs["kernel_ns"] / rs["n_dispatch"],
-                     "oracle_ns_per_tick": t_cpu * 1e9 / ref.n_ticks}
+                     "device_ns_per_dispatch": rs["kernel_ns"] / rs["n_dispatch"]}
     return out
 
 
@@ -469,59 +531,91 @@ def overhead_vs_standalone(S, device, dims=(1024, 1024, 1024, 1024), batch=256, 
             "standalone_torch_graph_iter_us": torch_us, "ratio": salus_us / torch_us}
 
 
-def cpu_baseline(jobs, cap, budget_s=12.0):
-    """The oracle as it stands, on this host's cores, on a bounded sample of
-    the same workload: the full schedule simulation plus as many fp64
-    iterations of the sweep's jobs as fit in ~budget_s."""
-    from threadpoolctl import threadpool_info
-    from oracle import layers as OL, scheduler as OS
+def _oracle_sample_worker(args):
+    """One process of the CPU baseline: fp64 oracle iterations (the oracle
+    as it stands) of its share of the sampled jobs, one BLAS thread, until
+    the deadline.  Returns (iterations, algorithmic flops, busy seconds)."""
+    job_list, iters_per_job, deadline = args
+    from threadpoolctl import threadpool_limits
+    from oracle import layers as OL
+    done, flops, busy = 0, 0, 0.0
+    with threadpool_limits(1):
+        for j in job_list:
+            if time.time() >= deadline:
+                break
+            W = OL.init_weights(j)
+            for k in range(min(iters_per_job, j.n_iters)):
+                if time.time() >= deadline:
+                    break
+                t0 = time.perf_counter()
+                if j.kind == TRAIN:
+                    OL.train_step(W, j, k)
+                else:
+                    OL.infer_step(W, j, k)
+                busy += time.perf_counter() - t0
+                done += 1
+                flops += algorithmic_flops(j.kind, j.dims, j.batch)
+    return done, flops, busy
+
+
+def cpu_baseline(jobs, cap, policy, budget_s=12.0, iters_per_job=2, seed=0):
+    """The oracle as it stands, timed on this host's cores (the cpu_baseline
+    leg: the only place bench.py runs oracle/): the full schedule simulation
+    of the workload (one core, Python) plus fp64 layer math of a bounded
+    sample -- a seeded shuffle of the jobs, `iters_per_job` iterations each,
+    spread over one process per core (one BLAS thread each) for ~budget_s --
+    extrapolated to every iteration of the workload by algorithmic flops."""
+    import multiprocessing as mp
+    from oracle import scheduler as OS
     t0 = time.perf_counter()
-    OS.simulate(jobs, cap, OS.PACK)
+    ref = OS.simulate(jobs, cap, policy)
     t_sched = time.perf_counter() - t0
-    done = 0
-    t0 = time.perf_counter()
-    W_cache = {}
-    for j in jobs:
-        W = W_cache.setdefault(j.job_id, OL.init_weights(j))
-        k = 0
-        while k < j.n_iters and time.perf_counter() - t0 < budget_s:
-            OL.train_step(W, j, k)
-            k += 1
-            done += 1
-        if time.perf_counter() - t0 >= budget_s:
-            break
-    t_math = time.perf_counter() - t0
+    cores = os.cpu_count() or 1
+    order = [jobs[i] for i in np.random.default_rng(seed).permutation(len(jobs))]
+    deadline = time.time() + budget_s
+    with mp.get_context("spawn").Pool(cores) as pool:
+        res = pool.map(_oracle_sample_worker, [(order[w::cores], iters_per_job, deadline) for w in range(cores)])
+    done = sum(r[0] for r in res)
+    rate = sum(r[1] / r[2] for r in res if r[2] > 0)            # flop/s over all cores
     total_iters = sum(j.n_iters for j in jobs)
-    per_iter = t_math / max(1, done)
-    value = total_iters / (t_sched + per_iter * total_iters)
-    threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    return {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-            "sample": f"full schedule simulation of {len(jobs)} jobs ({t_sched:.2f} s) + {done} fp64 "
-                      f"training iterations timed ({t_math:.1f} s), extrapolated to {total_iters} iterations"}
+    total_flops = sum(j.n_iters * algorithmic_flops(j.kind, j.dims, j.batch) for j in jobs)
+    t_math = total_flops / rate if rate > 0 else float("inf")
+    value = total_iters / (t_sched + t_math)
+    return {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"full schedule simulation of {len(jobs)} jobs / {ref.n_ticks} ticks ({t_sched:.2f} s, "
+                      f"1 core) + {done} fp64 iterations of a seeded job sample on {cores} processes x 1 BLAS "
+                      f"thread ({rate / 1e9:.1f} GFLOP/s aggregate), extrapolated by flops to {total_iters} "
+                      f"iterations ({t_math:.1f} s)",
+            "oracle_sched_ns_per_tick": t_sched * 1e9 / max(1, ref.n_ticks),
+            "extrapolated": True}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the oracle (CPU) is this tier's reference arm."""
+    """--impl reference: the oracle (CPU) is this tier's reference arm, timed
+    on the host's cores on the headline workload (C2a): W untimed warm-up
+    samples, then K timed steps, each a bounded sample of the workload."""
     if rank != 0:
         return
     jobs, cap = workload(1, 0)
     for _ in range(args.warmup):
-        pass
-    vals = []
+        cpu_baseline(jobs, cap, S_PACK, budget_s=1.0, iters_per_job=1, seed=99)
+    vals, cbs = [], []
     t_all = time.perf_counter()
-    for _ in range(args.steps):
-        cb = cpu_baseline(jobs, cap, budget_s=max(2.0, 20.0 / max(1, args.steps)))
+    for k in range(args.steps):
+        cb = cpu_baseline(jobs, cap, S_PACK, budget_s=max(3.0, 60.0 / max(1, args.steps)), seed=k)
         vals.append(cb["value"])
+        cbs.append(cb)
     value = float(np.mean(vals))
     elapsed = time.perf_counter() - t_all
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1000.0 * sum(j.n_iters for j in jobs) / value,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": "C2a sweep (oracle, CPU)", "jobs": len(jobs),
+            "data": "synthetic", "config": {"workload": "C2a hyper-parameter sweep (BASELINE configs[1]), "
+                                                        "oracle on CPU", "jobs": len(jobs),
                                             "iters_per_job": N_ITERS, "policy": "pack"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"], "kind": "oracle",
-                             "sample": cb["sample"]},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cbs[-1]["cores"], "kind": "oracle",
+                             "sample": cbs[-1]["sample"]},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": elapsed}
     print(json.dumps(line), flush=True)
@@ -558,6 +652,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="salus", choices=["salus", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c5", action="store_true", help="skip the C5 (2000-job) strong-scaling section")
     ap.add_argument("--only", default="",
                     help="comma list of side sections to run alone and print (c1,c2b,c3,c3rate,c4,evict,jct,online,overhead,sched)")
     args = ap.parse_args()
@@ -669,9 +764,17 @@ def main():
                 d = (int(r["start_ns"]) - int(prev["end_ns"])) / 1e3
                 (gap if prev["job"] == r["job"] else sw).append(d)
             last[ln] = r
-        from oracle import metrics as OM, scheduler as OS   # JCT vs the FIFO baseline (logical)
-        fifo = OM.summarize(jobs, OS.simulate(jobs, cap, OS.FIFO).stats)
-        pack = OM.summarize(jobs, OS.simulate(jobs, cap, OS.PACK).stats)
+        # JCT vs the FIFO baseline (logical ticks), both from the device's
+        # records: the timed PACK run and the same sweep under FIFO
+        # (schedule only, SALUS_FLAG_NULL_WORK: logical ticks do not depend
+        # on the work executed)
+        from paper_1902_04610_b200 import metrics as PM
+        cf = S.Context(jobs, cap, S.FIFO, device=local, log=False, null_work=True)
+        try:
+            fifo = PM.summarize(jobs, cf.run())
+        finally:
+            cf.close()
+        pack = PM.summarize(jobs, stats)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": max(3, args.warmup), "ms_per_step": ms_max, "higher_is_better": True,
@@ -696,13 +799,16 @@ def main():
                           "p99": float(np.percentile(sw, 99)) if sw else None},
             "iter_gap_us": {"n": len(gap), "p50": float(np.median(gap)) if gap else None,
                             "p99": float(np.percentile(gap, 99)) if gap else None},
-            "jct": {"avg_fifo_ticks": fifo["avg_jct"], "avg_pack_ticks": pack["avg_jct"],
-                    "fifo_over_pack": fifo["avg_jct"] / pack["avg_jct"],
-                    "makespan_fifo_over_pack": fifo["makespan"] / pack["makespan"]},
+            "jct": {"source": "device per-job records (FIFO: schedule-only run; PACK: the logged run)",
+                    "avg_fifo_ticks": fifo["avg_jct_ticks"], "avg_pack_ticks": pack["avg_jct_ticks"],
+                    "fifo_over_pack": fifo["avg_jct_ticks"] / pack["avg_jct_ticks"],
+                    "makespan_fifo_over_pack": fifo["makespan_ticks"] / pack["makespan_ticks"]},
             "stats_allgathered": len(all_stats), "allgather_us": allgather_us,
             "sched_wait_frac": rs0["sched_wait_ns"] / max(1, rs0["kernel_ns"]),
         }
-        for k in SIDE_SECTIONS:
+        # single-GPU side measurements: at N = 1 only (the other ranks would
+        # otherwise wait minutes at the C5 barrier)
+        for k in (SIDE_SECTIONS if world == 1 else ()):
             line[SIDE_SECTIONS[k][0]] = side_section(k, S, local, jobs, cap)
         # the paper's figures (2x P100, TF 1.5, private traces) beside ours: context only
         try:
@@ -719,9 +825,15 @@ def main():
         except Exception as exc:  # noqa: BLE001
             line["paper_context"] = {"error": str(exc)[:200]}
         if not args.no_cpu_baseline and world == 1:
-            line["cpu_baseline"] = cpu_baseline(jobs, cap)
-        print(json.dumps(line), flush=True)
+            line["cpu_baseline"] = cpu_baseline(jobs, cap, S_PACK)
     ctx.close()
+    # C5 (configs[4], the metric's multi-GPU config): every rank takes part
+    if not args.no_c5:
+        c5 = c5_section(S, local, rank, world, with_cpu_baseline=(not args.no_cpu_baseline and world == 1))
+        if rank == 0:
+            line["c5"] = c5
+    if rank == 0:
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

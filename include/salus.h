@@ -88,6 +88,9 @@ enum {
 enum {
   SALUS_DUMP_OUTPUTS = 1,    /* keep fp32 A_L of every iteration / request       */
   SALUS_DUMP_WEIGHTS = 2,    /* keep fp32 master weights after the last iteration */
+  SALUS_DUMP_WEIGHT_STEPS = 8, /* keep fp32 master weights after EVERY iteration
+                                (parity checks of each step from the kernel's own
+                                state; n_iters x the weight count floats)        */
   SALUS_DUMP_STATE = 4       /* migration: when the job
                                 finishes, the kernel copies its persistent device
                                 state (the opaque image salus_read_state returns)
@@ -347,6 +350,9 @@ int salus_read_wall(salus_ctx *ctx, salus_wall_rec *buf, uint64_t cap_recs, uint
  *   iter <  n_iters   : A_L of that iteration/request, batch x d_L row-major
  *   iter == 0xFFFFFFFF: final weights W_1..W_L concatenated, each
  *                       d_{l-1} x d_l row-major (Z = A W orientation)
+ *                       (SALUS_DUMP_WEIGHTS or SALUS_DUMP_WEIGHT_STEPS)
+ *   iter == 0x80000000 | k (k < n_iters, SALUS_DUMP_WEIGHT_STEPS): the
+ *                       weights after iteration k, same layout
  * *n = floats written.  E_INVAL if the job did not dump that item. */
 int salus_read_layers(salus_ctx *ctx, uint32_t job_id, uint32_t iter, float *buf,
                       uint64_t cap_floats, uint64_t *n);

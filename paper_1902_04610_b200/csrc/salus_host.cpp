@@ -245,8 +245,13 @@ int salus_submit_job(salus_ctx *ctx, const salus_job *job) {
   if (ctx->jobs.size() >= ctx->cfg.max_jobs) return fail(ctx, SALUS_E_CAPACITY, "max_jobs reached");
   uint64_t df = 0;
   if (job->dump & SALUS_DUMP_OUTPUTS) df += (uint64_t)job->n_iters * job->batch * job->dims[job->n_layers];
-  if (job->dump & SALUS_DUMP_WEIGHTS)
-    for (uint32_t l = 1; l <= job->n_layers; l++) df += (uint64_t)job->dims[l - 1] * job->dims[l];
+  if (job->dump & (SALUS_DUMP_WEIGHTS | SALUS_DUMP_WEIGHT_STEPS)) {
+    uint64_t wc = 0;
+    for (uint32_t l = 1; l <= job->n_layers; l++) wc += (uint64_t)job->dims[l - 1] * job->dims[l];
+    df += (job->dump & SALUS_DUMP_WEIGHT_STEPS) ? wc * job->n_iters : wc;
+  }
+  if ((job->dump & SALUS_DUMP_WEIGHT_STEPS) && job->kind != SALUS_TRAIN)
+    return fail(ctx, SALUS_E_INVAL, "SALUS_DUMP_WEIGHT_STEPS is for TRAIN jobs");
   if (ctx->cfg.dump_bytes && (ctx->dump_floats + df) * 4 > ctx->cfg.dump_bytes)
     return fail(ctx, SALUS_E_CAPACITY, "dump_bytes exceeded");
   HostJob h;
@@ -345,8 +350,10 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
     D.dump_out_off = dump_cur;
     if (j.dump & SALUS_DUMP_OUTPUTS) dump_cur += (uint64_t)j.n_iters * j.batch * j.dims[L];
     D.dump_w_off = dump_cur;
-    if (j.dump & SALUS_DUMP_WEIGHTS)
-      for (uint32_t l = 1; l <= L; l++) dump_cur += (uint64_t)j.dims[l - 1] * j.dims[l];
+    D.w_count = 0;
+    for (uint32_t l = 1; l <= L; l++) D.w_count += (uint64_t)j.dims[l - 1] * j.dims[l];
+    if (j.dump & SALUS_DUMP_WEIGHT_STEPS) dump_cur += D.w_count * j.n_iters;
+    else if (j.dump & SALUS_DUMP_WEIGHTS) dump_cur += D.w_count;
 }
 
 static void compute_layout(salus_ctx *c) {
@@ -886,11 +893,17 @@ int salus_read_layers(salus_ctx *ctx, uint32_t job_id, uint32_t iter, float *buf
   if (it == ctx->id_to_dense.end()) return fail(ctx, SALUS_E_INVAL, "unknown job");
   const DevJob &D = ctx->djobs[it->second];
   uint64_t off, cnt;
+  const bool steps = (D.dump & SALUS_DUMP_WEIGHT_STEPS) != 0;
   if (iter == 0xFFFFFFFFu) {
-    if (!(D.dump & SALUS_DUMP_WEIGHTS)) return fail(ctx, SALUS_E_INVAL, "job did not dump weights");
-    off = D.dump_w_off;
-    cnt = 0;
-    for (uint32_t l = 1; l <= D.n_layers; l++) cnt += (uint64_t)D.dims[l - 1] * D.dims[l];
+    if (!(D.dump & (SALUS_DUMP_WEIGHTS | SALUS_DUMP_WEIGHT_STEPS)))
+      return fail(ctx, SALUS_E_INVAL, "job did not dump weights");
+    cnt = D.w_count;
+    off = D.dump_w_off + (steps ? (uint64_t)(D.n_iters - 1) * cnt : 0);
+  } else if (iter & 0x80000000u) {
+    const uint32_t k = iter & 0x7FFFFFFFu;
+    if (!steps || k >= D.n_iters) return fail(ctx, SALUS_E_INVAL, "no such weight step (SALUS_DUMP_WEIGHT_STEPS)");
+    cnt = D.w_count;
+    off = D.dump_w_off + (uint64_t)k * cnt;
   } else {
     if (!(D.dump & SALUS_DUMP_OUTPUTS) || iter >= D.n_iters) return fail(ctx, SALUS_E_INVAL, "no such output");
     cnt = (uint64_t)D.batch * D.dims[D.n_layers];

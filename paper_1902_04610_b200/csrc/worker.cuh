@@ -370,8 +370,9 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
         for (uint32_t q = 0; q < N / 64; q++)
           defer(td, PTR_AUX + q, jt, J.wb_off[l - 1][(kg + 1) & 1] + (td.n0 / 64 + q) * J.dpad[l] * 128u + mb * 16384u);
       }
-      if (td.valid && (J.dump & SALUS_DUMP_WEIGHTS) && k + 1 == J.n_iters) {
-        uint64_t base = J.dump_w_off;
+      const bool wsteps = (J.dump & SALUS_DUMP_WEIGHT_STEPS) != 0;
+      if (td.valid && (wsteps || ((J.dump & SALUS_DUMP_WEIGHTS) && k + 1 == J.n_iters))) {
+        uint64_t base = J.dump_w_off + (wsteps ? (uint64_t)k * J.w_count : 0);
         for (uint32_t q = 1; q < l; q++) base += (uint64_t)J.dims[q - 1] * J.dims[q];
         td.dump_off = (int64_t)base;
       }

@@ -13,29 +13,34 @@ from typing import Dict, Iterable
 
 import numpy as np
 
-# one int64 record per job: job_id, first_lane, admit, first_start, completion, completion_seq, rank
+# one int64 record per job: job_id, first_lane, admit, first_start, completion,
+# completion_seq, rank, and the physical end of its last iteration relative to
+# its rank's kernel start (ns; -1 if the caller gave no start stamp)
 REC_FIELDS = ("job_id", "first_lane", "admit_tick", "first_start_tick", "completion_tick",
-              "completion_seq", "rank")
+              "completion_seq", "rank", "wall_end_rel_ns")
 
 
-def pack_stats(stats: Dict[int, dict], rank: int, n_pad: int):
-    """{job_id: stat dict} -> int64 array [n_pad, 7], padded with job_id -1."""
+def pack_stats(stats: Dict[int, dict], rank: int, n_pad: int, t0_ns=None):
+    """{job_id: stat dict} -> int64 array [n_pad, 8], padded with job_id -1."""
     out = np.full((n_pad, len(REC_FIELDS)), -1, dtype=np.int64)
     for i, jid in enumerate(sorted(stats)):
         s = stats[jid]
+        rel = int(s["wall_end_ns"]) - int(t0_ns) if t0_ns is not None and "wall_end_ns" in s else -1
         out[i] = (s["job_id"], s["first_lane"], s["admit_tick"], s["first_start_tick"],
-                  s["completion_tick"], np.int64(np.uint64(s["completion_seq"]).astype(np.int64)), rank)
+                  s["completion_tick"], np.int64(np.uint64(s["completion_seq"]).astype(np.int64)), rank, rel)
     return out
 
 
-def gather_stats(stats: Dict[int, dict], rank: int, world: int, device=None) -> Dict[int, dict]:
-    """All-gather every rank's per-job records; returns the merged dict."""
+def gather_stats(stats: Dict[int, dict], rank: int, world: int, device=None, t0_ns=None) -> Dict[int, dict]:
+    """All-gather every rank's per-job records; returns the merged dict.
+    `t0_ns` (this rank's kernel start, globaltimer) turns each job's
+    wall_end_ns into a rank-relative physical completion time."""
     import torch
     import torch.distributed as dist
     n = torch.tensor([len(stats)], dtype=torch.int64, device=device)
     if world > 1:
         dist.all_reduce(n, op=dist.ReduceOp.MAX)
-    rec = torch.from_numpy(pack_stats(stats, rank, int(n.item()))).to(device)
+    rec = torch.from_numpy(pack_stats(stats, rank, int(n.item()), t0_ns)).to(device)
     parts = [torch.empty_like(rec) for _ in range(world)]
     if world > 1:
         dist.all_gather(parts, rec)

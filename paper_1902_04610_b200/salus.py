@@ -20,8 +20,13 @@ LIB_PATH = os.environ.get("SALUS_LIB", os.path.join(HERE, "libsalus.so"))
 FIFO, SRTF, PACK, FAIR = 0, 1, 2, 3
 TRAIN, INFER = 0, 1
 FLAG_LOG, FLAG_NULL_WORK, FLAG_CHECK, FLAG_TRACE, FLAG_ONLINE, FLAG_EVICT = 1, 2, 4, 8, 16, 32
-DUMP_OUTPUTS, DUMP_WEIGHTS, DUMP_STATE = 1, 2, 4
+DUMP_OUTPUTS, DUMP_WEIGHTS, DUMP_STATE, DUMP_WEIGHT_STEPS = 1, 2, 4, 8
 WEIGHTS = 0xFFFFFFFF
+
+
+def weights_after(k: int) -> int:
+    """salus_read_layers index of the weights after iteration k (DUMP_WEIGHT_STEPS)."""
+    return 0x80000000 | int(k)
 
 ERRORS = {-1: "E_INVAL", -2: "E_DUPLICATE", -3: "E_UNSCHEDULABLE", -4: "E_STATE",
           -5: "E_CAPACITY", -6: "E_CUDA", -7: "E_STUCK", -8: "E_TIMEOUT"}

@@ -98,6 +98,9 @@ def test_submit_errors(L):
     inf = make_job(5, INFER, 10, (128, 128), 1, 2, iter_ticks=5, request_ticks=(12, 11))
     d, keep = S.job_desc(inf)
     assert L.salus_submit_job(ctx, C.byref(d)) == -1                 # unsorted requests
+    inf = make_job(6, INFER, 10, (128, 128), 1, 2, iter_ticks=5, request_ticks=(11, 12))
+    d, keep = S.job_desc(inf, dump=S.DUMP_WEIGHT_STEPS)
+    assert L.salus_submit_job(ctx, C.byref(d)) == -1                 # weight steps: TRAIN only
     n = C.c_uint64()
     assert L.salus_meta_bytes(ctx, C.byref(n)) == 0 and n.value > 0
     assert L.salus_run(ctx, None, 0, None) == -4                     # not prepared

@@ -77,3 +77,20 @@ def test_random_traces(policy):
         ml = int(rng.integers(1, 9)) if policy != OS.FIFO else 0
         assert_schedule_parity(jobs, cap, policy, max_lanes=ml,
                                switch_ticks=int(rng.integers(0, 3)), check=True)[0].close()
+
+
+def test_fair_a28_hand_trace():
+    """The hand-worked FAIR trace pinning A28 (tests/golden/hand_traces.json
+    HW_FAIR_A28): the device scheduler's log equals the oracle's, whose
+    dispatches tests/test_oracle_sched.py holds to the hand-worked ones."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(__file__))
+    from test_oracle_sched import _gold, fair_a28_jobs
+    from workloads import PAGE_BYTES
+    want = _gold("hand_traces.json")["HW_FAIR_A28"]["dispatch"]
+    for real in (False, True):
+        ctx, ref, stats = assert_schedule_parity(fair_a28_jobs(real), 64 * PAGE_BYTES, OS.FAIR,
+                                                 null_work=not real, check=True)
+        ctx.close()
+        assert [[t, job, it] for seq, t, lane, job, it, end in ref.dispatch] == want

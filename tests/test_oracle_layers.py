@@ -154,3 +154,50 @@ def test_bf16_storage_equals_fp64_when_everything_is_representable():
     assert np.array_equal(LY.forward(W, X, LY.bf16)[-1], LY.forward(W, X)[-1])
     _, d16 = LY.gradients(W, X, T, LY.bf16)
     assert np.array_equal(d16[0], X.T @ LY.bf16((X @ W[0] - T) / 5))
+
+
+def test_bf16_storage_mask_flip_hand_worked():
+    """Reading A31 pinned by a 3-layer example worked by hand (exact binary
+    fractions), in which storing A_1 in bf16 flips the ReLU mask of layer 2.
+
+      dims (2, 2, 1, 1), B = 1, X = [1+2^-7, 1], T = [1], lr = 1/2
+      W_1 = diag(1+2^-7, 1+2^-6),  W_2 = [1, -1]^T,  W_3 = [1+2^-9]
+
+    fp64:  Z_1 = [1+2^-6+2^-14, 1+2^-6],  Z_2 = 2^-14 > 0,  A_3 = 2^-14 (1+2^-9),
+           G_3 = A_3 - 1,  G_2 = G_3 (1+2^-9),  G_1 = [G_2, -G_2]
+    bf16:  A_1 = bf16(Z_1) = [1+2^-6, 1+2^-6] (2^-14 is below half an ulp),
+           Z_2 = 0 -> mask [A_2 > 0] = 0;  the W_3 copy is bf16(1+2^-9) = 1,
+           so A_3 = 0, G_3 = -1 and every other gradient is 0: the step
+           leaves W_1, W_2, W_3 unchanged (the fp64 master is untouched).
+    Fails if the activation storage rounding, the weight-copy rounding or
+    the mask placement of the bf16 mode were dropped or moved."""
+    from fractions import Fraction as F
+    u7, u6, u9, u14 = F(1, 2**7), F(1, 2**6), F(1, 2**9), F(1, 2**14)
+    X = np.array([[float(1 + u7), 1.0]])
+    T = np.array([[1.0]])
+    W = [np.diag([float(1 + u7), float(1 + u6)]), np.array([[1.0], [-1.0]]), np.array([[float(1 + u9)]])]
+    # fp64 definition
+    A, dW = LY.gradients(W, X, T)
+    z1 = [(1 + u7) ** 2, 1 + u6]
+    a3 = u14 * (1 + u9)
+    g3 = a3 - 1
+    g2 = g3 * (1 + u9)
+    exp_dW = [[[(1 + u7) * g2, -(1 + u7) * g2], [g2, -g2]], [[z1[0] * g2], [z1[1] * g2]], [[u14 * g3]]]
+    assert [float(x) for x in A[1].ravel()] == [float(z) for z in z1]
+    assert float(A[2][0, 0]) == float(u14) and float(A[3][0, 0]) == float(a3)
+    for got, exp in zip(dW, exp_dW):
+        e = np.array([[float(v) for v in row] for row in exp])
+        assert np.allclose(got, e, rtol=1e-15, atol=0), (got, e)
+    # bf16-storage mode: the mask flips and every update vanishes
+    A16, dW16 = LY.gradients(W, X, T, LY.bf16)
+    assert list(A16[1].ravel()) == [float(1 + u6)] * 2
+    assert A16[2][0, 0] == 0.0 and A16[3][0, 0] == 0.0
+    assert all(np.all(d == 0.0) for d in dW16)
+    job = make_job(0, TRAIN, 0, (2, 2, 1, 1), 1, 1, lr=0.5)
+    W16 = [w.copy() for w in W]
+    _, d16 = LY.gradients(W16, X, T, LY.bf16)
+    for w, d in zip(W16, d16):
+        w -= np.float32(job.lr) * d
+    assert all(np.array_equal(a, b) for a, b in zip(W16, W))
+    # fp64 step moves W_1 by -lr * dW_1 exactly
+    assert float(W[0][0, 0] - 0.5 * dW[0][0, 0]) == float(1 + u7 - F(1, 2) * (1 + u7) * g2)

@@ -356,3 +356,28 @@ def test_pack_beats_fifo_makespan_when_memory_allows():
     fifo = M.summarize(jobs, S.simulate(jobs, 64 * G, S.FIFO).stats)["makespan"]
     pack = M.summarize(jobs, S.simulate(jobs, 64 * G, S.PACK).stats)["makespan"]
     assert fifo == 400 and pack == 50
+
+
+def fair_a28_jobs(real_work=False):
+    """The hand trace HW_FAIR_A28 (tests/golden/hand_traces.json).  With
+    real_work the declared sizes are the device footprints (all still fit
+    one lane, so the dispatches are the same)."""
+    G = PAGE_BYTES
+    spec = _gold("hand_traces.json")["HW_FAIR_A28"]["jobs"]
+    sz = {} if real_work else {"persistent_bytes": G, "ephemeral_bytes": G}
+    return [make_job(j, TRAIN if kind == "train" else INFER, a, (128, 128), 128, n, iter_ticks=c,
+                     request_ticks=tuple(req), **sz)
+            for j, (kind, a, n, c, req) in enumerate(spec)]
+
+
+def test_fair_idle_inference_reentry_a28():
+    """A28 pinned by a hand-worked FAIR trace: an inference job that
+    went idle re-enters at the min service of its lane's runnable
+    co-residents; the golden file lists which mutation of the rule changes
+    which dispatch."""
+    g = _gold("hand_traces.json")["HW_FAIR_A28"]
+    jobs = fair_a28_jobs()
+    res = S.simulate(jobs, 64 * PAGE_BYTES, S.FAIR, check_invariants=True)
+    assert [[t, job, it] for seq, t, lane, job, it, end in res.dispatch] == g["dispatch"]
+    assert {str(k): v.completion_tick for k, v in res.stats.items()} == g["completion"]
+    assert {d[2] for d in res.dispatch} == {0}          # one lane for life (A9, I6)
