@@ -26,6 +26,10 @@ int max_coresident_grid(int device, int *grid);
 
 using namespace salus;
 
+#ifndef SALUS_DEFAULT_EAGER_LANES
+#define SALUS_DEFAULT_EAGER_LANES 64
+#endif
+
 namespace {
 
 inline uint64_t pad128(uint64_t x) { return (x + 127) / 128 * 128; }
@@ -589,6 +593,11 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   P.flags = ctx->cfg.flags;
   P.n_workers = ctx->grid / 2 - 1;
   P.switch_ticks = (int64_t)ctx->cfg.switch_ticks;
+  {   // eager stage publication (latency mode) while few lanes are open; the
+      // SALUS_EAGER_LANES environment variable overrides (0 = never)
+    const char *ev = getenv("SALUS_EAGER_LANES");
+    P.eager_lanes = ev ? (uint32_t)atoi(ev) : SALUS_DEFAULT_EAGER_LANES;
+  }
   P.timeout_ns = (uint64_t)ctx->cfg.timeout_ms * 1000000ull;
   P.live = nullptr;
   P.max_jobs = ctx->cfg.max_jobs;

@@ -837,7 +837,8 @@ struct Sched {
     if (tid == 0) {
       volatile DispRec *vr = &sl.recs[tl % RQ];
       vr->job = j; vr->iter = S.done[j]; vr->seq = pseq; vr->lseq = seq; vr->lane_id = lane_id;
-      vr->kind = kind | ((kind == REC_ITER && S.xpre[j]) ? REC_FLAG_XPRE : 0u);
+      vr->kind = kind | ((kind == REC_ITER && S.xpre[j]) ? REC_FLAG_XPRE : 0u) |
+                 ((kind == REC_ITER && nl <= P.eager_lanes) ? REC_FLAG_EAGER : 0u);
       vr->append_ns = ptx::globaltimer();
       // publish (release) and learn whether the slot was idle in one atomic;
       // only the scheduler ever sets `running`, so taking it needs no CAS
@@ -850,17 +851,25 @@ struct Sched {
     __syncwarp();
     won = __shfl_sync(0xffffffffu, won, 0);
     if (!won) return;
-    uint32_t got = 0, first = 0, jj = 0;
+    uint32_t got = 0, first = 0, second = NONE32, jj = 0;
     if (tid == 0) {
       DispRec r;
       got = take_next(sl, &r);
-      if (got) { first = begin_iteration(sl, r, P.jobs); jj = r.job; }
+      if (got) {
+        first = begin_iteration(sl, r, P.jobs);
+        jj = r.job;
+        second = eager_second(P.jobs[jj], r.kind, first);
+      }
     }
     got = __shfl_sync(0xffffffffu, got, 0);
     if (!got) return;
     first = __shfl_sync(0xffffffffu, first, 0);
+    second = __shfl_sync(0xffffffffu, second, 0);
     jj = __shfl_sync(0xffffffffu, jj, 0);
     enqueue(slot, first, stage_ntiles(P.jobs[jj], first));
+    // eager: the second stage's tiles go behind the first's (higher ring
+    // positions), so every tile's dependency sits at a lower position
+    if (second != NONE32) enqueue(slot, second, stage_ntiles(P.jobs[jj], second));
   }
 
   // End of the schedule: wait for every slot to drain its ring.

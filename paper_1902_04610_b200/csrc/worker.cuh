@@ -95,7 +95,11 @@ struct OpDesc {
 
 
 struct TileDesc {
+  // next_stage / next_ntiles: the stage this one's completion publishes (its
+  // successor; eager records: the successor's successor, 0 tiles if none)
   uint32_t kind, payload, slot, stage, job, iter, ntiles, next_ntiles, is_last, first_stage, next_stage;
+  uint8_t eager, wait, dep_stage, pad8;   // eager record; wait for stage dep_stage (dep_want counts)
+  uint32_t dep_want;
   uint32_t valid;          // this CTA's half exists (odd block counts leave the peer's empty)
   uint32_t peer_valid;     // the pair's second M block exists
   uint32_t peer_nca;       // (leader) A copies per K-chunk of the peer CTA
@@ -244,16 +248,29 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
                             TileDesc &td, uint32_t h) {
   td.payload = payload;
   const uint32_t slot = payload >> 26, stage = (payload >> 21) & 31u, tile = payload & ((1u << 21) - 1);
-  const uint32_t k = sl.iter;                         // this context's iteration index
+  const uint32_t k = sl.iter & ~ITER_EAGER_BIT;       // this context's iteration index
   const uint32_t kg = k + J.iter_base;                // the job's own (migration, NEXT-4)
   const uint32_t L = J.n_layers, bp = J.bpad;
   td.slot = slot; td.stage = stage; td.job = sl.job; td.iter = k; td.seq = sl.seq; td.lseq = sl.lseq;
+  td.eager = 0; td.wait = 0;
   td.ntiles = stage_ntiles(J, stage);
   td.is_last = stage >= STAGE_SWAP_OUT || stage == last_stage(J.kind, L);
-  td.next_stage = td.is_last ? 0 : next_stage(J, stage);
-  td.next_ntiles = td.is_last ? 0 : J.stage_tiles[td.next_stage];
   td.first_stage = stage >= STAGE_SWAP_OUT ? stage
                    : (k == 0 && !(J.dump & DUMP_INTERNAL_RESUME)) ? 0u : (J.xpre ? 2u : 1u);
+  td.eager = (sl.iter & ITER_EAGER_BIT) != 0 && stage < STAGE_SWAP_OUT;
+  td.next_stage = td.is_last ? 0 : next_stage(J, stage);
+  if (td.eager && !td.is_last) {
+    // the successor was published with this stage: publish the one after it
+    td.next_stage = td.next_stage == last_stage(J.kind, L) ? 0 : next_stage(J, td.next_stage);
+    td.next_ntiles = td.next_stage ? J.stage_tiles[td.next_stage] : 0;
+  } else {
+    td.next_ntiles = td.is_last ? 0 : J.stage_tiles[td.next_stage];
+  }
+  // every stage of an eager record but its first was published while its
+  // predecessor ran: wait for it before touching what it produces
+  td.wait = td.eager && stage != td.first_stage;
+  td.dep_stage = td.wait ? (uint8_t)prev_stage(J, stage) : 0;
+  td.dep_want = td.wait ? 2 * stage_ntiles(J, td.dep_stage) : 0;
   td.dump_off = -1;
   td.n_ech = 0;
   td.xt_mask = 0;
@@ -741,6 +758,24 @@ __device__ __forceinline__ int32_t tma_row(uint32_t page, uint32_t off) {
   return (int32_t)((page << (PAGE_SHIFT - 7)) + ((off & (PAGE_BYTES - 1)) >> 7));
 }
 
+// Eager records (REC_FLAG_EAGER): block until the slot's stage `stage` has
+// completed (`want` = its pair tasks x 2 CTA halves), then make the
+// producers' generic-proxy stores visible to this CTA's async-proxy (TMA)
+// reads.  Spins relaxed (an acquire load per spin would invalidate L1),
+// then one acquire load, like the decoder's ring poll.
+__device__ __forceinline__ void wait_stage(const Params &P, uint32_t slot, uint32_t stage, uint32_t want) {
+  const uint32_t *c = &P.slots[slot].stage_done[stage];
+  uint32_t spins = 0;
+  for (;;) {
+    uint32_t v;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    if (v >= want) break;
+    if ((++spins & 4095u) == 0 && *(volatile uint32_t *)&P.ctrl->abort) __trap();
+  }
+  (void)ld_acquire_u32(c);
+  ptx::fence_proxy_async_global();
+}
+
 // Operand loader (1 thread).  The page-table reads of chunk kc + 2 are issued
 // before the copies of chunk kc, so their latency (an L2 round trip: the
 // completion warp's gpu-scope fences keep invalidating L1) is off the
@@ -766,9 +801,37 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W, uint32_t h) {
 #else
       const uint64_t pol_a = normal, pol_b = normal;
 #endif
-      ChunkPages p0 = chunk_pages(a, b, nca, ncb, 0);
-      ChunkPages p1 = nk > 1 ? chunk_pages(a, b, nca, ncb, 1) : p0;
-      for (uint32_t kc = 0; kc < nk; kc++) {
+      const void *ta = ab == 16384u ? (const void *)&P.tmap16 : (const void *)&P.tmap8;
+      const void *tb = bb == 16384u ? (const void *)&P.tmap16 : (const void *)&P.tmap8;
+      // eager (td.wait): operand A is what the previous stage produces.  The
+      // first `pre` chunks' stages are armed and their B (weights /
+      // activations of earlier stages) issued before the wait; their A after.
+      const uint32_t pre = (td.wait && nca > 0) ? min(nk, PIPE) : 0;
+      if (pre) {
+        uint32_t s2 = s, ph2 = s_phase;
+        ChunkPages pg[PIPE];
+        for (uint32_t kc = 0; kc < pre; kc++) {
+          pg[kc] = chunk_pages(a, b, nca, ncb, kc);
+          ptx::mbar_wait_abortable(&W.empty[s2], ph2 ^ 1, &P.ctrl->abort);
+          const uint32_t bar = ptx::mapa(&W.full[s2], 0);
+          if (h == 0) ptx::mbar_arrive_expect_tx(&W.full[s2], tx_pair);
+          uint8_t *sb = W.stage[s2] + STAGE_A_BYTES;
+          if (ncb > 0) ptx::tma_load_2d_pair(sb, tb, 0, tma_row(pg[kc].b0, copy_off(b, kc, 0)), bar, pol_b);
+          if (ncb > 1) ptx::tma_load_2d_pair(sb + bb, tb, 0, tma_row(pg[kc].b1, copy_off(b, kc, 1)), bar, pol_b);
+          if (++s2 == PIPE) { s2 = 0; ph2 ^= 1; }
+        }
+        wait_stage(P, td.slot, td.dep_stage, td.dep_want);
+        for (uint32_t kc = 0; kc < pre; kc++) {
+          const uint32_t bar = ptx::mapa(&W.full[s], 0);
+          uint8_t *sa = W.stage[s];
+          ptx::tma_load_2d_pair(sa, ta, 0, tma_row(pg[kc].a0, copy_off(a, kc, 0)), bar, pol_a);
+          if (nca > 1) ptx::tma_load_2d_pair(sa + ab, ta, 0, tma_row(pg[kc].a1, copy_off(a, kc, 1)), bar, pol_a);
+          if (++s == PIPE) { s = 0; s_phase ^= 1; }
+        }
+      }
+      ChunkPages p0 = pre < nk ? chunk_pages(a, b, nca, ncb, pre) : ChunkPages{0, 0, 0, 0};
+      ChunkPages p1 = pre + 1 < nk ? chunk_pages(a, b, nca, ncb, pre + 1) : p0;
+      for (uint32_t kc = pre; kc < nk; kc++) {
         const ChunkPages cur = p0;
         p0 = p1;
         if (kc + 2 < nk) p1 = chunk_pages(a, b, nca, ncb, kc + 2);
@@ -781,8 +844,6 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W, uint32_t h) {
         const uint32_t bar = ptx::mapa(&W.full[s], 0);
         if (h == 0) ptx::mbar_arrive_expect_tx(&W.full[s], tx_pair);
         uint8_t *sa = W.stage[s], *sb = W.stage[s] + STAGE_A_BYTES;
-        const void *ta = ab == 16384u ? (const void *)&P.tmap16 : (const void *)&P.tmap8;
-        const void *tb = bb == 16384u ? (const void *)&P.tmap16 : (const void *)&P.tmap8;
         if (nca > 0) ptx::tma_load_2d_pair(sa, ta, 0, tma_row(cur.a0, copy_off(a, kc, 0)), bar, pol_a);
         if (nca > 1) ptx::tma_load_2d_pair(sa + ab, ta, 0, tma_row(cur.a1, copy_off(a, kc, 1)), bar, pol_a);
         if (ncb > 0) ptx::tma_load_2d_pair(sb, tb, 0, tma_row(cur.b0, copy_off(b, kc, 0)), bar, pol_b);
@@ -822,6 +883,11 @@ __device__ void epi_loader(const Params &P, WorkerSmem &W, uint32_t h) {
     if (td.kind == T_GEMM) {
       const uint32_t n = td.n_ech;
       const bool sgd = td.epi == EPI_SGD;
+      // eager: every epilogue input was produced before the predecessor
+      // stage began (earlier stages or iterations), except the prefetched
+      // targets T_0 of a 1-layer GEN-prefetch job, which its INIT stage --
+      // the loss stage's own predecessor -- generates
+      if (td.wait && td.epi == EPI_LOSS && n && td.iter == 0) wait_stage(P, td.slot, td.dep_stage, td.dep_want);
       for (uint32_t c = 0; c < n; c++) {
         ptx::mbar_wait_abortable(&W.epi_empty[e], e_phase ^ 1, &P.ctrl->abort);
         ptx::mbar_arrive_expect_tx(&W.epi_full[e], ECH_BYTES);
@@ -953,10 +1019,13 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
     } else if (!td.valid) {
     } else if (td.kind == T_COPY) {
       copy_page(td, et);
-    } else if (td.kind == T_INIT) {
-      init_tile(td, r, h);
     } else {
-      gen_tile(td, r, h);
+      if (td.wait) {   // eager: a GEN tile of a non-first stage completes only after its predecessor
+        if (et == 0) wait_stage(P, td.slot, td.dep_stage, td.dep_want);
+        named_bar(1, EPI_THREADS);
+      }
+      if (td.kind == T_INIT) init_tile(td, r, h);
+      else gen_tile(td, r, h);
     }
     // hand the tile to the completion warp: all epilogue stores are issued
     // before the CTA barrier; the completion thread's gpu-scope fence after
@@ -985,7 +1054,7 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
     const TileDesc &td = W.desc[d];
     if (td.kind == T_EXIT) break;
     ptx::mbar_wait_abortable(&W.epi_done[d], d_phase, &P.ctrl->abort);
-    uint32_t pub = 0, ps = 0, pst = 0, pn = 0;
+    uint32_t pub = 0, ps = 0, pst = 0, pn = 0, pst2 = NONE32, pn2 = 0;
     unsigned long long pb = 0;
     if (lane == 0) {
       // The epilogue's stores happen-before this thread's acq_rel stage-counter
@@ -1029,10 +1098,13 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
           DispRec rec;
           if (take_next(sl, &rec)) {
             pst = begin_iteration(sl, rec, P.jobs);
-            pub = 1; ps = td.slot; pn = stage_ntiles(P.jobs[rec.job], pst);
-            pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)pn);
+            const DevJob &JN = P.jobs[rec.job];
+            pub = 1; ps = td.slot; pn = stage_ntiles(JN, pst);
+            pst2 = eager_second(JN, rec.kind, pst);
+            pn2 = pst2 != NONE32 ? stage_ntiles(JN, pst2) : 0;
+            pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)(pn + pn2));
           }
-        } else {
+        } else if (td.next_ntiles) {
           pub = 1; ps = td.slot; pst = td.next_stage; pn = td.next_ntiles;
           pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)pn);
         }
@@ -1043,10 +1115,14 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
       ps = __shfl_sync(0xffffffffu, ps, 0);
       pst = __shfl_sync(0xffffffffu, pst, 0);
       pn = __shfl_sync(0xffffffffu, pn, 0);
+      pst2 = __shfl_sync(0xffffffffu, pst2, 0);
+      pn2 = __shfl_sync(0xffffffffu, pn2, 0);
       pb = __shfl_sync(0xffffffffu, pb, 0);
-      for (uint32_t x = lane; x < pn; x += 32) {
+      // the first stage's tiles, then (eager) the second's at higher positions
+      for (uint32_t x = lane; x < pn + pn2; x += 32) {
         const unsigned long long pos = pb + x;
-        ptx::st_release_u64(&P.ring[pos & P.ring_mask], ((pos + 1) << 32) | task_pack(ps, pst, x));
+        const uint32_t task = x < pn ? task_pack(ps, pst, x) : task_pack(ps, pst2, x - pn);
+        ptx::st_release_u64(&P.ring[pos & P.ring_mask], ((pos + 1) << 32) | task);
       }
     }
     __syncwarp();
