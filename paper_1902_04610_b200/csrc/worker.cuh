@@ -806,7 +806,12 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W, uint32_t h) {
       // eager (td.wait): operand A is what the previous stage produces.  The
       // first `pre` chunks' stages are armed and their B (weights /
       // activations of earlier stages) issued before the wait; their A after.
-      const uint32_t pre = (td.wait && nca > 0) ? min(nk, PIPE) : 0;
+      // Exception: when the predecessor is INIT (iteration 0 of a
+      // GEN-prefetch job, whose F_1 directly follows INIT), B is the weights
+      // INIT is still writing -- wait before any load.
+      const bool dep_init = td.wait && td.dep_stage == 0;
+      if (dep_init) wait_stage(P, td.slot, 0, td.dep_want);
+      const uint32_t pre = (td.wait && !dep_init && nca > 0) ? min(nk, PIPE) : 0;
       if (pre) {
         uint32_t s2 = s, ph2 = s_phase;
         ChunkPages pg[PIPE];

@@ -179,7 +179,8 @@ class Context:
                  check: bool = False, dump: Optional[Dict[int, int]] = None, n_workers: int = 0,
                  timeout_ms: int = 0, page_bytes: int = 65536, trace: bool = False,
                  trace_capacity: int = 0, online: bool = False, max_jobs: int = 0, dump_bytes: int = 0,
-                 evict: bool = False, resume: Optional[Dict[int, tuple]] = None):
+                 evict: bool = False, resume: Optional[Dict[int, tuple]] = None,
+                 poison: Optional[bool] = None):
         import torch
         self._torch = torch
         self.L = lib()
@@ -188,6 +189,10 @@ class Context:
         G = page_bytes
         Cp = capacity_bytes // G
         self.arena = torch.empty(Cp * G, dtype=torch.uint8, device=f"cuda:{device}")
+        # debug: fill the arena with 0xFF (NaN in bf16 and fp32) before every
+        # run, so a read of a page this run has not written yet shows up as NaN
+        # instead of whatever an earlier run left there (SALUS_POISON=1)
+        self.poison = (os.environ.get("SALUS_POISON") == "1") if poison is None else poison
         self.stream = torch.cuda.current_stream(device)
         cfg = Config()
         cfg.device = device
@@ -229,6 +234,11 @@ class Context:
         self.meta = torch.empty(max(256, mb.value), dtype=torch.uint8, device=f"cuda:{device}")
         self._check(self.L.salus_prepare(self.ctx, C.c_void_p(self.meta.data_ptr()), mb.value), "prepare")
 
+    def _poison(self):
+        if self.poison:
+            with self._torch.cuda.stream(self.stream):
+                self.arena.fill_(0xFF)
+
     def _check(self, rc, what):
         if rc != 0:
             msg = self.L.salus_last_error(self.ctx) if getattr(self, "ctx", None) else b""
@@ -246,11 +256,13 @@ class Context:
 
     def run(self) -> Dict[int, dict]:
         """One salus_run; returns {job_id: stat dict}."""
+        self._poison()
         return self._stats(self.L.salus_run, "run")
 
     # ---- online submission (online=True; SURVEY §8(f) NEXT-2)
     def run_async(self):
         """Launch the persistent kernel and return while it runs."""
+        self._poison()
         self._check(self.L.salus_run_async(self.ctx), "run_async")
 
     def submit_live(self, job, dump: int = 0):
