@@ -70,7 +70,9 @@ __device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec
   sl.append_ns = rec.append_ns;
   sl.start_ns = ~0ull;
   sl.end_ns = 0;
-  for (uint32_t k = 0; k < MAX_STAGES + 2; k++) sl.stage_done[k] = 0;
+  for (uint32_t k = 0; k < N_STAGE_COUNTERS; k++) sl.stage_done[k] = 0;
+  sl.end_ticket = 0;
+  for (uint32_t k = 0; k < MAX_STAGES; k++) sl.pub_ticket[k] = 0;
   const uint32_t kind = rec.kind & REC_KIND_MASK;
   if (kind != REC_ITER) { sl.stage_done[STAGE_SWAP_OUT] = 0; sl.stage_done[STAGE_SWAP_IN] = 0; }
   __threadfence();

@@ -27,7 +27,7 @@ int max_coresident_grid(int device, int *grid);
 using namespace salus;
 
 #ifndef SALUS_DEFAULT_EAGER_LANES
-#define SALUS_DEFAULT_EAGER_LANES 64
+#define SALUS_DEFAULT_EAGER_LANES 8
 #endif
 
 namespace {
@@ -134,6 +134,18 @@ uint32_t default_max_lanes(uint32_t policy) {
     case SALUS_PACK: return 64;
     default: return 1;   // FIFO, SRTF, FAIR (A9)
   }
+}
+
+// Latency-mode knobs (DevJob.lat_narrow / relax): SALUS_NARROW_BELOW (pair
+// tasks at N = 256 below which a stage takes N = 128 in latency mode; 0 =
+// never) and SALUS_RELAX ("0" disables the relaxed backward barrier).
+uint32_t narrow_below() {
+  static const uint32_t v = [] { const char *e = getenv("SALUS_NARROW_BELOW"); return e ? (uint32_t)atoi(e) : 32u; }();
+  return v;
+}
+bool relax_enabled() {
+  static const bool v = [] { const char *e = getenv("SALUS_RELAX"); return !(e && e[0] == '0'); }();
+  return v;
 }
 
 // Persistent backing pages of a job: its footprint, plus two X buffers for
@@ -331,6 +343,16 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
       D.g_off[0] = (uint32_t)off; off += 2 * bp * mx;
       D.g_off[1] = (uint32_t)off; off += 2 * bp * mx;
     }
+    // latency mode's relaxed backward barrier: a third G buffer from the
+    // declared E's slack (jobs that declare exactly their footprint keep the
+    // full stage barrier)
+    D.relax = 0; D.g_off3 = 0;
+    if (j.kind == SALUS_TRAIN && L >= 2 && !(c->cfg.flags & SALUS_FLAG_NULL_WORK) && relax_enabled() &&
+        (uint64_t)D.e_pages * G >= off + 2 * bp * mx) {
+      D.relax = 1;
+      D.g_off3 = (uint32_t)off;
+      D.ae_pages = (uint32_t)((off + 2 * bp * mx + G - 1) / G);
+    }
     // stage tasks: pair tasks (a CTA pair computes 2 blocks / a 256-row super-tile)
     auto pairs = [](uint32_t n) { return (n + 1) / 2; };
     uint32_t ti = 0;
@@ -351,6 +373,21 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
       }
     }
     D.n_stages = last_stage(j.kind, L) + 1;
+    // latency mode: GEMM stages with fewer than narrow_below() pair tasks at
+    // N = 256 take the N = 128 tile (twice the tasks; same formulas at nt = 128)
+    D.lat_narrow = 0;
+    for (uint32_t s = 0; s < MAX_STAGES; s++) D.stage_tiles_lat[s] = (uint16_t)std::min<uint32_t>(D.stage_tiles[s], 0xFFFF);
+    for (uint32_t s = 2; s < D.n_stages; s++) {
+      const bool fwd = s <= L + 1;
+      const uint32_t l = fwd ? s - 1 : L - (s - (L + 2));
+      const uint32_t dn = fwd ? D.dpad[l] : D.dpad[l - 1];      // the N dimension of the stage's GEMMs
+      const uint32_t extra = (fwd && s == 2 && D.xpre) ? D.stage_tiles[1] + D.t_gen_tiles : 0;
+      if (ntile_for(dn) != 256 || D.stage_tiles[s] - extra >= narrow_below()) continue;
+      D.lat_narrow |= 1u << s;
+      const uint32_t t = fwd ? pairs(D.bpad / 128) * (dn / 128)
+                             : pairs(D.dpad[l] / 128) * (dn / 128) + (l > 1 ? pairs(D.bpad / 128) * (dn / 128) : 0);
+      D.stage_tiles_lat[s] = (uint16_t)(t + extra);
+    }
     D.dump_out_off = dump_cur;
     if (j.dump & SALUS_DUMP_OUTPUTS) dump_cur += (uint64_t)j.n_iters * j.batch * j.dims[L];
     D.dump_w_off = dump_cur;
@@ -380,7 +417,8 @@ static void compute_layout(salus_ctx *c) {
     DevJob &D = c->djobs[d];
     c->id_to_dense[j.job_id] = d;
     fill_devjob(c, h, D, req_total, ppt_total, dump_cur);
-    for (uint32_t s = 0; s < D.n_stages; s++) max_tiles = std::max<uint64_t>(max_tiles, D.stage_tiles[s]);
+    for (uint32_t s = 0; s < D.n_stages; s++)
+      max_tiles = std::max<uint64_t>(max_tiles, std::max<uint32_t>(D.stage_tiles[s], D.stage_tiles_lat[s]));
     if (c->cfg.flags & SALUS_FLAG_EVICT) max_tiles = std::max<uint64_t>(max_tiles, (D.ap_pages + 1) / 2);
     max_ae = std::max<uint64_t>(max_ae, D.ae_pages);
     dispatches += j.n_iters;
@@ -720,7 +758,8 @@ int salus_submit_live(salus_ctx *ctx, const salus_job *job) {
   if (ppt > ctx->ppt_cap) return fail(ctx, SALUS_E_CAPACITY, "live page-table space exhausted");
   if (dump > ctx->dump_cap) return fail(ctx, SALUS_E_CAPACITY, "dump_bytes exceeded");
   for (uint32_t s = 0; s < D.n_stages; s++)
-    if (D.stage_tiles[s] > ctx->ring_tiles) return fail(ctx, SALUS_E_CAPACITY, "stage exceeds the task ring");
+    if (std::max<uint32_t>(D.stage_tiles[s], D.stage_tiles_lat[s]) > ctx->ring_tiles)
+      return fail(ctx, SALUS_E_CAPACITY, "stage exceeds the task ring");
   const uint32_t d = (uint32_t)ctx->jobs.size();   // dense index = publication order
   cudaError_t ce = cudaSetDevice(ctx->cfg.device);
   if (ce == cudaSuccess)

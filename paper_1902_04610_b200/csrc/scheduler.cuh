@@ -851,7 +851,7 @@ struct Sched {
     __syncwarp();
     won = __shfl_sync(0xffffffffu, won, 0);
     if (!won) return;
-    uint32_t got = 0, first = 0, second = NONE32, jj = 0;
+    uint32_t got = 0, first = 0, second = NONE32, jj = 0, lat = 0;
     if (tid == 0) {
       DispRec r;
       got = take_next(sl, &r);
@@ -859,6 +859,7 @@ struct Sched {
         first = begin_iteration(sl, r, P.jobs);
         jj = r.job;
         second = eager_second(P.jobs[jj], r.kind, first);
+        lat = (r.kind & REC_FLAG_EAGER) != 0;
       }
     }
     got = __shfl_sync(0xffffffffu, got, 0);
@@ -866,10 +867,11 @@ struct Sched {
     first = __shfl_sync(0xffffffffu, first, 0);
     second = __shfl_sync(0xffffffffu, second, 0);
     jj = __shfl_sync(0xffffffffu, jj, 0);
-    enqueue(slot, first, stage_ntiles(P.jobs[jj], first));
+    lat = __shfl_sync(0xffffffffu, lat, 0);
+    enqueue(slot, first, stage_ntiles(P.jobs[jj], first, lat));
     // eager: the second stage's tiles go behind the first's (higher ring
     // positions), so every tile's dependency sits at a lower position
-    if (second != NONE32) enqueue(slot, second, stage_ntiles(P.jobs[jj], second));
+    if (second != NONE32) enqueue(slot, second, stage_ntiles(P.jobs[jj], second, lat));
   }
 
   // End of the schedule: wait for every slot to drain its ring.

@@ -97,9 +97,14 @@ struct OpDesc {
 struct TileDesc {
   // next_stage / next_ntiles: the stage this one's completion publishes (its
   // successor; eager records: the successor's successor, 0 tiles if none)
-  uint32_t kind, payload, slot, stage, job, iter, ntiles, next_ntiles, is_last, first_stage, next_stage;
-  uint8_t eager, wait, dep_stage, pad8;   // eager record; wait for stage dep_stage (dep_want counts)
-  uint32_t dep_want;
+  uint32_t kind, payload, slot, stage, job, iter, ntiles, next_ntiles, first_stage, next_stage;
+  uint8_t eager, wait, dep_stage, end2;   // eager record; wait for counter dep_stage (dep_want counts);
+                                          // end2: relaxed record's B_2 / B_1 (end ticket)
+  // dx_ctr: relaxed record, this dX tile also counts on stage_done[dx_ctr] (0 = no);
+  // next_tk: next_stage needs a publication ticket; next2_stage: a relaxed
+  // backward stage also arrives on the ticket of the stage three after it
+  uint8_t is_last, dx_ctr, next_tk, next2_stage;
+  uint32_t dep_want, next2_ntiles;
   uint32_t valid;          // this CTA's half exists (odd block counts leave the peer's empty)
   uint32_t peer_valid;     // the pair's second M block exists
   uint32_t peer_nca;       // (leader) A copies per K-chunk of the peer CTA
@@ -110,9 +115,9 @@ struct TileDesc {
   uint32_t n_ech;          // epilogue-input chunks (0 = none)
   OpDesc a, b;
   uint8_t *ptr[NPTR];
-  const uint32_t *xt_table[NPTR];
+  const uint32_t *xt_tab[2];   // page tables deferred translations use: lane (0), job (1)
   uint32_t xt_off[NPTR];
-  uint32_t xt_mask;
+  uint32_t xt_mask, xt_sel;    // pending translations; bit set in xt_sel = through xt_tab[1]
   uint32_t m0, n0;
   uint32_t rows_valid, cols_valid, ld_logical;
   uint64_t key;
@@ -145,7 +150,7 @@ __device__ __forceinline__ uint8_t *xlate(const Params &P, const uint32_t *table
 }
 
 __device__ __forceinline__ void defer(TileDesc &td, uint32_t which, const uint32_t *table, uint32_t off) {
-  td.xt_table[which] = table;
+  if (table == td.xt_tab[1]) td.xt_sel |= 1u << which;
   td.xt_off[which] = off;
   td.xt_mask |= 1u << which;
 }
@@ -253,31 +258,53 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   const uint32_t L = J.n_layers, bp = J.bpad;
   td.slot = slot; td.stage = stage; td.job = sl.job; td.iter = k; td.seq = sl.seq; td.lseq = sl.lseq;
   td.eager = 0; td.wait = 0;
-  td.ntiles = stage_ntiles(J, stage);
-  td.is_last = stage >= STAGE_SWAP_OUT || stage == last_stage(J.kind, L);
   td.first_stage = stage >= STAGE_SWAP_OUT ? stage
                    : (k == 0 && !(J.dump & DUMP_INTERNAL_RESUME)) ? 0u : (J.xpre ? 2u : 1u);
-  td.eager = (sl.iter & ITER_EAGER_BIT) != 0 && stage < STAGE_SWAP_OUT;
-  td.next_stage = td.is_last ? 0 : next_stage(J, stage);
-  if (td.eager && !td.is_last) {
+  // latency mode (eager record): eager publication, narrow tiles on the
+  // stages lat_narrow marks, relaxed backward barrier for relax jobs
+  const bool lat = (sl.iter & ITER_EAGER_BIT) != 0 && stage < STAGE_SWAP_OUT;
+  const bool relaxed = lat && J.relax && J.kind == SALUS_TRAIN && L >= 2;
+  const uint32_t lastS = last_stage(J.kind, L);
+  td.eager = lat;
+  td.ntiles = stage_ntiles(J, stage, lat);
+  td.is_last = stage >= STAGE_SWAP_OUT || (stage == lastS && !relaxed);
+  // relaxed: B_2 and B_1 may finish in either order; the second to finish ends the record
+  td.end2 = relaxed && stage + 1 >= lastS;
+  td.dx_ctr = 0;
+  td.next_stage = stage == lastS || stage >= STAGE_SWAP_OUT ? 0 : next_stage(J, stage);
+  if (td.eager && td.next_stage) {
     // the successor was published with this stage: publish the one after it
-    td.next_stage = td.next_stage == last_stage(J.kind, L) ? 0 : next_stage(J, td.next_stage);
-    td.next_ntiles = td.next_stage ? J.stage_tiles[td.next_stage] : 0;
-  } else {
-    td.next_ntiles = td.is_last ? 0 : J.stage_tiles[td.next_stage];
+    td.next_stage = td.next_stage == lastS ? 0 : next_stage(J, td.next_stage);
   }
+  td.next_ntiles = td.next_stage ? stage_ntiles(J, td.next_stage, lat) : 0;
+  // relaxed: stage u >= L+5 is published on the completions of u-2 and u-3
+  td.next_tk = relaxed && td.next_stage >= L + 5;
+  td.next2_stage = relaxed && stage >= L + 2 && stage + 3 <= lastS ? stage + 3 : 0;
+  td.next2_ntiles = td.next2_stage ? stage_ntiles(J, td.next2_stage, lat) : 0;
   // every stage of an eager record but its first was published while its
-  // predecessor ran: wait for it before touching what it produces
+  // predecessor ran: wait for it before touching what it produces -- in a
+  // relaxed record, a backward stage after B_L waits only for its
+  // predecessor's dX tiles (counter dx_counter), which produce its G input
   td.wait = td.eager && stage != td.first_stage;
   td.dep_stage = td.wait ? (uint8_t)prev_stage(J, stage) : 0;
-  td.dep_want = td.wait ? 2 * stage_ntiles(J, td.dep_stage) : 0;
+  td.dep_want = td.wait ? 2 * stage_ntiles(J, td.dep_stage, lat) : 0;
+  if (td.wait && relaxed && stage > L + 2) {
+    const uint32_t lp = L - (td.dep_stage - (L + 2));            // the predecessor is B_lp
+    const uint32_t Np = (J.lat_narrow >> td.dep_stage) & 1u ? 128u : ntile_for(J.dpad[lp - 1]);
+    const uint32_t nWp = ((J.dpad[lp] / 128 + 1) / 2) * (J.dpad[lp - 1] / Np);
+    td.dep_want = 2 * (stage_ntiles(J, td.dep_stage, true) - nWp);
+    td.dep_stage = (uint8_t)dx_counter(L, td.dep_stage);
+  }
   td.dump_off = -1;
   td.n_ech = 0;
   td.xt_mask = 0;
+  td.xt_sel = 0;
   td.valid = 1;
   td.ptr[PTR_W32] = nullptr;
   const uint32_t *lt = P.lpt + (uint64_t)slot * P.lpt_stride;   // lane (ephemeral) space
   const uint32_t *jt = P.ppt + J.pt_off;                        // job (persistent) space
+  td.xt_tab[0] = lt;
+  td.xt_tab[1] = jt;
 
   if (stage >= STAGE_SWAP_OUT) {                      // A35 swap: CTA h copies page 2 tile + h
     td.kind = T_COPY;
@@ -295,7 +322,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   // GEN-prefetch jobs: the INIT stage (X_k) and the F_1 stage (X_{k+1}) end
   // with the GEN tiles of stage 1's shape, into the per-job X buffers
   if (J.xpre && (stage == 0 || stage == 2)) {
-    const uint32_t ngx = J.stage_tiles[1], base = J.stage_tiles[stage] - ngx - J.t_gen_tiles;
+    const uint32_t ngx = J.stage_tiles[1], base = stage_ntiles(J, stage, lat) - ngx - J.t_gen_tiles;
     const uint32_t kx = stage == 0 ? kg : kg + 1;
     if (tile >= base + ngx) { decode_gen(td, J, tile - base - ngx, h, jt, J.t_off[kx & 1], kx, true); return; }
     if (tile >= base) { decode_gen(td, J, tile - base, h, jt, J.x_off[kx & 1], kx); return; }
@@ -330,7 +357,8 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   const uint32_t xo = J.xpre ? J.x_off[kg & 1] : J.act_off[0];
   td.kind = T_GEMM;
   if (stage <= L + 1) {                               // forward F_l
-    const uint32_t l = stage - 1, N = ntile_for(J.dpad[l]), ntn = J.dpad[l] / N;
+    const uint32_t l = stage - 1;
+    const uint32_t N = lat && ((J.lat_narrow >> stage) & 1u) ? 128u : ntile_for(J.dpad[l]), ntn = J.dpad[l] / N;
     const uint32_t mb = 2 * (tile / ntn) + h, nb = tile % ntn;
     td.valid = mb < bp / 128;
     td.peer_valid = (mb | 1u) < bp / 128;
@@ -359,13 +387,18 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   } else {                                            // backward B_l
     const uint32_t tile_in = tile;
     const uint32_t l = L - (stage - (L + 2));
-    const uint32_t N = ntile_for(J.dpad[l - 1]), ntn = J.dpad[l - 1] / N;
+    const uint32_t N = lat && ((J.lat_narrow >> stage) & 1u) ? 128u : ntile_for(J.dpad[l - 1]);
+    const uint32_t ntn = J.dpad[l - 1] / N;
     const uint32_t nW = ((J.dpad[l] / 128 + 1) / 2) * ntn;     // dW pair tasks
-    const uint32_t gin = J.g_off[(L - l) & 1], gout = J.g_off[(L - l + 1) & 1];
+    // G_l lives in buffer (L - l) mod 2, or mod 3 in a relaxed record
+    const uint32_t g3[3] = {J.g_off[0], J.g_off[1], J.g_off3};
+    const uint32_t gin = relaxed ? g3[(L - l) % 3] : J.g_off[(L - l) & 1];
+    const uint32_t gout = relaxed ? g3[(L - l + 1) % 3] : J.g_off[(L - l + 1) & 1];
     td.layer = l; td.N = N;
     // the long-K dX tiles take the stage's first task indices, so they are
     // claimed first (longest first within the stage)
-    const uint32_t nX = J.stage_tiles[stage] - nW;
+    const uint32_t nX = td.ntiles - nW;
+    if (relaxed && tile_in < nX) td.dx_ctr = dx_counter(L, stage);
     const uint32_t tile = tile_in < nX ? nW + tile_in : tile_in - nX;
     if (tile < nW) {                                  // dW_l^T = G_l^T A_{l-1}; SGD
       const uint32_t mb = 2 * (tile / ntn) + h, nb = tile % ntn;
@@ -732,7 +765,8 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint
       ptx::fence_proxy_async_global();
       ptx::mbar_arrive(&W.desc_full[d]);
     }
-    if (lane < NPTR && ((td.xt_mask >> lane) & 1u)) td.ptr[lane] = xlate(P, td.xt_table[lane], td.xt_off[lane]);
+    if (lane < NPTR && ((td.xt_mask >> lane) & 1u))
+      td.ptr[lane] = xlate(P, td.xt_tab[(td.xt_sel >> lane) & 1u], td.xt_off[lane]);
     __syncwarp();
     if (lane == 0) ptx::mbar_arrive(&W.desc_ptrs[d]);
     __syncwarp();
@@ -1077,9 +1111,14 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
         }
       }
       Slot &sl = P.slots[td.slot];
+      // relaxed record: a dX tile first releases its G output to the next
+      // backward stage (the counter that stage waits on)
+      if (td.dx_ctr) ptx::atom_add_acqrel_u32(&sl.stage_done[td.dx_ctr], 1u);
       const uint32_t old = ptx::atom_add_acqrel_u32(&sl.stage_done[td.stage], 1u);
       if (old + 1 == 2 * td.ntiles) {
-        if (td.is_last) {                      // the record is physically complete
+        // relaxed: B_2 and B_1 each take an end ticket; the second one ends the record
+        const bool end = td.is_last || (td.end2 && ptx::atom_add_acqrel_u32(&sl.end_ticket, 1u) == 1u);
+        if (end) {                             // the record is physically complete
           const uint64_t end = ptx::globaltimer(), start = sl.start_ns;
           sl.end_ns = end;
           const DevJob &J = P.jobs[td.job];
@@ -1104,14 +1143,25 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
           if (take_next(sl, &rec)) {
             pst = begin_iteration(sl, rec, P.jobs);
             const DevJob &JN = P.jobs[rec.job];
-            pub = 1; ps = td.slot; pn = stage_ntiles(JN, pst);
+            const bool lat = (rec.kind & REC_FLAG_EAGER) != 0;
+            pub = 1; ps = td.slot; pn = stage_ntiles(JN, pst, lat);
             pst2 = eager_second(JN, rec.kind, pst);
-            pn2 = pst2 != NONE32 ? stage_ntiles(JN, pst2) : 0;
+            pn2 = pst2 != NONE32 ? stage_ntiles(JN, pst2, lat) : 0;
             pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)(pn + pn2));
           }
-        } else if (td.next_ntiles) {
-          pub = 1; ps = td.slot; pst = td.next_stage; pn = td.next_ntiles;
-          pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)pn);
+        } else {
+          // the stage two after this one (eager), and in a relaxed record
+          // the one three after it, once their publication tickets are full
+          const bool p1 = td.next_ntiles &&
+                          (!td.next_tk || ptx::atom_add_acqrel_u32(&sl.pub_ticket[td.next_stage], 1u) == 1u);
+          const bool p2 = td.next2_stage && ptx::atom_add_acqrel_u32(&sl.pub_ticket[td.next2_stage], 1u) == 1u;
+          if (p1 || p2) {
+            pub = 1; ps = td.slot;
+            pst = p1 ? td.next_stage : td.next2_stage;
+            pn = p1 ? td.next_ntiles : td.next2_ntiles;
+            if (p1 && p2) { pst2 = td.next2_stage; pn2 = td.next2_ntiles; }
+            pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)(pn + pn2));
+          }
         }
       }
     }

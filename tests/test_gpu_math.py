@@ -151,18 +151,24 @@ def test_c3_inference_real_work_sampled():
         ctx.close()
 
 
-def test_c4_real_work_sampled():
-    """C4 (100-job mixed trace, SRTF, real work at full size): schedule
-    parity; full weight trajectories of the small jobs compared to the oracle."""
+@pytest.mark.parametrize("policy,eager", [(OS.SRTF, None), (OS.PACK, None), (OS.PACK, "0"), (OS.FAIR, None)])
+def test_c4_real_work_sampled(policy, eager, monkeypatch):
+    """C4 (100-job mixed trace, real work at full size): schedule parity; full
+    weight trajectories of the small jobs compared to the oracle.  Under PACK
+    up to 8 lanes run latency-mode records (eager publication, narrow tiles,
+    relaxed backward barrier) side by side; eager="0" forces the throughput
+    mode everywhere."""
     from paper_1902_04610_b200 import salus as S
     from workloads import c4_trace
+    if eager is not None:
+        monkeypatch.setenv("SALUS_EAGER_LANES", eager)
     jobs, cap = c4_trace()
     small = sorted((j for j in jobs if j.dims[0] <= 512 and j.n_iters <= 60),
                    key=lambda j: j.n_iters)[:2]
     assert small
     dump = {j.job_id: S.DUMP_OUTPUTS | S.DUMP_WEIGHTS for j in small}
-    ctx, ref, stats = assert_schedule_parity(jobs, cap, OS.SRTF, null_work=False, dump=dump,
-                                             timeout_ms=300000)
+    ctx, ref, stats = assert_schedule_parity(jobs, cap, policy, null_work=False, dump=dump,
+                                             timeout_ms=120000)
     try:
         _check_math(ctx, small)
     finally:
