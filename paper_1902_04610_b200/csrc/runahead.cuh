@@ -62,7 +62,8 @@ __device__ __forceinline__ bool take_next(Slot &sl, DispRec *rec) {
 // (the fence orders these writes first).
 __device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec, const DevJob *jobs) {
   sl.job = rec.job;
-  sl.iter = rec.iter | ((rec.kind & REC_FLAG_EAGER) ? ITER_EAGER_BIT : 0u);
+  sl.iter = rec.iter | ((rec.kind & REC_FLAG_EAGER) ? ITER_EAGER_BIT : 0u) |
+            ((rec.kind & REC_FLAG_NARROW) ? ITER_NARROW_BIT : 0u);
   sl.seq = rec.seq;
   sl.lseq = rec.lseq;
   sl.rkind = rec.kind;

@@ -140,12 +140,19 @@ uint32_t default_max_lanes(uint32_t policy) {
 // tasks at N = 256 below which a stage takes N = 128 in latency mode; 0 =
 // never) and SALUS_RELAX ("0" disables the relaxed backward barrier).
 uint32_t narrow_below() {
-  static const uint32_t v = [] { const char *e = getenv("SALUS_NARROW_BELOW"); return e ? (uint32_t)atoi(e) : 32u; }();
-  return v;
+  const char *e = getenv("SALUS_NARROW_BELOW");   // read per call: tests change it between contexts
+  return e ? (uint32_t)atoi(e) : 32u;
+}
+// K9 transposed tiles are opt-in (SALUS_SWAP=1): measured on C3 they cost
+// 20 us per request in latency mode and gained 0.6% in throughput mode
+// (profiles/r02/ab_c3.txt)
+bool swap_enabled() {
+  const char *e = getenv("SALUS_SWAP");
+  return e && e[0] == '1';
 }
 bool relax_enabled() {
-  static const bool v = [] { const char *e = getenv("SALUS_RELAX"); return !(e && e[0] == '0'); }();
-  return v;
+  const char *e = getenv("SALUS_RELAX");
+  return !(e && e[0] == '0');
 }
 
 // Persistent backing pages of a job: its footprint, plus two X buffers for
@@ -157,7 +164,8 @@ uint32_t backing_pages(const salus_job &j, const Footprint &fp, bool null_work, 
   const uint64_t p_pages = (j.persistent_bytes + G - 1) / G;
   const uint64_t xb = 2ull * pad128(j.batch) * pad128(j.dims[0]);
   const uint64_t tb = j.kind == SALUS_TRAIN ? 2ull * pad128(j.batch) * pad128(j.dims[j.n_layers]) : 0;
-  static const bool enabled = [] { const char *e = getenv("SALUS_XPRE"); return !(e && e[0] == '0'); }();
+  const char *xe = getenv("SALUS_XPRE");
+  const bool enabled = !(xe && xe[0] == '0');
   *xpre = 0;
   *xbytes = xb;
   // DevJob byte offsets inside a job's persistent space are 32-bit: the
@@ -359,34 +367,48 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
     for (uint32_t l = 1; l <= L; l++) ti += (D.dpad[l] / 128) * (D.dpad[l - 1] / 128);
     D.stage_tiles[0] = pairs(ti);
     D.stage_tiles[1] = pairs((D.bpad / 128) * (D.dpad[0] / 128));
-    for (uint32_t l = 1; l <= L; l++) D.stage_tiles[1 + l] = pairs(D.bpad / 128) * (D.dpad[l] / ntile_for(D.dpad[l]));
     D.t_gen_tiles = (D.xpre && j.kind == SALUS_TRAIN) ? pairs((D.bpad / 128) * (D.dpad[L] / 128)) : 0;
-    if (D.xpre) {                    // INIT and F_1 also generate X and T (GEN prefetch)
-      D.stage_tiles[0] += D.stage_tiles[1] + D.t_gen_tiles;
-      D.stage_tiles[2] += D.stage_tiles[1] + D.t_gen_tiles;
-    }
-    if (j.kind == SALUS_TRAIN) {
-      for (uint32_t l = L; l >= 1; l--) {
-        const uint32_t s = L + 2 + (L - l), nt = ntile_for(D.dpad[l - 1]);
-        D.stage_tiles[s] = pairs(D.dpad[l] / 128) * (D.dpad[l - 1] / nt) +
-                           (l > 1 ? pairs(D.bpad / 128) * (D.dpad[l - 1] / nt) : 0);
-      }
-    }
     D.n_stages = last_stage(j.kind, L) + 1;
-    // latency mode: GEMM stages with fewer than narrow_below() pair tasks at
-    // N = 256 take the N = 128 tile (twice the tasks; same formulas at nt = 128)
+    // K9 (opt-in, swap_enabled): an inference job with a 128-row batch
+    // (b <= 128; C3's requests of b = 1..16) takes transposed
+    // (swap-AB) F_l tiles except in narrow records: pairs of 128-feature
+    // output blocks.  (Measured on C4's training jobs, transposed F / dX
+    // tiles were 1% slower -- half the tasks of the N = 128 tiles,
+    // profiles/r02/ab_k9.txt -- so training jobs never take them.)
+    const bool skinny = D.bpad == 128 && j.kind == SALUS_INFER && swap_enabled();
+    D.swap_mask = 0;
     D.lat_narrow = 0;
-    for (uint32_t s = 0; s < MAX_STAGES; s++) D.stage_tiles_lat[s] = (uint16_t)std::min<uint32_t>(D.stage_tiles[s], 0xFFFF);
+    // GEN-prefetch tiles ride on INIT (stage 0) and F_1 (stage 2)
+    const uint32_t gen_extra = D.xpre ? D.stage_tiles[1] + D.t_gen_tiles : 0;
+    if (D.xpre) D.stage_tiles[0] += gen_extra;
+    for (uint32_t s = 0; s < 2; s++) D.stage_tiles_lat[s] = (uint16_t)std::min<uint32_t>(D.stage_tiles[s], 0xFFFF);
     for (uint32_t s = 2; s < D.n_stages; s++) {
       const bool fwd = s <= L + 1;
+      if (!fwd && j.kind != SALUS_TRAIN) break;
       const uint32_t l = fwd ? s - 1 : L - (s - (L + 2));
-      const uint32_t dn = fwd ? D.dpad[l] : D.dpad[l - 1];      // the N dimension of the stage's GEMMs
-      const uint32_t extra = (fwd && s == 2 && D.xpre) ? D.stage_tiles[1] + D.t_gen_tiles : 0;
-      if (ntile_for(dn) != 256 || D.stage_tiles[s] - extra >= narrow_below()) continue;
-      D.lat_narrow |= 1u << s;
-      const uint32_t t = fwd ? pairs(D.bpad / 128) * (dn / 128)
-                             : pairs(D.dpad[l] / 128) * (dn / 128) + (l > 1 ? pairs(D.bpad / 128) * (dn / 128) : 0);
-      D.stage_tiles_lat[s] = (uint16_t)(t + extra);
+      const uint32_t dn = fwd ? D.dpad[l] : D.dpad[l - 1];      // N of the stage's (non-swap) GEMMs
+      const uint32_t extra = (s == 2) ? gen_extra : 0;
+      const bool has_x = fwd || l > 1;                          // F tiles / dX tiles (B_1 has none)
+      // tasks of the F / dX part and of the dW part at N tile nt (non-swap)
+      auto x_tiles = [&](uint32_t nt) { return has_x ? pairs(D.bpad / 128) * (dn / nt) : 0u; };
+      auto w_tiles = [&](uint32_t nt) { return fwd ? 0u : pairs(D.dpad[l] / 128) * (dn / nt); };
+      const uint32_t nt0 = ntile_for(dn);
+      uint32_t xw = x_tiles(nt0), ww = w_tiles(nt0);
+      if (skinny && has_x) { D.swap_mask |= 1u << s; xw = pairs(dn / 128); }
+      D.stage_tiles[s] = xw + ww + extra;
+      // narrow latency mode (no K9 tiles): N = 128 on the stages with few tasks
+      uint32_t xl = x_tiles(nt0), wl = ww;
+      if (nt0 == 256 && xl + ww < narrow_below()) {
+        D.lat_narrow |= 1u << s;
+        wl = w_tiles(128);
+        xl = x_tiles(128);
+      }
+      D.stage_tiles_lat[s] = (uint16_t)std::min<uint32_t>(xl + wl + extra, 0xFFFF);
+    }
+    {
+      uint64_t tot = 0;
+      for (uint32_t s = 2; s < D.n_stages; s++) tot += D.stage_tiles[s];
+      D.lat_cost = (uint16_t)std::min<uint64_t>(0xFFFF, tot / std::max<uint32_t>(1, D.n_stages - 2));
     }
     D.dump_out_off = dump_cur;
     if (j.dump & SALUS_DUMP_OUTPUTS) dump_cur += (uint64_t)j.n_iters * j.batch * j.dims[L];
@@ -635,6 +657,8 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
       // SALUS_EAGER_LANES environment variable overrides (0 = never)
     const char *ev = getenv("SALUS_EAGER_LANES");
     P.eager_lanes = ev ? (uint32_t)atoi(ev) : SALUS_DEFAULT_EAGER_LANES;
+    const char *nv = getenv("SALUS_NARROW_LANES");
+    P.narrow_lanes = nv ? (uint32_t)atoi(nv) : 2u;
   }
   P.timeout_ns = (uint64_t)ctx->cfg.timeout_ms * 1000000ull;
   P.live = nullptr;

@@ -279,7 +279,12 @@ struct Sched {
     S.svc[j] = 0; S.c[j] = J.iter_ticks; S.done[j] = 0; S.pending[j] = 0; S.next_req[j] = 0;
     S.n[j] = J.n_iters; S.p[j] = J.p_pages; S.e[j] = J.e_pages; S.ap[j] = J.ap_pages; S.ae[j] = J.ae_pages;
     S.id[j] = J.job_id; S.st[j] = ST_NOT_ARRIVED; S.jslot[j] = 0xFF; S.kind[j] = (uint8_t)J.kind;
-    S.xpre[j] = (uint8_t)J.xpre;
+    // bit 0: GEN prefetch; bits 1-4: latency-mode lane limit of the job --
+    // eager records only while nl x (its mean stage tasks) <= 2 x workers,
+    // i.e. while the open lanes' stages cannot fill the GPU anyway (C2b's
+    // 8 wide jobs would otherwise hold pairs waiting on each other's
+    // stages), or while it runs alone (nl = 1: nothing else to wait for)
+    S.xpre[j] = (uint8_t)(J.xpre | (min(15u, 2u * P.n_workers / max(1u, (uint32_t)J.lat_cost)) << 1));
     S.nrt[j] = J.kind == SALUS_INFER ? rq[J.req_off] : IDLE_T;
     S.req_off[j] = J.req_off;
     salus_job_stat &st = P.stats[j];
@@ -837,8 +842,9 @@ struct Sched {
     if (tid == 0) {
       volatile DispRec *vr = &sl.recs[tl % RQ];
       vr->job = j; vr->iter = S.done[j]; vr->seq = pseq; vr->lseq = seq; vr->lane_id = lane_id;
-      vr->kind = kind | ((kind == REC_ITER && S.xpre[j]) ? REC_FLAG_XPRE : 0u) |
-                 ((kind == REC_ITER && nl <= P.eager_lanes) ? REC_FLAG_EAGER : 0u);
+      const bool eager = kind == REC_ITER && nl <= P.eager_lanes && (nl == 1 || nl <= (uint32_t)(S.xpre[j] >> 1));
+      vr->kind = kind | ((kind == REC_ITER && (S.xpre[j] & 1u)) ? REC_FLAG_XPRE : 0u) |
+                 (eager ? REC_FLAG_EAGER : 0u) | ((eager && nl <= P.narrow_lanes) ? REC_FLAG_NARROW : 0u);
       vr->append_ns = ptx::globaltimer();
       // publish (release) and learn whether the slot was idle in one atomic;
       // only the scheduler ever sets `running`, so taking it needs no CAS
@@ -859,7 +865,7 @@ struct Sched {
         first = begin_iteration(sl, r, P.jobs);
         jj = r.job;
         second = eager_second(P.jobs[jj], r.kind, first);
-        lat = (r.kind & REC_FLAG_EAGER) != 0;
+        lat = (r.kind & REC_FLAG_NARROW) != 0;
       }
     }
     got = __shfl_sync(0xffffffffu, got, 0);

@@ -105,6 +105,9 @@ struct TileDesc {
   // backward stage also arrives on the ticket of the stage three after it
   uint8_t is_last, dx_ctr, next_tk, next2_stage;
   uint32_t dep_want, next2_ntiles;
+  // K9: transposed (swap-AB) tile; ech_load: the epilogue-input chunk is
+  // loaded (else only reserved as the output block's staging buffer)
+  uint8_t swap, ech_load, pad_k9[2];
   uint32_t valid;          // this CTA's half exists (odd block counts leave the peer's empty)
   uint32_t peer_valid;     // the pair's second M block exists
   uint32_t peer_nca;       // (leader) A copies per K-chunk of the peer CTA
@@ -253,7 +256,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
                             TileDesc &td, uint32_t h) {
   td.payload = payload;
   const uint32_t slot = payload >> 26, stage = (payload >> 21) & 31u, tile = payload & ((1u << 21) - 1);
-  const uint32_t k = sl.iter & ~ITER_EAGER_BIT;       // this context's iteration index
+  const uint32_t k = sl.iter & ~ITER_FLAG_BITS;       // this context's iteration index
   const uint32_t kg = k + J.iter_base;                // the job's own (migration, NEXT-4)
   const uint32_t L = J.n_layers, bp = J.bpad;
   td.slot = slot; td.stage = stage; td.job = sl.job; td.iter = k; td.seq = sl.seq; td.lseq = sl.lseq;
@@ -263,10 +266,11 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   // latency mode (eager record): eager publication, narrow tiles on the
   // stages lat_narrow marks, relaxed backward barrier for relax jobs
   const bool lat = (sl.iter & ITER_EAGER_BIT) != 0 && stage < STAGE_SWAP_OUT;
+  const bool narrow = lat && (sl.iter & ITER_NARROW_BIT) != 0;
   const bool relaxed = lat && J.relax && J.kind == SALUS_TRAIN && L >= 2;
   const uint32_t lastS = last_stage(J.kind, L);
   td.eager = lat;
-  td.ntiles = stage_ntiles(J, stage, lat);
+  td.ntiles = stage_ntiles(J, stage, narrow);
   td.is_last = stage >= STAGE_SWAP_OUT || (stage == lastS && !relaxed);
   // relaxed: B_2 and B_1 may finish in either order; the second to finish ends the record
   td.end2 = relaxed && stage + 1 >= lastS;
@@ -276,29 +280,30 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     // the successor was published with this stage: publish the one after it
     td.next_stage = td.next_stage == lastS ? 0 : next_stage(J, td.next_stage);
   }
-  td.next_ntiles = td.next_stage ? stage_ntiles(J, td.next_stage, lat) : 0;
+  td.next_ntiles = td.next_stage ? stage_ntiles(J, td.next_stage, narrow) : 0;
   // relaxed: stage u >= L+5 is published on the completions of u-2 and u-3
   td.next_tk = relaxed && td.next_stage >= L + 5;
   td.next2_stage = relaxed && stage >= L + 2 && stage + 3 <= lastS ? stage + 3 : 0;
-  td.next2_ntiles = td.next2_stage ? stage_ntiles(J, td.next2_stage, lat) : 0;
+  td.next2_ntiles = td.next2_stage ? stage_ntiles(J, td.next2_stage, narrow) : 0;
   // every stage of an eager record but its first was published while its
   // predecessor ran: wait for it before touching what it produces -- in a
   // relaxed record, a backward stage after B_L waits only for its
   // predecessor's dX tiles (counter dx_counter), which produce its G input
   td.wait = td.eager && stage != td.first_stage;
   td.dep_stage = td.wait ? (uint8_t)prev_stage(J, stage) : 0;
-  td.dep_want = td.wait ? 2 * stage_ntiles(J, td.dep_stage, lat) : 0;
+  td.dep_want = td.wait ? 2 * stage_ntiles(J, td.dep_stage, narrow) : 0;
   if (td.wait && relaxed && stage > L + 2) {
     const uint32_t lp = L - (td.dep_stage - (L + 2));            // the predecessor is B_lp
-    const uint32_t Np = (J.lat_narrow >> td.dep_stage) & 1u ? 128u : ntile_for(J.dpad[lp - 1]);
+    const uint32_t Np = narrow && ((J.lat_narrow >> td.dep_stage) & 1u) ? 128u : ntile_for(J.dpad[lp - 1]);
     const uint32_t nWp = ((J.dpad[lp] / 128 + 1) / 2) * (J.dpad[lp - 1] / Np);
-    td.dep_want = 2 * (stage_ntiles(J, td.dep_stage, true) - nWp);
+    td.dep_want = 2 * (stage_ntiles(J, td.dep_stage, narrow) - nWp);
     td.dep_stage = (uint8_t)dx_counter(L, td.dep_stage);
   }
   td.dump_off = -1;
   td.n_ech = 0;
   td.xt_mask = 0;
   td.xt_sel = 0;
+  td.swap = 0; td.ech_load = 1;
   td.valid = 1;
   td.ptr[PTR_W32] = nullptr;
   const uint32_t *lt = P.lpt + (uint64_t)slot * P.lpt_stride;   // lane (ephemeral) space
@@ -322,7 +327,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   // GEN-prefetch jobs: the INIT stage (X_k) and the F_1 stage (X_{k+1}) end
   // with the GEN tiles of stage 1's shape, into the per-job X buffers
   if (J.xpre && (stage == 0 || stage == 2)) {
-    const uint32_t ngx = J.stage_tiles[1], base = stage_ntiles(J, stage, lat) - ngx - J.t_gen_tiles;
+    const uint32_t ngx = J.stage_tiles[1], base = stage_ntiles(J, stage, narrow) - ngx - J.t_gen_tiles;
     const uint32_t kx = stage == 0 ? kg : kg + 1;
     if (tile >= base + ngx) { decode_gen(td, J, tile - base - ngx, h, jt, J.t_off[kx & 1], kx, true); return; }
     if (tile >= base) { decode_gen(td, J, tile - base, h, jt, J.x_off[kx & 1], kx); return; }
@@ -356,9 +361,40 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   const uint32_t *xt = J.xpre ? jt : lt;
   const uint32_t xo = J.xpre ? J.x_off[kg & 1] : J.act_off[0];
   td.kind = T_GEMM;
-  if (stage <= L + 1) {                               // forward F_l
+  // K9 tiles (inference requests of b <= 128) except in narrow records,
+  // whose non-transposed N = 128 tiles give a skinny stage twice the tasks
+  const bool swap = !narrow && ((J.swap_mask >> stage) & 1u);
+  if (stage <= L + 1 && swap) {                       // K9 forward F_l^T = W_l^T A_{l-1}^T
+    const uint32_t l = stage - 1, mb = 2 * tile + h;
+    td.swap = 1;
+    td.valid = mb < J.dpad[l] / 128;
+    td.peer_valid = (mb | 1u) < J.dpad[l] / 128;
+    td.layer = l; td.N = bp; td.nk = J.dpad[l - 1] / 64;
+    // A: 128 rows (output features) of W_l^T, K-major; B: this CTA's 64 batch rows, K-major
+    td.a = OpDesc{jt, J.wb_off[l - 1][kg & 1], J.dpad[l], mb * 128, 0};
+    td.b = l == 1 ? OpDesc{xt, xo, bp, h * 64, 0} : OpDesc{lt, J.act_off[l - 1], bp, h * 64, 0};
+    td.m0 = mb * 128; td.n0 = 0;
+    td.rows_valid = J.dims[l]; td.cols_valid = J.batch; td.ld_logical = J.dims[l];
+    uint32_t out_off;
+    td.ech_load = 0;
+    if (l < L) { td.epi = EPI_RELU; out_off = J.act_off[l]; }
+    else if (J.kind == SALUS_TRAIN) {
+      td.epi = EPI_LOSS; out_off = J.g_off[0];
+      td.key = gen_key(J.seed, J.job_id, GEN_T, L, kg);
+      if (J.t_gen_tiles && td.valid) {                 // prefetched T_k: the block's 2 target panels
+        for (uint32_t q = 0; q < 2; q++) defer(td, PTR_EPI + q, jt, J.t_off[kg & 1] + (2 * mb + q) * bp * 128u);
+        td.ech_load = 1;
+      }
+    } else { td.epi = EPI_OUT; out_off = J.act_off[L]; }
+    if (td.valid) {
+      if (l == L && (J.dump & SALUS_DUMP_OUTPUTS))
+        td.dump_off = (int64_t)(J.dump_out_off + (uint64_t)k * J.batch * J.dims[L]);
+      for (uint32_t q = 0; q < 2; q++) defer(td, PTR_OUT + q, lt, out_off + (2 * mb + q) * bp * 128u);
+      td.n_ech = 1;                                    // the output block's staging chunk
+    }
+  } else if (stage <= L + 1) {                        // forward F_l
     const uint32_t l = stage - 1;
-    const uint32_t N = lat && ((J.lat_narrow >> stage) & 1u) ? 128u : ntile_for(J.dpad[l]), ntn = J.dpad[l] / N;
+    const uint32_t N = narrow && ((J.lat_narrow >> stage) & 1u) ? 128u : ntile_for(J.dpad[l]), ntn = J.dpad[l] / N;
     const uint32_t mb = 2 * (tile / ntn) + h, nb = tile % ntn;
     td.valid = mb < bp / 128;
     td.peer_valid = (mb | 1u) < bp / 128;
@@ -387,7 +423,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   } else {                                            // backward B_l
     const uint32_t tile_in = tile;
     const uint32_t l = L - (stage - (L + 2));
-    const uint32_t N = lat && ((J.lat_narrow >> stage) & 1u) ? 128u : ntile_for(J.dpad[l - 1]);
+    const uint32_t N = narrow && ((J.lat_narrow >> stage) & 1u) ? 128u : ntile_for(J.dpad[l - 1]);
     const uint32_t ntn = J.dpad[l - 1] / N;
     const uint32_t nW = ((J.dpad[l] / 128 + 1) / 2) * ntn;     // dW pair tasks
     // G_l lives in buffer (L - l) mod 2, or mod 3 in a relaxed record
@@ -608,6 +644,69 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
     }
     store_bf16_rows(tds.ptr[PTR_OUT + pan], u, r, ch0);
   }
+}
+
+// K9 transposed tile: TMEM lane r = output feature m0 + r, column c = batch
+// row c (N = the 128-row padded batch).  The output block (2 panels of the
+// batch-row-major tensor: 128 rows x 64 features each, 16 KiB) is staged in
+// the tile's epilogue-input chunk (an input chunk -- a mask or prefetched
+// loss targets -- would be read and overwritten in place element by element)
+// and copied out by all epilogue threads with 16-byte stores.  `hh` = this
+// warp's column half.
+__device__ __forceinline__ uint32_t swap_off(uint32_t r, uint32_t b) {
+  return (r >> 6) * 16384u + swz(b, (r & 63u) >> 3) + (r & 7u) * 2u;
+}
+
+__device__ void epilogue_swap(const Params &P, WorkerSmem &W, const TileDesc &td, uint32_t tacc, uint32_t r,
+                              uint32_t hh, uint32_t et, uint32_t lane, uint32_t &e, uint32_t &e_phase) {
+  const uint32_t taddr = tacc + (((r >> 5) * 32u) << 16);
+  const uint32_t ncc = td.N / 32, sub = ncc / EPI_HALVES, cc0 = hh * sub;
+  ptx::mbar_wait_abortable(&W.epi_full[e], e_phase, &P.ctrl->abort);
+  uint8_t *buf = W.epi_in[e];
+  const uint32_t f = td.m0 + r;
+  const bool fok = f < td.rows_valid;
+  const uint32_t batch = td.cols_valid;
+  const float inv_b = 1.0f / (float)batch;
+  float *dump = td.dump_off >= 0 ? P.dump + td.dump_off : nullptr;
+  for (uint32_t cc = cc0; cc < cc0 + sub; cc++) {
+    uint32_t raw[32];
+    ptx::tmem_ld32(taddr + cc * 32u, raw);
+    ptx::tmem_ld_wait();
+#pragma unroll 4
+    for (int x = 0; x < 32; x++) {
+      const float v = __uint_as_float(raw[x]);
+      const uint32_t b = cc * 32 + x;
+      const bool ok = fok && b < batch;
+      uint16_t *slot16 = reinterpret_cast<uint16_t *>(buf + swap_off(r, b));
+      float y;
+      if (td.epi == EPI_DX) {
+        const uint32_t m = *slot16;
+        y = ((m & 0x8000u) == 0 && (m & 0x7FFFu) != 0) ? v : 0.f;
+      } else {
+        if (dump && ok) dump[(uint64_t)b * td.ld_logical + f] = v;
+        if (td.epi == EPI_RELU) y = ok ? fmaxf(v, 0.f) : 0.f;
+        else if (td.epi == EPI_OUT) y = ok ? v : 0.f;
+        else {                                          // EPI_LOSS: G_L = (A_L - T) / B
+          const float t = td.ech_load ? __uint_as_float((uint32_t)*slot16 << 16)
+                                      : gen_value(td.key, (uint64_t)b * td.ld_logical + f, 1.0f);
+          y = ok ? (v - t) * inv_b : 0.f;
+        }
+      }
+      __nv_bfloat16 hb = __float2bfloat16_rn(y);
+      *slot16 = *reinterpret_cast<uint16_t *>(&hb);
+    }
+  }
+  named_bar(1, EPI_THREADS);                            // the block is staged
+#pragma unroll
+  for (uint32_t k = 0; k < 2 * 16384u / (16u * EPI_THREADS); k++) {
+    const uint32_t o = (k * EPI_THREADS + et) * 16u;
+    const uint4 val = *reinterpret_cast<const uint4 *>(buf + o);
+    uint8_t *dst = o < 16384u ? td.ptr[PTR_OUT] + o : td.ptr[PTR_OUT + 1] + (o - 16384u);
+    *reinterpret_cast<uint4 *>(dst) = val;
+  }
+  __syncwarp();
+  if (lane == 0) ptx::mbar_arrive(&W.epi_empty[e]);
+  if (++e == EBUF) { e = 0; e_phase ^= 1; }
 }
 
 // INIT: W_l block (rows j = m0 + r of W^T storage, 128 columns i)
@@ -845,7 +944,10 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W, uint32_t h) {
       // INIT is still writing -- wait before any load.
       const bool dep_init = td.wait && td.dep_stage == 0;
       if (dep_init) wait_stage(P, td.slot, 0, td.dep_want);
-      const uint32_t pre = (td.wait && !dep_init && nca > 0) ? min(nk, PIPE) : 0;
+      // the operand the predecessor produces: A, except in a K9 transposed
+      // tile, whose A is the weights and B the activations / gradients
+      const bool dep_b = td.swap;
+      const uint32_t pre = (td.wait && !dep_init && (dep_b ? ncb : nca) > 0) ? min(nk, PIPE) : 0;
       if (pre) {
         uint32_t s2 = s, ph2 = s_phase;
         ChunkPages pg[PIPE];
@@ -854,17 +956,27 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W, uint32_t h) {
           ptx::mbar_wait_abortable(&W.empty[s2], ph2 ^ 1, &P.ctrl->abort);
           const uint32_t bar = ptx::mapa(&W.full[s2], 0);
           if (h == 0) ptx::mbar_arrive_expect_tx(&W.full[s2], tx_pair);
-          uint8_t *sb = W.stage[s2] + STAGE_A_BYTES;
-          if (ncb > 0) ptx::tma_load_2d_pair(sb, tb, 0, tma_row(pg[kc].b0, copy_off(b, kc, 0)), bar, pol_b);
-          if (ncb > 1) ptx::tma_load_2d_pair(sb + bb, tb, 0, tma_row(pg[kc].b1, copy_off(b, kc, 1)), bar, pol_b);
+          uint8_t *sa = W.stage[s2], *sb = W.stage[s2] + STAGE_A_BYTES;
+          if (dep_b) {
+            if (nca > 0) ptx::tma_load_2d_pair(sa, ta, 0, tma_row(pg[kc].a0, copy_off(a, kc, 0)), bar, pol_a);
+            if (nca > 1) ptx::tma_load_2d_pair(sa + ab, ta, 0, tma_row(pg[kc].a1, copy_off(a, kc, 1)), bar, pol_a);
+          } else {
+            if (ncb > 0) ptx::tma_load_2d_pair(sb, tb, 0, tma_row(pg[kc].b0, copy_off(b, kc, 0)), bar, pol_b);
+            if (ncb > 1) ptx::tma_load_2d_pair(sb + bb, tb, 0, tma_row(pg[kc].b1, copy_off(b, kc, 1)), bar, pol_b);
+          }
           if (++s2 == PIPE) { s2 = 0; ph2 ^= 1; }
         }
         wait_stage(P, td.slot, td.dep_stage, td.dep_want);
         for (uint32_t kc = 0; kc < pre; kc++) {
           const uint32_t bar = ptx::mapa(&W.full[s], 0);
-          uint8_t *sa = W.stage[s];
-          ptx::tma_load_2d_pair(sa, ta, 0, tma_row(pg[kc].a0, copy_off(a, kc, 0)), bar, pol_a);
-          if (nca > 1) ptx::tma_load_2d_pair(sa + ab, ta, 0, tma_row(pg[kc].a1, copy_off(a, kc, 1)), bar, pol_a);
+          uint8_t *sa = W.stage[s], *sb = W.stage[s] + STAGE_A_BYTES;
+          if (dep_b) {
+            if (ncb > 0) ptx::tma_load_2d_pair(sb, tb, 0, tma_row(pg[kc].b0, copy_off(b, kc, 0)), bar, pol_b);
+            if (ncb > 1) ptx::tma_load_2d_pair(sb + bb, tb, 0, tma_row(pg[kc].b1, copy_off(b, kc, 1)), bar, pol_b);
+          } else {
+            ptx::tma_load_2d_pair(sa, ta, 0, tma_row(pg[kc].a0, copy_off(a, kc, 0)), bar, pol_a);
+            if (nca > 1) ptx::tma_load_2d_pair(sa + ab, ta, 0, tma_row(pg[kc].a1, copy_off(a, kc, 1)), bar, pol_a);
+          }
           if (++s == PIPE) { s = 0; s_phase ^= 1; }
         }
       }
@@ -929,6 +1041,11 @@ __device__ void epi_loader(const Params &P, WorkerSmem &W, uint32_t h) {
       if (td.wait && td.epi == EPI_LOSS && n && td.iter == 0) wait_stage(P, td.slot, td.dep_stage, td.dep_want);
       for (uint32_t c = 0; c < n; c++) {
         ptx::mbar_wait_abortable(&W.epi_empty[e], e_phase ^ 1, &P.ctrl->abort);
+        if (!td.ech_load) {                   // K9 staging chunk: reserved, nothing to load
+          ptx::mbar_arrive(&W.epi_full[e]);
+          if (++e == EBUF) { e = 0; e_phase ^= 1; }
+          continue;
+        }
         ptx::mbar_arrive_expect_tx(&W.epi_full[e], ECH_BYTES);
         if (sgd) {
           ptx::bulk_g2s_hint(W.epi_in[e], td.ptr[PTR_W32 + (c >> 1)] + (c & 1) * 32768u, ECH_BYTES, &W.epi_full[e],
@@ -1034,6 +1151,8 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
       const uint32_t tacc = tmem + b * ACC_COLS;
       if (!td.valid) {
         // the peer half of a super-tile past the last M block: nothing to store
+      } else if (td.swap) {
+        epilogue_swap(P, W, td, tacc, r, h, et, lane, e, e_phase);
       } else if (n == 0) {
         const uint32_t sub = ncc / EPI_HALVES;
         epilogue_cols(P, td, ev, tacc, r, 0, h * sub, (h + 1) * sub, nullptr);
@@ -1143,10 +1262,10 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
           if (take_next(sl, &rec)) {
             pst = begin_iteration(sl, rec, P.jobs);
             const DevJob &JN = P.jobs[rec.job];
-            const bool lat = (rec.kind & REC_FLAG_EAGER) != 0;
-            pub = 1; ps = td.slot; pn = stage_ntiles(JN, pst, lat);
+            const bool narrow = (rec.kind & REC_FLAG_NARROW) != 0;
+            pub = 1; ps = td.slot; pn = stage_ntiles(JN, pst, narrow);
             pst2 = eager_second(JN, rec.kind, pst);
-            pn2 = pst2 != NONE32 ? stage_ntiles(JN, pst2, lat) : 0;
+            pn2 = pst2 != NONE32 ? stage_ntiles(JN, pst2, narrow) : 0;
             pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)(pn + pn2));
           }
         } else {

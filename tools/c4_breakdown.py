@@ -32,20 +32,24 @@ def main():
     for r in w:
         meas[int(r["job"])] += (int(r["end_ns"]) - int(r["start_ns"])) / 1e9
     groups = defaultdict(lambda: [0.0, 0.0, 0])
+    gb = defaultdict(lambda: [0.0, 0.0, 0])
     for jid, j in J.items():
         ideal = j.n_iters * max(algorithmic_flops(j.kind, j.dims, j.batch) / tf,
                                 algorithmic_bytes(j.kind, j.dims, j.batch) / bw)
-        g = groups[(j.dims[0], len(j.dims) - 1)]
-        g[0] += meas[jid]
-        g[1] += ideal
-        g[2] += j.n_iters
+        for g in (groups[(j.dims[0], len(j.dims) - 1)], gb[(j.dims[0], j.batch)]):
+            g[0] += meas[jid]
+            g[1] += ideal
+            g[2] += j.n_iters
     kern = rs["kernel_ns"] / 1e9
     busy = sum(meas.values())
     out = {"kernel_s": kern, "sum_iteration_s": busy, "gap_s": kern - busy,
            "groups": {f"w{k[0]}_L{k[1]}": {"measured_s": v[0], "ideal_s": v[1], "frac": v[1] / v[0] if v[0] else None,
                                           "iters": v[2], "us_per_iter": 1e6 * v[0] / v[2]}
-                      for k, v in sorted(groups.items())}}
-    print(json.dumps(out))
+                      for k, v in sorted(groups.items())},
+           "by_batch": {f"w{k[0]}_B{k[1]}": {"measured_s": round(v[0], 4), "frac": round(v[1] / v[0], 3) if v[0] else None,
+                                             "us_per_iter": round(1e6 * v[0] / v[2], 1)}
+                        for k, v in sorted(gb.items())}}
+    print(json.dumps(out, indent=1))
 
 
 if __name__ == "__main__":
