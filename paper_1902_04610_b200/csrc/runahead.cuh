@@ -8,7 +8,7 @@
 // the scheduler after an append to an idle slot, or the worker thread that
 // completes an iteration's last tile — takes the next record and starts it.
 // The handoff goes through one 64-bit word per slot, qstate = tail << 32 |
-// running: the appender's atomic add (release) publishes a record and tells
+// head << 1 | running: the appender's atomic add (release) publishes a record and tells
 // it whether the slot was idle; the holder releases `running` only with a
 // CAS that expects the tail it has consumed up to, so an append racing with
 // the last completion is never lost and no store/fence/load Dekker pair (two
@@ -39,28 +39,54 @@ __device__ __forceinline__ unsigned long long atom_add_release_u64(unsigned long
   return old;
 }
 
+// qstate = tail << 32 | head << 1 | running: records appended (tail, 32
+// bits), records started (head, 31 bits), running bit.  One acquire load
+// gives the holder both counters; it bumps head with one release add.
+constexpr unsigned long long QS_HEAD_ONE = 2ull, QS_TAIL_ONE = 1ull << 32;
+__host__ __device__ __forceinline__ uint32_t qs_head(unsigned long long st) { return (uint32_t)(st >> 1) & 0x7FFFFFFFu; }
+__host__ __device__ __forceinline__ uint32_t qs_tail(unsigned long long st) { return (uint32_t)(st >> 32) & 0x7FFFFFFFu; }
+
+__device__ __forceinline__ void red_add_release_u64(unsigned long long *p, unsigned long long v) {
+  asm volatile("red.release.gpu.global.add.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // Caller holds `running`.  Takes the next record (true) or releases the token
 // (false): the CAS succeeds only if no record was appended since the load.
+// The head bump is a release so the record's slot in the ring (reused RQ
+// records later) is only handed back after it was read.
 __device__ __forceinline__ bool take_next(Slot &sl, DispRec *rec) {
   for (;;) {
-    const uint32_t h = *(volatile uint32_t *)&sl.q_head;
     const unsigned long long st = ld_acquire_u64q(&sl.qstate);
-    if ((uint32_t)(st >> 32) != h) {
+    const uint32_t h = qs_head(st);
+    if (qs_tail(st) != h) {
       const volatile DispRec *vr = &sl.recs[h % RQ];
       rec->job = vr->job; rec->iter = vr->iter; rec->seq = vr->seq; rec->lane_id = vr->lane_id; rec->kind = vr->kind;
       rec->append_ns = vr->append_ns; rec->lseq = vr->lseq;
-      st_release_u32(&sl.q_head, h + 1);
+      red_add_release_u64(&sl.qstate, QS_HEAD_ONE);
       return true;
     }
     if (atomicCAS(&sl.qstate, st, st & ~1ull) == st) return false;   // released
   }
 }
 
-// Single thread: make `rec` the slot's in-flight record.  Returns the first
-// stage (INIT before a job's first iteration, else GEN; the copy stage of a
-// swap record); the caller enqueues that stage's tiles after this returns
-// (the fence orders these writes first).
-__device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec, const DevJob *jobs) {
+// The first stage of record `rec` (INIT before a job's first iteration, else
+// GEN, or F_1 for a GEN-prefetch job; the copy stage of a swap record).
+__device__ __forceinline__ uint32_t first_stage_of(const DispRec &rec, const DevJob *jobs) {
+  const uint32_t kind = rec.kind & REC_KIND_MASK;
+  if (kind == REC_SWAP_OUT) return STAGE_SWAP_OUT;
+  if (kind == REC_SWAP_IN) return STAGE_SWAP_IN;
+  // a job's first iteration initialises its weights -- unless it resumes a
+  // migrated state (NEXT-4), whose swap-in record already put them in place;
+  // a GEN-prefetch job's X is already there (stage 1 skipped)
+  if (rec.iter == 0 && !(jobs[rec.job].dump & DUMP_INTERNAL_RESUME)) return 0u;
+  return (rec.kind & REC_FLAG_XPRE) ? 2u : 1u;
+}
+
+// Single thread: make `rec` the slot's in-flight record.  The caller
+// publishes the first stage's tiles after this returns (the fence orders
+// these writes first); it may reserve their ring positions before calling,
+// so that atomic's round trip overlaps this fence.
+__device__ __forceinline__ void begin_iteration(Slot &sl, const DispRec &rec) {
   sl.job = rec.job;
   sl.iter = rec.iter | ((rec.kind & REC_FLAG_EAGER) ? ITER_EAGER_BIT : 0u) |
             ((rec.kind & REC_FLAG_NARROW) ? ITER_NARROW_BIT : 0u);
@@ -74,16 +100,8 @@ __device__ __forceinline__ uint32_t begin_iteration(Slot &sl, const DispRec &rec
   for (uint32_t k = 0; k < N_STAGE_COUNTERS; k++) sl.stage_done[k] = 0;
   sl.end_ticket = 0;
   for (uint32_t k = 0; k < MAX_STAGES; k++) sl.pub_ticket[k] = 0;
-  const uint32_t kind = rec.kind & REC_KIND_MASK;
-  if (kind != REC_ITER) { sl.stage_done[STAGE_SWAP_OUT] = 0; sl.stage_done[STAGE_SWAP_IN] = 0; }
+  if ((rec.kind & REC_KIND_MASK) != REC_ITER) { sl.stage_done[STAGE_SWAP_OUT] = 0; sl.stage_done[STAGE_SWAP_IN] = 0; }
   __threadfence();
-  if (kind == REC_SWAP_OUT) return STAGE_SWAP_OUT;
-  if (kind == REC_SWAP_IN) return STAGE_SWAP_IN;
-  // a job's first iteration initialises its weights -- unless it resumes a
-  // migrated state (NEXT-4), whose swap-in record already put them in place;
-  // a GEN-prefetch job's X is already there (stage 1 skipped)
-  if (rec.iter == 0 && !(jobs[rec.job].dump & DUMP_INTERNAL_RESUME)) return 0u;
-  return (rec.kind & REC_FLAG_XPRE) ? 2u : 1u;
 }
 
 }  // namespace salus

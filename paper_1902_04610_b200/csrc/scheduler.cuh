@@ -241,17 +241,6 @@ struct Sched {
     return warp_min_i64(m);
   }
 
-  __device__ void enqueue(uint32_t slot, uint32_t stage, uint32_t ntiles) {
-    unsigned long long base = 0;
-    if (tid == 0) base = atomicAdd(&P.ctrl->q_head, (unsigned long long)ntiles);
-    base = __shfl_sync(0xffffffffu, base, 0);
-    for (uint32_t k = tid; k < ntiles; k += 32) {
-      unsigned long long pos = base + k;
-      ptx::st_release_u64(&P.ring[pos & P.ring_mask], ((pos + 1) << 32) | task_pack(slot, stage, k));
-    }
-    __syncwarp();
-  }
-
   __device__ bool host_abort() const { return P.host_abort && ptx::ld_volatile_u32(P.host_abort) != 0; }
 
   // Spin until `slot` has physically completed the iteration with seq + 1 ==
@@ -823,8 +812,11 @@ struct Sched {
       while (true) {
         // the cached head usually proves there is room without a load
         if (tid == 0) {
-          full = tl - S.q_head_seen[slot] >= RQ;
-          if (full) { S.q_head_seen[slot] = ld_acquire_u32(&sl.q_head); full = tl - S.q_head_seen[slot] >= RQ; }
+          full = ((tl - S.q_head_seen[slot]) & 0x7FFFFFFFu) >= RQ;
+          if (full) {
+            S.q_head_seen[slot] = qs_head(ld_acquire_u64q(&sl.qstate));
+            full = ((tl - S.q_head_seen[slot]) & 0x7FFFFFFFu) >= RQ;
+          }
         }
         full = __shfl_sync(0xffffffffu, full, 0);
         if (!full) break;
@@ -839,17 +831,19 @@ struct Sched {
       if (t0) { wait_ns += ptx::globaltimer() - t0; wait_ring_ns += ptx::globaltimer() - t0; }
     }
     uint32_t won = 0;
+    DispRec rec;                                           // (thread 0) the record as appended
     if (tid == 0) {
       volatile DispRec *vr = &sl.recs[tl % RQ];
-      vr->job = j; vr->iter = S.done[j]; vr->seq = pseq; vr->lseq = seq; vr->lane_id = lane_id;
       const bool eager = kind == REC_ITER && nl <= P.eager_lanes && (nl == 1 || nl <= (uint32_t)(S.xpre[j] >> 1));
-      vr->kind = kind | ((kind == REC_ITER && (S.xpre[j] & 1u)) ? REC_FLAG_XPRE : 0u) |
+      rec.job = j; rec.iter = S.done[j]; rec.seq = pseq; rec.lseq = seq; rec.lane_id = lane_id;
+      rec.kind = kind | ((kind == REC_ITER && (S.xpre[j] & 1u)) ? REC_FLAG_XPRE : 0u) |
                  (eager ? REC_FLAG_EAGER : 0u) | ((eager && nl <= P.narrow_lanes) ? REC_FLAG_NARROW : 0u);
-      vr->append_ns = ptx::globaltimer();
+      rec.append_ns = ptx::globaltimer();
+      vr->job = rec.job; vr->iter = rec.iter; vr->seq = rec.seq; vr->lseq = rec.lseq;
+      vr->lane_id = rec.lane_id; vr->kind = rec.kind; vr->append_ns = rec.append_ns;
       // publish (release) and learn whether the slot was idle in one atomic;
       // only the scheduler ever sets `running`, so taking it needs no CAS
-      won = (atom_add_release_u64(&sl.qstate, 1ull << 32) & 1ull) == 0;
-      if (won) atomicOr(&sl.qstate, 1ull);
+      won = (atom_add_release_u64(&sl.qstate, QS_TAIL_ONE) & 1ull) == 0;
       S.sq_tail[slot] = tl + 1;
       S.last_app[slot] = pseq + 1;
     }
@@ -857,27 +851,36 @@ struct Sched {
     __syncwarp();
     won = __shfl_sync(0xffffffffu, won, 0);
     if (!won) return;
-    uint32_t got = 0, first = 0, second = NONE32, jj = 0, lat = 0;
+    uint32_t first = 0, second = NONE32, n1 = 0, n2 = 0;
+    unsigned long long base = 0;
     if (tid == 0) {
-      DispRec r;
-      got = take_next(sl, &r);
-      if (got) {
-        first = begin_iteration(sl, r, P.jobs);
-        jj = r.job;
-        second = eager_second(P.jobs[jj], r.kind, first);
-        lat = (r.kind & REC_FLAG_NARROW) != 0;
-      }
+      // running was clear, so the ring was empty (a holder consumes every
+      // record before releasing): the record just appended at index tl is
+      // the only one -- take it from registers (set running, head + 1)
+      // instead of take_next's round trips through the ring
+      atomicAdd(&sl.qstate, 1ull + QS_HEAD_ONE);
+      const DevJob &JJ = P.jobs[rec.job];
+      const bool narrow = (rec.kind & REC_FLAG_NARROW) != 0;
+      first = first_stage_of(rec, P.jobs);
+      second = eager_second(JJ, rec.kind, first);
+      n1 = stage_ntiles(JJ, first, narrow);
+      n2 = second != NONE32 ? stage_ntiles(JJ, second, narrow) : 0;
+      base = atomicAdd(&P.ctrl->q_head, (unsigned long long)(n1 + n2));   // overlaps the fence below
+      begin_iteration(sl, rec);
     }
-    got = __shfl_sync(0xffffffffu, got, 0);
-    if (!got) return;
     first = __shfl_sync(0xffffffffu, first, 0);
     second = __shfl_sync(0xffffffffu, second, 0);
-    jj = __shfl_sync(0xffffffffu, jj, 0);
-    lat = __shfl_sync(0xffffffffu, lat, 0);
-    enqueue(slot, first, stage_ntiles(P.jobs[jj], first, lat));
+    n1 = __shfl_sync(0xffffffffu, n1, 0);
+    n2 = __shfl_sync(0xffffffffu, n2, 0);
+    base = __shfl_sync(0xffffffffu, base, 0);
     // eager: the second stage's tiles go behind the first's (higher ring
     // positions), so every tile's dependency sits at a lower position
-    if (second != NONE32) enqueue(slot, second, stage_ntiles(P.jobs[jj], second, lat));
+    for (uint32_t k = tid; k < n1 + n2; k += 32) {
+      const unsigned long long pos = base + k;
+      const uint32_t task = k < n1 ? task_pack(slot, first, k) : task_pack(slot, second, k - n1);
+      ptx::st_release_u64(&P.ring[pos & P.ring_mask], ((pos + 1) << 32) | task);
+    }
+    __syncwarp();
   }
 
   // End of the schedule: wait for every slot to drain its ring.
@@ -888,6 +891,7 @@ struct Sched {
 
   // P4: every idle lane dispatches its next iteration
   __device__ void phase_dispatch() {
+
     // one pass over the residents: the minimum key of each slot (a lane owns
     // one slot and a job one lane, so dispatching on one lane never changes
     // another lane's minimum)

@@ -1260,13 +1260,16 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
           // run-ahead: start the slot's next queued iteration right here
           DispRec rec;
           if (take_next(sl, &rec)) {
-            pst = begin_iteration(sl, rec, P.jobs);
+            pst = first_stage_of(rec, P.jobs);
             const DevJob &JN = P.jobs[rec.job];
             const bool narrow = (rec.kind & REC_FLAG_NARROW) != 0;
             pub = 1; ps = td.slot; pn = stage_ntiles(JN, pst, narrow);
             pst2 = eager_second(JN, rec.kind, pst);
             pn2 = pst2 != NONE32 ? stage_ntiles(JN, pst2, narrow) : 0;
+            // reserve the ring positions first: the atomic's round trip
+            // overlaps begin_iteration's fence
             pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)(pn + pn2));
+            begin_iteration(sl, rec);
           }
         } else {
           // the stage two after this one (eager), and in a relaxed record
