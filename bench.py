@@ -255,6 +255,81 @@ def switch_latency(S, device):
             "paper_context": "inference latency overhead < 5 ms average on P100 (P:737)"}
 
 
+def c3_live(S, device, rates=((20, 1.0), (100, 0.5), (1000, 0.2)), seed=3):
+    """C3 in wall-clock time (SURVEY §8(d) C3, NEXT-2 live requests): the 42
+    models stay resident under FAIR over 8 lanes while a host thread submits
+    each model's Poisson requests (rate lambda per model, for `duration` s of
+    wall time) through salus_submit_requests as they fall due.  Per request,
+    from the device's own stamps: queueing = first tile start - the moment the
+    scheduler saw it, latency = last tile end - seen; per lane, the physical
+    switch gap = start - max(previous end, seen).  Sustained = every request
+    served and the run ending within the offered window plus the tail."""
+    import dataclasses
+    base, cap = c3_trace()
+    out = {}
+    for lam, dur in rates:
+        rng = np.random.default_rng(seed)
+        due, jobs = [], []
+        for j in base:
+            t = np.cumsum(rng.exponential(1.0 / lam, size=int(lam * dur * 3) + 8))
+            t = t[t < dur]
+            if len(t) == 0:
+                t = np.array([dur * rng.random()])
+            jobs.append(dataclasses.replace(j, n_iters=len(t), request_ticks=()))
+            due += [(float(x), j.job_id) for x in t]
+        due.sort()
+        ctx = S.Context(jobs, cap, S.FAIR, device=device, max_lanes=8, log=True, online=True)
+        try:
+            ctx.run_async()
+            t0 = time.perf_counter()
+            lag, k = [], 0
+            while k < len(due):
+                now = time.perf_counter() - t0
+                if due[k][0] > now:
+                    if due[k][0] - now > 5e-4:
+                        time.sleep(due[k][0] - now - 3e-4)
+                    continue
+                m = k
+                while m < len(due) and due[m][0] <= now:
+                    m += 1
+                ctx.submit_requests([jid for _, jid in due[k:m]])
+                lag += [now - due[i][0] for i in range(k, m)]
+                k = m
+            ctx.end_submissions()
+            ctx.wait()
+            span = time.perf_counter() - t0
+            w = ctx.wall()
+            seen = {j.job_id: ctx.requests(j.job_id)[1].astype(np.int64) for j in jobs}
+        finally:
+            ctx.close()
+        w = w[np.argsort(w["seq"])]
+        kreq, q, lat, sw, last = {}, [], [], [], {}
+        for r in w:
+            jid = int(r["job"])
+            kk = kreq.get(jid, 0)
+            kreq[jid] = kk + 1
+            s0 = int(seen[jid][kk])
+            q.append((int(r["start_ns"]) - s0) / 1e3)
+            lat.append((int(r["end_ns"]) - s0) / 1e3)
+            ln = int(r["lane"])
+            if ln in last and int(last[ln]["job"]) != jid:
+                sw.append((int(r["start_ns"]) - max(int(last[ln]["end_ns"]), s0)) / 1e3)
+            last[ln] = r
+
+        def pct(a):
+            return {"n": len(a), "p50": float(np.percentile(a, 50)) if a else None,
+                    "p99": float(np.percentile(a, 99)) if a else None,
+                    "max": float(np.max(a)) if a else None}
+        out[f"lambda{lam}"] = {
+            "models": len(jobs), "requests": len(due), "offered_rps": len(due) / dur, "window_s": dur,
+            "served": int(len(w)), "run_s": span,
+            "queueing_us": pct(q), "latency_us": pct(lat), "switch_gap_us": pct(sw),
+            "host_submit_lag_us": pct([x * 1e6 for x in lag])}
+    return {"config": "C3 live: 42 inference models (14 archs x 3), FAIR over 8 lanes, 16 GiB; "
+                      "Poisson requests per model in wall time via salus_submit_requests",
+            "paper_context": "inference latency overhead < 5 ms average on P100 (P:737)", **out}
+
+
 def c1_config(S, device):
     """BASELINE configs[0] (C1: 2 jobs, FIFO vs SRTF): the device schedule's
     average JCT in logical ticks (bit-identical to the oracle's) and the
@@ -624,6 +699,7 @@ def run_reference(args, rank, world):
 SIDE_SECTIONS = {
     "overhead": ("overhead_vs_standalone", lambda S, d, jobs, cap: overhead_vs_standalone(S, d)),
     "c3": ("c3_switch", lambda S, d, jobs, cap: switch_latency(S, d)),
+    "c3live": ("c3_live", lambda S, d, jobs, cap: c3_live(S, d)),
     "c1": ("c1", lambda S, d, jobs, cap: c1_config(S, d)),
     "jct": ("jct_physical", lambda S, d, jobs, cap: jct_physical(S, d, jobs, cap)),
     "c4": ("c4_jct", lambda S, d, jobs, cap: c4_jct(S, d)),

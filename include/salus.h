@@ -202,7 +202,10 @@ typedef struct {
   uint32_t dump;             /* SALUS_DUMP_* bits                                  */
   uint64_t seed;             /* data generator seed (A29)                          */
   const int64_t *request_ticks; /* host; INFER: n_iters non-decreasing ticks
-                                   >= arrival_tick; copied at submit              */
+                                   >= arrival_tick; copied at submit.  NULL in an
+                                   online context (SALUS_FLAG_ONLINE, submitted
+                                   before the run): the job's n_iters requests
+                                   arrive live via salus_submit_requests      */
   /* Migration (NEXT-4): resume a job another context ran for resume_iter
    * iterations.  resume_state (host, copied at submit) is the image that
    * context's salus_read_state returned for a job of identical kind, dims and
@@ -301,6 +304,30 @@ int salus_run_async(salus_ctx *ctx);
 int salus_submit_live(salus_ctx *ctx, const salus_job *job);
 int salus_end_submissions(salus_ctx *ctx);
 int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64_t *n_stats);
+
+/* Live inference requests (online contexts; wall-clock arrival of the
+ * paper's low-rate inference requests, A27: one request = one
+ * iteration).  An INFER job submitted before the run with request_ticks =
+ * NULL receives its n_iters requests while the kernel runs:
+ * salus_submit_requests appends n job ids (host array, copied) to a mapped
+ * pinned request ring and publishes them with one store; the device
+ * scheduler polls the ring (every tick while idle, every 8 ticks while
+ * busy), gives every request it finds at tick t the arrival tick t + 1 (as
+ * A34 does for live jobs) and stamps the globaltimer it saw it at.  The
+ * log is then that of an offline trace with those request ticks, which is
+ * the parity check.  Thread-safe.  Errors: E_STATE (nothing running,
+ * submissions ended), E_INVAL (unknown job, not a live-request job),
+ * E_CAPACITY (more requests than the job's n_iters).  The run ends once
+ * every job -- a live-request job after its n_iters-th request -- is done
+ * and salus_end_submissions was called.
+ *
+ * salus_read_requests: after salus_wait, the job's request ticks (arrival
+ * tick of request k; live: as assigned) and, for live requests, the
+ * globaltimer at which the scheduler saw request k (0 for offline
+ * requests).  Either buffer may be NULL; *n = requests (n_iters). */
+int salus_submit_requests(salus_ctx *ctx, const uint32_t *job_ids, uint32_t n);
+int salus_read_requests(salus_ctx *ctx, uint32_t job_id, int64_t *ticks, uint64_t *seen_ns, uint64_t cap,
+                        uint64_t *n);
 
 /* Streaming statistics: while a salus_run_async is in
  * flight, copy the per-job records as they stand (host `stats`, submit

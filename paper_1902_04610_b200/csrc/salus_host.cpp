@@ -63,6 +63,7 @@ Footprint footprint(const salus_job &j) {
 
 struct HostJob {
   salus_job j;
+  bool live_req = false;              // INFER job whose requests arrive live (salus_submit_requests)
   std::vector<int64_t> req;
   std::vector<uint8_t> resume;        // migration: the persistent image to resume from
   Footprint fp;
@@ -90,7 +91,7 @@ struct salus_ctx {
   uint64_t ring_cap = 0, log_cap = 0;
   uint64_t off_ctrl = 0, off_jobs = 0, off_req = 0, off_inf = 0, off_ppt = 0, off_lpt = 0, off_free = 0,
            off_slots = 0, off_ring = 0, off_fslot = 0, off_fseq = 0, off_pend = 0, off_log = 0, off_wall = 0, off_stats = 0, off_dump = 0, off_trace = 0,
-           off_swfence = 0, off_evl = 0, total = 0;
+           off_swfence = 0, off_evl = 0, off_reqseen = 0, off_lreqcnt = 0, total = 0;
   // caller-owned pinned host swap area: SALUS_FLAG_EVICT (A35) and migration
   // (SALUS_DUMP_STATE / resume_state, NEXT-4); job j's region at pt_off pages
   uint8_t *swap_dev = nullptr, *swap_host = nullptr;
@@ -106,6 +107,10 @@ struct salus_ctx {
   bool running = false, ended = false;
   std::mutex live_mu;
   uint32_t *live = nullptr, *live_dev = nullptr;   // mapped pinned {n_published, closed}
+  // live requests: mapped pinned {n_published, pad, dense job index[lreq_cap]}
+  uint32_t *lreq = nullptr, *lreq_dev = nullptr;
+  uint32_t lreq_cap = 0, lreq_pub = 0;
+  std::vector<uint32_t> lreq_left;                 // per dense job: live requests still to come
   cudaStream_t side = nullptr;                     // private stream for descriptor uploads
   uint64_t ppt_used = 0, ppt_cap = 0, ring_tiles = 0, dump_cur = 0, dump_cap = 0;
   uint32_t max_id = 0, n_pre = 0;
@@ -177,7 +182,7 @@ uint32_t backing_pages(const salus_job &j, const Footprint &fp, bool null_work, 
   return (uint32_t)std::min<uint64_t>((fp.p + G - 1) / G, p_pages);
 }
 
-int validate_job(const salus_job *j, bool null_work, std::string *why) {
+int validate_job(const salus_job *j, bool null_work, std::string *why, bool live_req_ok = false) {
   if (j->kind > SALUS_INFER) { *why = "kind"; return SALUS_E_INVAL; }
   if (j->n_layers < 1 || j->n_layers > MAX_LAYERS) { *why = "n_layers must be 1..8"; return SALUS_E_INVAL; }
   for (uint32_t l = 0; l <= j->n_layers; l++)
@@ -190,9 +195,12 @@ int validate_job(const salus_job *j, bool null_work, std::string *why) {
     return SALUS_E_INVAL;
   }
   if (j->kind == SALUS_INFER) {
-    if (!j->request_ticks) { *why = "INFER job needs request_ticks"; return SALUS_E_INVAL; }
+    if (!j->request_ticks && !live_req_ok) {
+      *why = "INFER job needs request_ticks (NULL = live requests, online contexts only)";
+      return SALUS_E_INVAL;
+    }
     int64_t prev = j->arrival_tick;
-    for (uint32_t k = 0; k < j->n_iters; k++) {
+    for (uint32_t k = 0; j->request_ticks && k < j->n_iters; k++) {
       if (j->request_ticks[k] < prev) { *why = "request_ticks must be sorted and >= arrival"; return SALUS_E_INVAL; }
       prev = j->request_ticks[k];
     }
@@ -261,7 +269,8 @@ int salus_submit_job(salus_ctx *ctx, const salus_job *job) {
   if (ctx->state != 0) return fail(ctx, SALUS_E_STATE, "submit after prepare");
   if (ctx->id_to_submit.count(job->job_id)) return fail(ctx, SALUS_E_DUPLICATE, "duplicate job id");
   std::string why;
-  int rc = validate_job(job, (ctx->cfg.flags & SALUS_FLAG_NULL_WORK) != 0, &why);
+  int rc = validate_job(job, (ctx->cfg.flags & SALUS_FLAG_NULL_WORK) != 0, &why,
+                        (ctx->cfg.flags & SALUS_FLAG_ONLINE) != 0);
   if (rc) return fail(ctx, rc, "job " + std::to_string(job->job_id) + ": " + why);
   const uint64_t G = ctx->cfg.page_bytes;
   const uint64_t p = (job->persistent_bytes + G - 1) / G, e = (job->ephemeral_bytes + G - 1) / G;
@@ -280,7 +289,11 @@ int salus_submit_job(salus_ctx *ctx, const salus_job *job) {
     return fail(ctx, SALUS_E_CAPACITY, "dump_bytes exceeded");
   HostJob h;
   h.j = *job;
-  if (job->kind == SALUS_INFER) h.req.assign(job->request_ticks, job->request_ticks + job->n_iters);
+  if (job->kind == SALUS_INFER && job->request_ticks) h.req.assign(job->request_ticks, job->request_ticks + job->n_iters);
+  if (job->kind == SALUS_INFER && !job->request_ticks) {   // live requests: ticks assigned on arrival
+    h.live_req = true;
+    h.req.assign(job->n_iters, INT64_MAX);
+  }
   h.j.request_ticks = nullptr;
   if (job->resume_state) {
     const uint8_t *r = static_cast<const uint8_t *>(job->resume_state);
@@ -499,6 +512,8 @@ static void compute_layout(salus_ctx *c) {
   c->off_trace = take(sizeof(salus_trace_rec) * std::max<uint64_t>(c->trace_cap, 1));
   c->off_swfence = take(8 * std::max<uint64_t>(n_cap, 1));
   c->off_evl = take(2 * std::max<uint64_t>(n_cap, 1));
+  c->off_reqseen = take(8 * std::max<uint64_t>(req_total, 1));   // live requests: globaltimer when seen
+  c->off_lreqcnt = take(4 * std::max<uint64_t>(n_cap, 1));        // live requests received per job
   c->total = o;
 }
 
@@ -621,7 +636,9 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   }
   P.ctrl = reinterpret_cast<Ctrl *>(m + ctx->off_ctrl);
   P.jobs = reinterpret_cast<const DevJob *>(m + ctx->off_jobs);
-  P.req_ticks = reinterpret_cast<const int64_t *>(m + ctx->off_req);
+  P.req_ticks = reinterpret_cast<int64_t *>(m + ctx->off_req);
+  P.req_seen = reinterpret_cast<uint64_t *>(m + ctx->off_reqseen);
+  P.lreq_cnt = reinterpret_cast<uint32_t *>(m + ctx->off_lreqcnt);
   P.infer_list = reinterpret_cast<const uint16_t *>(m + ctx->off_inf);
   P.ppt = reinterpret_cast<uint32_t *>(m + ctx->off_ppt);
   P.lpt = reinterpret_cast<uint32_t *>(m + ctx->off_lpt);
@@ -671,6 +688,20 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
     if ((e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking))) return cuda_fail(ctx, e, "side stream");
     P.live = ctx->live_dev;
     for (const HostJob &h : ctx->jobs) ctx->max_id = std::max(ctx->max_id, h.j.job_id);
+    ctx->lreq_cap = 0;
+    ctx->lreq_left.assign(ctx->djobs.size(), 0);
+    for (uint32_t d = 0; d < (uint32_t)ctx->djobs.size(); d++) {
+      const HostJob &h = ctx->jobs[ctx->dense_to_submit[d]];
+      if (h.live_req) ctx->lreq_cap += h.j.n_iters;
+    }
+    if (ctx->lreq_cap) {
+      if ((e = cudaHostAlloc(reinterpret_cast<void **>(&ctx->lreq), 4ull * (ctx->lreq_cap + 2), cudaHostAllocMapped)))
+        return cuda_fail(ctx, e, "cudaHostAlloc requests");
+      if ((e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&ctx->lreq_dev), ctx->lreq, 0)))
+        return cuda_fail(ctx, e, "cudaHostGetDevicePointer requests");
+      P.lreq = ctx->lreq_dev;
+      P.n_lreq = ctx->lreq_cap;
+    }
   }
   ctx->state = 1;
   return SALUS_OK;
@@ -687,6 +718,7 @@ int salus_run_async(salus_ctx *ctx) {
   cudaStream_t st = static_cast<cudaStream_t>(ctx->cfg.stream);
   uint8_t *m = ctx->meta;
   if ((e = cudaMemsetAsync(m + ctx->off_ctrl, 0, sizeof(Ctrl), st)) ||
+      (e = cudaMemsetAsync(m + ctx->off_lreqcnt, 0, 4 * std::max<uint64_t>(ctx->n_cap, 1), st)) ||
       (e = cudaMemsetAsync(m + ctx->off_slots, 0, sizeof(Slot) * MAX_LANES, st)) ||
       (e = cudaMemsetAsync(m + ctx->off_ring, 0, 8 * ctx->ring_cap, st)) ||
       (e = cudaMemsetAsync(m + ctx->off_fseq, 0, 8ull * ctx->Cp, st)) ||
@@ -723,6 +755,14 @@ int salus_run_async(salus_ctx *ctx) {
     reinterpret_cast<volatile uint32_t *>(ctx->live)[0] = (uint32_t)ctx->jobs.size();   // published so far
     reinterpret_cast<volatile uint32_t *>(ctx->live)[1] = 0;                           // submissions open
     ctx->ended = false;
+    if (ctx->lreq) {
+      reinterpret_cast<volatile uint32_t *>(ctx->lreq)[0] = 0;
+      ctx->lreq_pub = 0;
+      for (uint32_t d = 0; d < (uint32_t)ctx->djobs.size(); d++) {
+        const HostJob &h = ctx->jobs[ctx->dense_to_submit[d]];
+        ctx->lreq_left[d] = h.live_req ? h.j.n_iters : 0;
+      }
+    }
   }
   int rc = launch_persistent(ctx->P, ctx->grid, st);
   if (rc) return cuda_fail(ctx, (cudaError_t)rc, "cooperative launch");
@@ -749,6 +789,57 @@ int salus_end_submissions(salus_ctx *ctx) {
   std::atomic_thread_fence(std::memory_order_seq_cst);
   reinterpret_cast<volatile uint32_t *>(ctx->live)[1] = 1;
   ctx->ended = true;
+  return SALUS_OK;
+}
+
+int salus_submit_requests(salus_ctx *ctx, const uint32_t *job_ids, uint32_t n) {
+  if (!ctx || (!job_ids && n)) return SALUS_E_INVAL;
+  if (!ctx->live) return fail(ctx, SALUS_E_STATE, "not an online context (SALUS_FLAG_ONLINE)");
+  std::lock_guard<std::mutex> g(ctx->live_mu);
+  if (!ctx->running || ctx->ended) return fail(ctx, SALUS_E_STATE, "no live run accepting submissions");
+  if (!ctx->lreq) return fail(ctx, SALUS_E_INVAL, "no live-request jobs (INFER with request_ticks = NULL)");
+  // check the whole batch before publishing any of it
+  std::unordered_map<uint32_t, uint32_t> take;
+  for (uint32_t i = 0; i < n; i++) {
+    auto it = ctx->id_to_dense.find(job_ids[i]);
+    if (it == ctx->id_to_dense.end() || it->second >= ctx->lreq_left.size() ||
+        !ctx->jobs[ctx->dense_to_submit[it->second]].live_req)
+      return fail(ctx, SALUS_E_INVAL, "job " + std::to_string(job_ids[i]) + " takes no live requests");
+    if (++take[it->second] > ctx->lreq_left[it->second])
+      return fail(ctx, SALUS_E_CAPACITY, "job " + std::to_string(job_ids[i]) + ": more requests than n_iters");
+  }
+  volatile uint32_t *ring = reinterpret_cast<volatile uint32_t *>(ctx->lreq);
+  for (uint32_t i = 0; i < n; i++) {
+    const uint32_t d = ctx->id_to_dense[job_ids[i]];
+    ring[2 + ctx->lreq_pub + i] = d;
+    ctx->lreq_left[d]--;
+  }
+  ctx->lreq_pub += n;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  ring[0] = ctx->lreq_pub;                                         // publish
+  return SALUS_OK;
+}
+
+int salus_read_requests(salus_ctx *ctx, uint32_t job_id, int64_t *ticks, uint64_t *seen_ns, uint64_t cap,
+                        uint64_t *n) {
+  if (!ctx || !n) return SALUS_E_INVAL;
+  if (!ctx->ran || ctx->running) return fail(ctx, SALUS_E_STATE, "no finished run");
+  auto it = ctx->id_to_dense.find(job_id);
+  if (it == ctx->id_to_dense.end()) return fail(ctx, SALUS_E_INVAL, "unknown job");
+  const DevJob &D = ctx->djobs[it->second];
+  *n = D.kind == SALUS_INFER ? D.n_iters : 0;
+  if (!*n || (!ticks && !seen_ns)) return SALUS_OK;
+  if (cap < *n) return fail(ctx, SALUS_E_CAPACITY, "buffer too small");
+  cudaError_t e = cudaSetDevice(ctx->cfg.device);
+  if (e == cudaSuccess && ticks)
+    e = cudaMemcpy(ticks, ctx->meta + ctx->off_req + 8ull * D.req_off, 8 * *n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && seen_ns) {
+    if (ctx->jobs[ctx->dense_to_submit[it->second]].live_req)
+      e = cudaMemcpy(seen_ns, ctx->meta + ctx->off_reqseen + 8ull * D.req_off, 8 * *n, cudaMemcpyDeviceToHost);
+    else
+      std::memset(seen_ns, 0, 8 * *n);
+  }
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "read requests");
   return SALUS_OK;
 }
 
@@ -999,6 +1090,7 @@ int salus_close(salus_ctx *ctx) {
   }
   if (ctx->host_abort) cudaFreeHost(ctx->host_abort);
   if (ctx->live) cudaFreeHost(ctx->live);
+  if (ctx->lreq) cudaFreeHost(ctx->lreq);
   if (ctx->side) cudaStreamDestroy(ctx->side);
   if (ctx->ev0) cudaEventDestroy(ctx->ev0);
   if (ctx->ev1) cudaEventDestroy(ctx->ev1);

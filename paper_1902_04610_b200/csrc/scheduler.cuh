@@ -122,6 +122,7 @@ struct Sched {
   bool physical = true;                      // false in SALUS_FLAG_NULL_WORK
   bool evict_mode = false;                   // SALUS_FLAG_EVICT (A35)
   uint64_t pend_mask = 0;                    // target slots with page-reuse fences
+  uint32_t lreq_seen = 0;                    // live requests taken from the host ring
 
   __device__ Sched(const Params &p_, SchedShared &s_)
       : P(p_), S(s_), tid(threadIdx.x & 31), physical(!(p_.flags & SALUS_FLAG_NULL_WORK)),
@@ -316,16 +317,50 @@ struct Sched {
     if (cl && np == n_jobs) live_done = true;
   }
 
-  // Nothing scheduled and the host may still submit: wait for it.
+  // Live requests (salus_submit_requests): take the requests the host has
+  // published since the last poll, in publication order, and give each the
+  // arrival tick t + 1 (never before its job's arrival) -- strictly after
+  // every processed tick, like A34 -- plus the globaltimer it was seen at.
+  // Returns true if any arrived.
+  __device__ bool poll_requests() {
+    if (!P.n_lreq || lreq_seen >= P.n_lreq) return false;
+    uint32_t np = 0;
+    if (tid == 0) np = ptx::ld_volatile_u32(P.lreq);
+    np = __shfl_sync(0xffffffffu, np, 0);
+    if (np == lreq_seen) return false;
+    if (np > P.n_lreq) { fail(SALUS_E_CAPACITY, 9); return false; }
+    if (tid == 0) {
+      __threadfence_system();                        // the entries were written before the count
+      const uint64_t now = ptx::globaltimer();
+      for (uint32_t k = lreq_seen; k < np; k++) {
+        const uint32_t j = ptx::ld_volatile_u32(P.lreq + 2 + k);
+        const uint32_t c = P.lreq_cnt[j]++;
+        const int64_t arr = P.jobs[j].arrival;
+        const int64_t tk = t + 1 > arr ? t + 1 : arr;
+        P.req_ticks[S.req_off[j] + c] = tk;
+        P.req_seen[S.req_off[j] + c] = now;
+        if (S.next_req[j] == c && S.nrt[j] == IDLE_T) S.nrt[j] = tk;   // the job was waiting for it
+      }
+    }
+    __syncwarp();
+    lreq_seen = np;
+    return true;
+  }
+
+  // Nothing scheduled and the host may still submit jobs or requests: wait.
   __device__ bool wait_live() {
     const uint64_t t0 = ptx::globaltimer();
-    while (!live_done && arr_ptr == n_jobs && !err) {
-      poll_live();
-      if (arr_ptr < n_jobs || live_done) break;
+    while (!err) {
+      if (!live_done) {
+        poll_live();
+        if (arr_ptr < n_jobs || live_done) break;
+      }
+      if (poll_requests()) break;
+      if (live_done && lreq_seen >= P.n_lreq) break;   // nothing more can come
       uint32_t bad = 0;
       if (tid == 0) bad = host_abort() || *(volatile uint32_t *)&P.ctrl->abort;
       if (__shfl_sync(0xffffffffu, bad, 0)) { fail(SALUS_E_TIMEOUT, 8); return false; }
-      __nanosleep(2000);
+      __nanosleep(200);
     }
     wait_ns += ptx::globaltimer() - t0;
     return !err;
@@ -333,7 +368,7 @@ struct Sched {
 
   __device__ void init() {
     const uint32_t N = P.n_jobs;
-    if (P.n_req <= REQ_STAGE) {
+    if (P.n_req <= REQ_STAGE && !P.n_lreq) {          // live requests write the global array
       for (uint32_t i = tid; i < P.n_req; i += 32) S.req_stage[i] = P.req_ticks[i];
       __syncwarp();
       rq = S.req_stage;
@@ -962,11 +997,12 @@ struct Sched {
 #endif
     while (!err) {
       if (!live_done && (n_ticks & 15) == 0) poll_live();
+      if ((n_ticks & 7) == 0) poll_requests();
       if (n_done == n_jobs && live_done) break;
       int64_t tn;
       SALUS_PH(0, tn = next_event())
       if (tn == IDLE_T) {
-        if (!live_done) { if (!wait_live()) break; continue; }
+        if (!live_done || lreq_seen < P.n_lreq) { if (!wait_live()) break; continue; }
         fail(SALUS_E_STUCK, 4);
         break;
       }

@@ -85,7 +85,8 @@ EXPORTS = ["salus_open", "salus_job_footprint", "salus_submit_job", "salus_meta_
            "salus_prepare", "salus_run", "salus_read_run_stats", "salus_read_log",
            "salus_read_wall", "salus_read_trace", "salus_read_layers", "salus_last_error", "salus_close",
            "salus_run_async", "salus_submit_live", "salus_end_submissions", "salus_wait",
-           "salus_swap_bytes", "salus_set_swap", "salus_poll_stats", "salus_read_state"]
+           "salus_swap_bytes", "salus_set_swap", "salus_poll_stats", "salus_read_state",
+           "salus_submit_requests", "salus_read_requests"]
 
 _lib = None
 _POISONED: List[tuple] = []   # buffers of poisoned contexts, kept alive for the process
@@ -118,6 +119,9 @@ def lib():
         L.salus_run_async.argtypes = [P]
         L.salus_submit_live.argtypes = [P, C.POINTER(JobDesc)]
         L.salus_end_submissions.argtypes = [P]
+        L.salus_submit_requests.argtypes = [P, C.POINTER(C.c_uint32), C.c_uint32]
+        L.salus_read_requests.argtypes = [P, C.c_uint32, C.POINTER(C.c_int64), C.POINTER(C.c_uint64),
+                                          C.c_uint64, C.POINTER(C.c_uint64)]
         L.salus_wait.argtypes = [P, C.POINTER(JobStat), C.c_uint64, C.POINTER(C.c_uint64)]
         L.salus_swap_bytes.argtypes = [P, C.POINTER(C.c_uint64)]
         L.salus_set_swap.argtypes = [P, P, C.c_uint64]
@@ -149,7 +153,7 @@ def job_desc(job, dump: int = 0, resume=None):
     d.dump = dump
     d.seed = job.seed & (2**64 - 1)
     keep = None
-    if job.kind == INFER:
+    if job.kind == INFER and len(job.request_ticks):   # empty: live requests (online contexts)
         keep = (C.c_int64 * len(job.request_ticks))(*job.request_ticks)
         d.request_ticks = C.cast(keep, C.POINTER(C.c_int64))
     if resume is not None:                       # migration (NEXT-4): (state image, iterations done)
@@ -273,6 +277,24 @@ class Context:
 
     def end_submissions(self):
         self._check(self.L.salus_end_submissions(self.ctx), "end_submissions")
+
+    def submit_requests(self, job_ids):
+        """Live inference requests: one request per entry, for INFER jobs
+        submitted with no request ticks (arrival stamped on device)."""
+        ids = np.ascontiguousarray(job_ids, dtype=np.uint32)
+        self._check(self.L.salus_submit_requests(self.ctx, ids.ctypes.data_as(C.POINTER(C.c_uint32)), len(ids)),
+                    "submit_requests")
+
+    def requests(self, job_id: int):
+        """(request ticks, globaltimer at which each live request was seen)."""
+        n = C.c_uint64()
+        self._check(self.L.salus_read_requests(self.ctx, job_id, None, None, 0, C.byref(n)), "requests size")
+        ticks = np.zeros(n.value, dtype=np.int64)
+        seen = np.zeros(n.value, dtype=np.uint64)
+        self._check(self.L.salus_read_requests(self.ctx, job_id, ticks.ctypes.data_as(C.POINTER(C.c_int64)),
+                                               seen.ctypes.data_as(C.POINTER(C.c_uint64)), n.value,
+                                               C.byref(n)), "requests")
+        return ticks, seen
 
     def wait(self) -> Dict[int, dict]:
         """Wait for the run to finish; returns {job_id: stat dict}."""

@@ -177,3 +177,117 @@ def test_poll_stats_streams_completions():
         for jid, s in st.items():
             if s["wall_end_ns"]:
                 assert s == final[jid], jid
+
+
+# --------------------------------------------------------------------------
+# Live inference requests (salus_submit_requests): the paper's low-rate
+# inference requests arriving in wall-clock time (A27).  Each
+# request the scheduler sees at tick t gets arrival tick t + 1; parity =
+# replaying the read-back request ticks through the oracle gives the log.
+# --------------------------------------------------------------------------
+
+def _infer(job_id, seed, n, dims=(256, 512, 128), b=8):
+    from workloads import INFER
+    from workloads.traces import footprint_bytes
+    p, e = footprint_bytes(INFER, dims, b)
+    return make_job(job_id, INFER, 0, dims, b, n, seed=seed, request_ticks=tuple([0] * n),
+                    persistent_bytes=p, ephemeral_bytes=e)
+
+
+def _live_request_run(policy, jobs, cap, schedule, max_lanes=0, dump=None, null_work=False):
+    """jobs: INFER jobs (their request_ticks are ignored: live); schedule:
+    list of (delay_s, [job ids]) batches."""
+    from paper_1902_04610_b200 import salus as S
+    live = [dataclasses.replace(j, request_ticks=()) for j in jobs]
+    ctx = S.Context(live, cap, policy, online=True, max_lanes=max_lanes, dump=dump, null_work=null_work)
+    ctx.run_async()
+    for dt, ids in schedule:
+        if dt:
+            time.sleep(dt)
+        ctx.submit_requests(ids)
+    ctx.end_submissions()
+    stats = ctx.wait()
+    return ctx, stats
+
+
+def _replay_requests(ctx, jobs, cap, policy, stats, max_lanes=0):
+    got = ctx.log_bytes()
+    replay, seen = [], {}
+    for j in jobs:
+        ticks, s = ctx.requests(j.job_id)
+        assert np.all(np.diff(ticks) >= 0) and np.all(s > 0)
+        seen[j.job_id] = s
+        replay.append(dataclasses.replace(j, request_ticks=tuple(int(x) for x in ticks)))
+    ref = OS.simulate(replay, cap, policy, max_lanes=max_lanes)
+    want = ref.log_bytes()
+    assert got == want, first_diff(got, want)
+    for jid, s in ref.stats.items():
+        assert stats[jid]["completion_tick"] == s.completion_tick
+    return replay, seen
+
+
+@pytest.mark.parametrize("policy,max_lanes", [(OS.PACK, 0), (OS.FAIR, 2), (OS.FAIR, 1)])
+def test_live_requests_replay_to_the_oracle_log(policy, max_lanes):
+    jobs = [_infer(i, 300 + i, 12) for i in range(5)]
+    rng = np.random.default_rng(7)
+    order = [j.job_id for j in jobs for _ in range(j.n_iters)]
+    rng.shuffle(order)
+    # batches of 1-3 requests, 0-300 us apart (some arrive while lanes are busy)
+    schedule, k = [], 0
+    while k < len(order):
+        n = int(rng.integers(1, 4))
+        schedule.append((float(rng.choice([0.0, 1e-4, 3e-4])), order[k:k + n]))
+        k += n
+    ctx, stats = _live_request_run(policy, jobs, 1 << 30, schedule, max_lanes=max_lanes)
+    try:
+        _replay_requests(ctx, jobs, 1 << 30, policy, stats, max_lanes=max_lanes)
+    finally:
+        ctx.close()
+
+
+def test_live_requests_math_and_latency_stamps():
+    """Outputs of live requests equal the oracle's (data keyed by the request
+    index, A29), and every request's first tile starts after it was seen."""
+    from paper_1902_04610_b200 import salus as S
+    jobs = [_infer(0, 401, 6, dims=(512, 1024, 256), b=16), _infer(1, 402, 6, dims=(128, 384, 64), b=1)]
+    schedule = [(2e-4, [0, 1]) for _ in range(6)]
+    ctx, stats = _live_request_run(OS.PACK, jobs, 1 << 30, schedule,
+                                   dump={0: S.DUMP_OUTPUTS, 1: S.DUMP_OUTPUTS})
+    try:
+        replay, seen = _replay_requests(ctx, jobs, 1 << 30, OS.PACK, stats)
+        for j in replay:
+            outs, _ = OL.run_job(j)
+            for k in range(j.n_iters):
+                g = ctx.layers(j.job_id, k).reshape(j.batch, j.dims[-1])
+                assert normwise_rel(g, outs[k]) <= 2e-2, (j.job_id, k)
+        w = ctx.wall()
+        for j in jobs:
+            starts = np.sort(w["start_ns"][w["job"] == j.job_id].astype(np.int64))
+            assert len(starts) == j.n_iters
+            assert np.all(starts >= seen[j.job_id].astype(np.int64))
+    finally:
+        ctx.close()
+
+
+def test_live_request_errors():
+    from paper_1902_04610_b200 import salus as S
+    jobs = [_infer(0, 501, 2)]
+    ctx = S.Context([dataclasses.replace(jobs[0], request_ticks=())], 1 << 30, OS.PACK, online=True,
+                    null_work=True)
+    try:
+        with pytest.raises(S.SalusError):
+            ctx.submit_requests([0])                      # not running
+        ctx.run_async()
+        with pytest.raises(S.SalusError):
+            ctx.submit_requests([7])                      # unknown job
+        with pytest.raises(S.SalusError):
+            ctx.submit_requests([0, 0, 0])                # more than n_iters: nothing published
+        ctx.submit_requests([0, 0])
+        ctx.end_submissions()
+        stats = ctx.wait()
+        assert stats[0]["completion_tick"] > 0
+    finally:
+        ctx.close()
+    # an offline context needs request ticks
+    with pytest.raises(S.SalusError):
+        S.Context([dataclasses.replace(jobs[0], request_ticks=())], 1 << 30, OS.PACK)
