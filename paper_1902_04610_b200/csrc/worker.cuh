@@ -92,6 +92,11 @@ struct OpDesc {
 #ifndef SALUS_L2HINT
 #define SALUS_L2HINT 1
 #endif
+// SGD epilogue: the fp32 master chunk is updated in its smem buffer and
+// written back with one 32 KiB bulk (TMA) store per chunk
+#ifndef SALUS_W32_BULK
+#define SALUS_W32_BULK 1
+#endif
 
 
 struct TileDesc {
@@ -540,7 +545,12 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
         w.y = fmaf(-td.lr, v[4 * g + 1], w.y);
         w.z = fmaf(-td.lr, v[4 * g + 2], w.z);
         w.w = fmaf(-td.lr, v[4 * g + 3], w.w);
-#if SALUS_L2HINT
+#if SALUS_W32_BULK
+        // updated in place: the chunk goes back to HBM as one bulk store
+        // (epilogue_warps) instead of 128 KiB of register stores per tile
+        *const_cast<float4 *>(wp) = w;
+        (void)grp;
+#elif SALUS_L2HINT
         ptx::st_global_v4_hint(tds.ptr[PTR_W32 + (grp >> 5)] + (grp & 31u) * 2048u + r * 16u,
                                make_uint4(__float_as_uint(w.x), __float_as_uint(w.y), __float_as_uint(w.z),
                                           __float_as_uint(w.w)),
@@ -1133,6 +1143,9 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
   const uint32_t h = (warp - EPI_WARP0) >> 2;     // column half (8 epilogue warps)
   const uint32_t et = tid - 32 * EPI_WARP0;       // 0..EPI_THREADS-1
   uint32_t d = 0, d_phase = 0, b = 0, b_phase = 0, e = 0, e_phase = 0;
+#if SALUS_W32_BULK
+  const uint64_t pol_w32 = ptx::policy_evict_first();   // fp32 masters stream
+#endif
   for (;;) {
     ptx::mbar_wait_abortable(&W.desc_full[d], d_phase, &P.ctrl->abort);
     const TileDesc &td = W.desc[d];
@@ -1162,10 +1175,28 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
         for (uint32_t c = 0; c < n; c++) {
           ptx::mbar_wait_abortable(&W.epi_full[e], e_phase, &P.ctrl->abort);
           epilogue_cols(P, td, ev, tacc, r, c * per, c * per + h * sub, c * per + (h + 1) * sub, W.epi_in[e]);
+#if SALUS_W32_BULK
+          if (td.epi == EPI_SGD) {
+            // the updated master chunk (contiguous in HBM: half a 64 KiB page)
+            // leaves smem in one bulk store; the buffer is handed back only
+            // once the TMA unit has read it
+            ptx::fence_proxy_async_smem();
+            named_bar(2, EPI_THREADS);
+            if (et == 0) {
+              ptx::bulk_s2g_hint(td.ptr[PTR_W32 + (c >> 1)] + (c & 1) * 32768u, W.epi_in[e], ECH_BYTES, pol_w32);
+              ptx::bulk_commit();
+              ptx::bulk_wait_read0();
+            }
+          }
+#endif
           __syncwarp();                               // each warp releases the chunk on its own
           if (lane == 0) ptx::mbar_arrive(&W.epi_empty[e]);
           if (++e == EBUF) { e = 0; e_phase ^= 1; }
         }
+#if SALUS_W32_BULK
+        // the tile completes only once its master writes are performed
+        if (td.epi == EPI_SGD && et == 0) { ptx::bulk_wait0(); ptx::fence_proxy_async_global(); }
+#endif
       }
       ptx::tc_fence_before();
       named_bar(1, EPI_THREADS);
