@@ -40,3 +40,62 @@ def place_lpt(jobs: Sequence, G: int) -> List[list]:
 
 def loads(parts) -> List[int]:
     return [sum(j.n_iters * j.iter_ticks for j in p) for p in parts]
+
+
+def rebalance(parts, cap, policy, max_moves=4, tol=0.05):
+    """Drain-time migration (reading A39), written out with the
+    oracle's own schedule simulation: while the busiest GPU m finishes more
+    than tol x its makespan after the first GPU d to drain, at T = d's
+    makespan move the rest of m's job with the most remaining logical work
+    (n - k) * c -- k = its iterations finished by T -- to d, arriving at T;
+    m keeps the first k.  The move is made only if afterwards both m and d
+    finish before m did; no GPU is both a source and a target.
+    Returns (moves [(job_id, src, dst, k, T)], makespans)."""
+    import dataclasses
+    from . import scheduler as OS
+    parts = [list(p) for p in parts]
+
+    def run(p):
+        r = OS.simulate(p, cap, policy)
+        ticks = {}
+        for rec in r.dispatch:                      # (seq, tick, lane, job, iter, busy_until)
+            ticks.setdefault(rec[3], []).append(rec[1])
+        return ticks, max([s.completion_tick for s in r.stats.values()] + [0])
+
+    res = [run(p) for p in parts]
+    moves, srcs, dsts = [], [], []
+    while len(moves) < max_moves:
+        ms = [x[1] for x in res]
+        d = ms.index(min(ms))                       # first (lowest) rank with the least
+        m = ms.index(max(ms))                       # first (lowest) rank with the most
+        if d == m or d in srcs or m in dsts or ms[m] - ms[d] <= tol * ms[m]:
+            break
+        T = ms[d]
+        pick = None
+        for j in sorted(parts[m], key=lambda x: x.job_id):
+            k = 0
+            for t in res[m][0].get(j.job_id, []):
+                if t + j.iter_ticks <= T:
+                    k += 1
+            if k == j.n_iters:
+                continue
+            rem = (j.n_iters - k) * j.iter_ticks
+            if pick is None or rem > pick[0]:
+                pick = (rem, j, k)
+        if pick is None:
+            break
+        _, j, k = pick
+        rest = [x for x in parts[m] if x.job_id != j.job_id]
+        if k > 0:
+            rest.append(dataclasses.replace(j, n_iters=k))
+        rest = sorted(rest, key=lambda x: (x.arrival_tick, x.job_id))
+        moved = dataclasses.replace(j, n_iters=j.n_iters - k, arrival_tick=max(T, j.arrival_tick))
+        more = sorted(parts[d] + [moved], key=lambda x: (x.arrival_tick, x.job_id))
+        rm, rd = run(rest), run(more)
+        if max(rm[1], rd[1]) >= ms[m]:              # no gain for the busier of the two: stop
+            break
+        parts[m], parts[d], res[m], res[d] = rest, more, rm, rd
+        moves.append((j.job_id, m, d, k, T))
+        srcs.append(m)
+        dsts.append(d)
+    return moves, [x[1] for x in res]

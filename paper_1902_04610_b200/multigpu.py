@@ -89,3 +89,137 @@ def progress(ctx, world: int, device=None):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return int(t.item())
+
+
+# --------------------------------------------------------------------------
+# Automatic migration at drain time (NEXT-4, reading A39 of DESIGN.md)
+# --------------------------------------------------------------------------
+
+def device_schedule(jobs, cap, policy, device=0, **kw):
+    """The logical schedule of one instance as this package's own device
+    scheduler computes it (a schedule-only run, SALUS_FLAG_NULL_WORK):
+    ({job_id: sorted dispatch ticks}, makespan in ticks)."""
+    from . import salus as S
+    ctx = S.Context(jobs, cap, policy, device=device, null_work=True, log=True, **kw)
+    try:
+        stats = ctx.run()
+        log = np.frombuffer(ctx.log_bytes(), dtype=S.LOG_DTYPE)
+    finally:
+        ctx.close()
+    disp = log[log["kind"] == 1]                          # DISPATCH records
+    ticks: Dict[int, list] = {}
+    for jid, t in zip(disp["job"].tolist(), disp["tick"].tolist()):
+        ticks.setdefault(int(jid), []).append(int(t))
+    makespan = max((int(s["completion_tick"]) for s in stats.values()), default=0)
+    return ticks, makespan
+
+
+def plan_rebalance(parts, schedule, max_moves: int = 4, tol: float = 0.05):
+    """Drain-time migration planner over G independent instances.
+
+    parts: per rank, its jobs (workloads.Job-like: job_id, n_iters,
+    iter_ticks, arrival_tick).  schedule(rank, jobs) -> ({job_id: dispatch
+    ticks}, makespan): the rank's logical schedule.  Repeatedly, while the
+    busiest rank m's makespan exceeds the first-draining rank d's by more
+    than tol x makespan[m]: at T = makespan[d], the job on m with the most
+    remaining logical work (n - k) * c, k = its iterations completed by T
+    (dispatch + c <= T), leaves m at that iteration boundary -- m keeps its
+    first k iterations, d runs the other n - k, arriving at T, resumed from
+    m's state image (A37).  A rank is never both a source and a target.
+    Returns (moves [(job_id, src, dst, k, T)], new parts, makespans)."""
+    import dataclasses
+    parts = [list(p) for p in parts]
+    scheds = [schedule(r, p) for r, p in enumerate(parts)]
+    moves, srcs, dsts = [], set(), set()
+    for _ in range(max_moves):
+        ms = [s[1] for s in scheds]
+        d = min(range(len(ms)), key=lambda r: (ms[r], r))
+        m = max(range(len(ms)), key=lambda r: (ms[r], -r))
+        if d == m or d in srcs or m in dsts or ms[m] - ms[d] <= tol * ms[m]:
+            break
+        T = ms[d]
+        best = None
+        for j in parts[m]:
+            ticks = scheds[m][0].get(j.job_id, [])
+            k = sum(1 for t in ticks if t + j.iter_ticks <= T)
+            rem = (j.n_iters - k) * j.iter_ticks
+            if k < j.n_iters and (best is None or (rem, -j.job_id) > (best[0], -best[1].job_id)):
+                best = (rem, j, k)
+        if best is None:
+            break
+        rem, j, k = best
+        keep = [x for x in parts[m] if x.job_id != j.job_id]
+        if k > 0:
+            keep.append(dataclasses.replace(j, n_iters=k))
+        new_m = sorted(keep, key=lambda x: (x.arrival_tick, x.job_id))
+        new_d = sorted(parts[d] + [dataclasses.replace(j, n_iters=j.n_iters - k, arrival_tick=max(T, j.arrival_tick))],
+                       key=lambda x: (x.arrival_tick, x.job_id))
+        sm, sd = schedule(m, new_m), schedule(d, new_d)
+        if max(sm[1], sd[1]) >= ms[m]:                 # a job's iterations are sequential: moving the
+            break                                      # tail only pays if m has other work behind it
+        parts[m], parts[d], scheds[m], scheds[d] = new_m, new_d, sm, sd
+        moves.append((j.job_id, m, d, k, T))
+        srcs.add(m)
+        dsts.add(d)
+    return moves, parts, [s[1] for s in scheds]
+
+
+def plan_rebalance_dist(my_jobs, rank: int, world: int, schedule, max_moves: int = 4, tol: float = 0.05):
+    """plan_rebalance run by every rank on its own partition, with
+    collectives instead of a central planner: per step one all_gather of
+    the makespans (all ranks then agree on m, d and T), the source m alone
+    computes its candidate and broadcasts it, every rank applies the move to
+    its own partition and m and d re-schedule.  schedule(jobs) -> (ticks,
+    makespan) of this rank.  Returns (moves, my new jobs, makespans)."""
+    import dataclasses
+    import torch.distributed as dist
+    mine = sorted(my_jobs, key=lambda x: (x.arrival_tick, x.job_id))
+    sched = schedule(mine)
+    moves, srcs, dsts = [], set(), set()
+    while True:
+        ms = [None] * world
+        if world > 1:
+            dist.all_gather_object(ms, sched[1])
+        else:
+            ms = [sched[1]]
+        if len(moves) >= max_moves:
+            break
+        d = min(range(world), key=lambda r: (ms[r], r))
+        m = max(range(world), key=lambda r: (ms[r], -r))
+        if d == m or d in srcs or m in dsts or ms[m] - ms[d] <= tol * ms[m]:
+            break
+        T = ms[d]
+        cand = [None]
+        if rank == m:
+            best = None
+            for j in mine:
+                k = sum(1 for t in sched[0].get(j.job_id, []) if t + j.iter_ticks <= T)
+                rem = (j.n_iters - k) * j.iter_ticks
+                if k < j.n_iters and (best is None or (rem, -j.job_id) > (best[0], -best[1].job_id)):
+                    best = (rem, j, k)
+            cand = [None if best is None else (best[1], best[2])]
+        if world > 1:
+            dist.broadcast_object_list(cand, src=m)
+        if cand[0] is None:
+            break
+        j, k = cand[0]
+        trial = mine
+        if rank == m:
+            trial = [x for x in mine if x.job_id != j.job_id] + ([dataclasses.replace(j, n_iters=k)] if k else [])
+        if rank == d:
+            trial = mine + [dataclasses.replace(j, n_iters=j.n_iters - k, arrival_tick=max(T, j.arrival_tick))]
+        trial = sorted(trial, key=lambda x: (x.arrival_tick, x.job_id))
+        tsched = schedule(trial) if rank in (m, d) else sched
+        # accepted only if it lowers the busier of the two (all ranks agree)
+        tm = [None] * world
+        if world > 1:
+            dist.all_gather_object(tm, tsched[1])
+        else:
+            tm = [tsched[1]]
+        if max(tm[m], tm[d]) >= ms[m]:
+            break
+        mine, sched = trial, tsched
+        moves.append((j.job_id, m, d, k, T))
+        srcs.add(m)
+        dsts.add(d)
+    return moves, mine, ms

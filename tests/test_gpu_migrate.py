@@ -106,3 +106,35 @@ def test_resumed_job_under_eviction():
         assert np.array_equal(ctx.layers(0, S.WEIGHTS), W_straight)
     finally:
         ctx.close()
+
+
+def test_rebalance_plan_from_device_schedules_equals_oracle():
+    """NEXT-4 (A39): the drain-time migration plan computed from this
+    package's own device schedules (schedule-only runs) equals the oracle
+    rule's, and the migrated job's two parts give the uninterrupted job's
+    weights bit for bit."""
+    from oracle import placement as OP
+    from paper_1902_04610_b200 import multigpu as MG, salus as S
+    from workloads import c4_trace
+    jobs, cap = c4_trace(n_jobs=40, seed=11, burst=True)
+    parts = OP.place_mod(jobs, 3)
+    moves, new, ms = MG.plan_rebalance(parts, lambda r, p: MG.device_schedule(p, cap, OS.PACK))
+    assert (moves, ms) == OP.rebalance(parts, cap, OS.PACK) and moves
+    jid, src, dst, k, T = moves[0]
+    full = [j for j in jobs if j.job_id == jid][0]
+    small = dataclasses.replace(full, n_iters=min(full.n_iters, k + 3))   # a short run of the same job
+    ctx = _run([small], {jid: S.DUMP_WEIGHTS}, cap=cap)
+    W_straight = ctx.layers(jid, S.WEIGHTS).copy()
+    ctx.close()
+    if k:
+        ctx = _run([dataclasses.replace(small, n_iters=k)], {jid: S.DUMP_STATE}, cap=cap)
+        img = ctx.read_state(jid)
+        ctx.close()
+        rest = dataclasses.replace(small, n_iters=small.n_iters - k, arrival_tick=T)
+        ctx = _run([rest], {jid: S.DUMP_WEIGHTS}, resume={jid: (img, k)}, cap=cap)
+    else:
+        ctx = _run([dataclasses.replace(small, arrival_tick=T)], {jid: S.DUMP_WEIGHTS}, cap=cap)
+    try:
+        assert np.array_equal(ctx.layers(jid, S.WEIGHTS), W_straight)
+    finally:
+        ctx.close()

@@ -167,3 +167,87 @@ def test_lpt_balances_c5_better_than_mod():
         assert sum(lm) == sum(ll)
         assert max(ll) <= max(lm)
         assert max(ll) <= 1.01 * sum(ll) / G      # near-perfect balance on 2000 jobs
+
+
+# ---------------------------------------------------------------- NEXT-4 migration (A39)
+
+def _oracle_schedule(cap, policy):
+    def sched(jobs):
+        r = OS.simulate(jobs, cap, policy)
+        ticks = {}
+        for rec in r.dispatch:
+            ticks.setdefault(rec[3], []).append(rec[1])
+        return ticks, max([s.completion_tick for s in r.stats.values()] + [0])
+    return sched
+
+
+def test_rebalance_hand_worked():
+    """Two GPUs under FIFO.  (a) GPU0 = one job of 10 x 100 ticks, GPU1 = 2 x 100:
+    moving the long job's last 8 iterations at T = 200 would only shift the
+    finish (200 + 800 = 1000 = before): no move.  (b) GPU0 also holds a job
+    of 5 x 100 queued behind it (FIFO: done at 1500): at T = 200 the long
+    job has finished k = 2 iterations (dispatched at 0 and 100), its 800
+    remaining ticks beat the queued job's 500, so it moves: GPU1 ends at
+    200 + 800 = 1000, GPU0 at 200 + 500 = 700."""
+    from oracle import placement as OP
+    from workloads import make_job, TRAIN
+    a = make_job(0, TRAIN, 0, (128, 128), 128, 10, iter_ticks=100)
+    b = make_job(1, TRAIN, 0, (128, 128), 128, 2, iter_ticks=100)
+    q = make_job(2, TRAIN, 0, (128, 128), 128, 5, iter_ticks=100)
+    assert OP.rebalance([[a], [b]], 1 << 30, OS.FIFO) == ([], [1000, 200])
+    assert OP.rebalance([[a, q], [b]], 1 << 30, OS.FIFO) == ([(0, 0, 1, 2, 200)], [700, 1000])
+    sched = _oracle_schedule(1 << 30, OS.FIFO)
+    moves, parts, ms = MG.plan_rebalance([[a, q], [b]], lambda r, p: sched(p))
+    assert (moves, ms) == ([(0, 0, 1, 2, 200)], [700, 1000])
+    assert [(j.job_id, j.n_iters, j.arrival_tick) for j in parts[1]] == [(1, 2, 0), (0, 8, 200)]
+
+
+@pytest.mark.parametrize("G,seed", [(2, 9), (3, 9), (3, 11), (4, 12)])
+def test_rebalance_planner_equals_oracle_rule(G, seed):
+    from oracle import placement as OP
+    jobs, cap = c4_trace(n_jobs=40, seed=seed, burst=True)
+    parts = OP.place_mod(jobs, G)
+    sched = _oracle_schedule(cap, OS.PACK)
+    moves, _, ms = MG.plan_rebalance(parts, lambda r, p: sched(p))
+    assert (moves, ms) == OP.rebalance(parts, cap, OS.PACK)
+    before = [sched(p)[1] for p in parts]
+    assert max(ms) <= max(before)
+
+
+def _rebalance_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        jobs, cap = c4_trace(n_jobs=40, seed=11, burst=True)
+        mine = MG.partition_jobs(jobs, world, rank)
+        moves, new, ms = MG.plan_rebalance_dist(mine, rank, world, _oracle_schedule(cap, OS.PACK))
+        out[rank] = (moves, [(j.job_id, j.n_iters, j.arrival_tick) for j in new], ms)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_world3_rebalance_matches_oracle():
+    """The collective planner (every rank on its own partition: all_gather of
+    makespans, the source broadcasts its candidate) against the oracle rule."""
+    from oracle import placement as OP
+    world, port = 3, _free_port()
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as m:
+        out = m.dict()
+        procs = [ctx.Process(target=_rebalance_worker, args=(r, world, port, out)) for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(300)
+            assert p.exitcode == 0
+        got = [out[r] for r in range(world)]
+    jobs, cap = c4_trace(n_jobs=40, seed=11, burst=True)
+    parts = OP.place_mod(jobs, world)
+    want_moves, want_ms = OP.rebalance(parts, cap, OS.PACK)
+    assert want_moves                                   # this trace does migrate
+    for r in range(world):
+        assert got[r][0] == want_moves and got[r][2] == want_ms
+    for jid, src, dst, k, T in want_moves:
+        assert (jid, [j for j in jobs if j.job_id == jid][0].n_iters - k, T) in \
+            [(a, n, t) for a, n, t in got[dst][1]]
