@@ -282,19 +282,7 @@ def c3_live(S, device, rates=((20, 1.0), (100, 0.5), (1000, 0.2)), seed=3):
         try:
             ctx.run_async()
             t0 = time.perf_counter()
-            lag, k = [], 0
-            while k < len(due):
-                now = time.perf_counter() - t0
-                if due[k][0] > now:
-                    if due[k][0] - now > 5e-4:
-                        time.sleep(due[k][0] - now - 3e-4)
-                    continue
-                m = k
-                while m < len(due) and due[m][0] <= now:
-                    m += 1
-                ctx.submit_requests([jid for _, jid in due[k:m]])
-                lag += [now - due[i][0] for i in range(k, m)]
-                k = m
+            lag = ctx.serve(due)
             ctx.end_submissions()
             ctx.wait()
             span = time.perf_counter() - t0

@@ -99,3 +99,43 @@ def rebalance(parts, cap, policy, max_moves=4, tol=0.05):
         srcs.append(m)
         dsts.append(d)
     return moves, [x[1] for x in res]
+
+
+def autoscale(rates, service_s, util_target=0.5, max_gpus=8):
+    """Request-rate autoscaling (reading A40), written out:
+    load_m = rate_m * service_m; G = ceil(sum load / util_target) clamped to
+    [1, max_gpus]; model m gets ceil(load_m / util_target) replicas (at
+    least 1, at most G) of load load_m / replicas each; replicas visited by
+    (-load, model, replica index), each to the GPU with the least load among
+    those not holding the model yet (all GPUs if every one does), ties to
+    the lowest GPU.  Returns (G, {model: [gpu per replica]}, per-GPU load)."""
+    import math
+    load = {}
+    for m in rates:
+        load[m] = rates[m] * service_s[m]
+    total = 0.0
+    for m in load:
+        total += load[m]
+    G = math.ceil(total / util_target - 1e-12)
+    G = max(1, min(max_gpus, G))
+    reps = []
+    for m in sorted(load):
+        r = math.ceil(load[m] / util_target - 1e-12)
+        r = max(1, min(G, r))
+        for i in range(r):
+            reps.append((-(load[m] / r), m, i))
+    reps.sort()
+    per_gpu = [0.0] * G
+    where = {}
+    for m in load:
+        where[m] = []
+    for neg, m, i in reps:
+        best = None
+        for g in range(G):
+            if g in where[m] and len(where[m]) < G:
+                continue
+            if best is None or per_gpu[g] < per_gpu[best]:
+                best = g
+        where[m].append(best)
+        per_gpu[best] += -neg
+    return G, where, per_gpu

@@ -223,3 +223,43 @@ def plan_rebalance_dist(my_jobs, rank: int, world: int, schedule, max_moves: int
         srcs.add(m)
         dsts.add(d)
     return moves, mine, ms
+
+
+# --------------------------------------------------------------------------
+# Request-rate autoscaling of inference models (NEXT-4; reading A40)
+# --------------------------------------------------------------------------
+
+def request_rates(arrivals, t_end: float, window: float):
+    """{model: requests per second} over the window (t_end - window, t_end]
+    of each model's arrival times (seconds)."""
+    return {m: sum(1 for t in ts if t_end - window < t <= t_end) / window for m, ts in arrivals.items()}
+
+
+def autoscale(rates, service_s, util_target: float = 0.5, max_gpus: int = 8):
+    """How many GPUs the inference models need and where each runs.
+
+    A model's load is rate x per-request service time (GPU-seconds per
+    second); the fleet gets G = ceil(total load / util_target) GPUs
+    (1..max_gpus) -- consolidation when requests are slow, scale-out when
+    they are not -- and a model whose own load exceeds util_target gets
+    ceil(load / util_target) replicas (<= G) sharing its requests equally.
+    Replicas are placed longest first on the least-loaded GPU that does not
+    yet hold the model (ties: lowest GPU).  Returns (G, {model: [gpus]},
+    per-GPU load)."""
+    import math
+    load = {m: rates[m] * service_s[m] for m in rates}
+    total = sum(load.values())
+    G = min(max_gpus, max(1, math.ceil(total / util_target - 1e-12)))
+    items = []
+    for m in sorted(load):
+        rep = min(G, max(1, math.ceil(load[m] / util_target - 1e-12)))
+        items += [(load[m] / rep, m, i) for i in range(rep)]
+    items.sort(key=lambda x: (-x[0], x[1], x[2]))
+    gpu_load = [0.0] * G
+    place = {m: [] for m in load}
+    for w, m, _ in items:
+        free = [g for g in range(G) if g not in place[m]] or list(range(G))
+        g = min(free, key=lambda x: (gpu_load[x], x))
+        place[m].append(g)
+        gpu_load[g] += w
+    return G, place, gpu_load

@@ -285,6 +285,28 @@ class Context:
         self._check(self.L.salus_submit_requests(self.ctx, ids.ctypes.data_as(C.POINTER(C.c_uint32)), len(ids)),
                     "submit_requests")
 
+    def serve(self, due):
+        """Submit live requests at their wall-clock times: `due` = sorted
+        (seconds from now, job_id) pairs; requests that fall due together go
+        in one salus_submit_requests call.  Returns each request's submit lag
+        (seconds after its due time)."""
+        import time
+        t0 = time.perf_counter()
+        lag, k = [], 0
+        while k < len(due):
+            now = time.perf_counter() - t0
+            if due[k][0] > now:
+                if due[k][0] - now > 5e-4:
+                    time.sleep(due[k][0] - now - 3e-4)
+                continue
+            m = k
+            while m < len(due) and due[m][0] <= now:
+                m += 1
+            self.submit_requests([jid for _, jid in due[k:m]])
+            lag += [now - due[i][0] for i in range(k, m)]
+            k = m
+        return lag
+
     def requests(self, job_id: int):
         """(request ticks, globaltimer at which each live request was seen)."""
         n = C.c_uint64()

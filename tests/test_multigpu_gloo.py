@@ -251,3 +251,39 @@ def test_gloo_world3_rebalance_matches_oracle():
     for jid, src, dst, k, T in want_moves:
         assert (jid, [j for j in jobs if j.job_id == jid][0].n_iters - k, T) in \
             [(a, n, t) for a, n, t in got[dst][1]]
+
+
+# ---------------------------------------------------------------- NEXT-4 autoscaling (A40)
+
+def test_autoscale_hand_worked():
+    """Loads 0.1, 0.1, 0.8 GPU-s/s at a 0.5 target: G = ceil(1.0 / 0.5) = 2;
+    model 2 gets ceil(0.8 / 0.5) = 2 replicas of 0.4 (one per GPU), models 0
+    and 1 fill to 0.5 each.  At a tenth of the rates one GPU takes all."""
+    from oracle import placement as OP
+    rates, svc = {0: 1000, 1: 500, 2: 4000}, {0: 1e-4, 1: 2e-4, 2: 2e-4}
+    want = (2, {0: [0], 1: [1], 2: [0, 1]}, [0.5, 0.5])
+    assert OP.autoscale(rates, svc) == want
+    assert MG.autoscale(rates, svc) == want
+    low = {m: r / 10 for m, r in rates.items()}
+    G, place, load = MG.autoscale(low, svc)
+    assert G == 1 and all(p == [0] for p in place.values())
+
+
+def test_autoscale_equals_oracle_rule_random():
+    import numpy as np
+    from oracle import placement as OP
+    rng = np.random.default_rng(0)
+    for _ in range(200):
+        n = int(rng.integers(1, 43))
+        rates = {m: float(rng.choice([0.0, rng.uniform(1, 5000)])) for m in range(n)}
+        svc = {m: float(rng.uniform(2e-5, 5e-4)) for m in range(n)}
+        u = float(rng.choice([0.3, 0.5, 0.8]))
+        got, want = MG.autoscale(rates, svc, u, 8), OP.autoscale(rates, svc, u, 8)
+        assert got[0] == want[0] and got[1] == want[1]
+        assert np.allclose(got[2], want[2])
+
+
+def test_request_rates_window():
+    arr = {0: [0.1, 0.5, 0.9, 1.2], 1: [1.05]}
+    assert MG.request_rates(arr, 1.0, 1.0) == {0: 3.0, 1: 0.0}
+    assert MG.request_rates(arr, 1.5, 0.5) == {0: 2.0, 1: 2.0}
