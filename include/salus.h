@@ -400,6 +400,24 @@ typedef struct {
 
 int salus_read_trace(salus_ctx *ctx, salus_trace_rec *buf, uint64_t cap_recs, uint64_t *n_recs);
 
+/* Page hand-offs of the last run (SALUS_FLAG_CHECK; "pages
+ * of a closed / shrunk lane or a finished job are re-handed out only after
+ * the previous owner's last iteration completed").  One record per page the
+ * free-page pool handed to lane slot `to` (logical lane `to_lane`) while it
+ * was still fenced on another slot's record: the page's last user was slot
+ * `from`, record `from_seq` (physical record seq); every record lane
+ * `to_lane` runs from physical seq `to_seq` on may use the page.  With the run's wall stamps
+ * (salus_read_wall; physical seq = logical seq without SALUS_FLAG_EVICT) a
+ * test checks that each such record starts after `from_seq` ended.  Up to
+ * 1 << 20 records; *n_recs = records written. */
+typedef struct {
+  uint32_t page, to, from;    /* page; target and source lane slots               */
+  uint32_t to_lane;           /* logical lane id of the target (wall records' lane) */
+  uint64_t from_seq, to_seq;
+} salus_handoff_rec;
+
+int salus_read_handoffs(salus_ctx *ctx, salus_handoff_rec *buf, uint64_t cap_recs, uint64_t *n_recs);
+
 const char *salus_last_error(const salus_ctx *ctx);
 
 /* Release the host context (NULL-safe).  Never frees caller buffers.

@@ -91,7 +91,8 @@ struct salus_ctx {
   uint64_t ring_cap = 0, log_cap = 0;
   uint64_t off_ctrl = 0, off_jobs = 0, off_req = 0, off_inf = 0, off_ppt = 0, off_lpt = 0, off_free = 0,
            off_slots = 0, off_ring = 0, off_fslot = 0, off_fseq = 0, off_pend = 0, off_log = 0, off_wall = 0, off_stats = 0, off_dump = 0, off_trace = 0,
-           off_swfence = 0, off_evl = 0, off_reqseen = 0, off_lreqcnt = 0, total = 0;
+           off_swfence = 0, off_evl = 0, off_reqseen = 0, off_lreqcnt = 0, off_handoff = 0, total = 0;
+  uint64_t handoff_cap = 0, n_handoff = 0;
   // caller-owned pinned host swap area: SALUS_FLAG_EVICT (A35) and migration
   // (SALUS_DUMP_STATE / resume_state, NEXT-4); job j's region at pt_off pages
   uint8_t *swap_dev = nullptr, *swap_host = nullptr;
@@ -514,6 +515,8 @@ static void compute_layout(salus_ctx *c) {
   c->off_evl = take(2 * std::max<uint64_t>(n_cap, 1));
   c->off_reqseen = take(8 * std::max<uint64_t>(req_total, 1));   // live requests: globaltimer when seen
   c->off_lreqcnt = take(4 * std::max<uint64_t>(n_cap, 1));        // live requests received per job
+  c->handoff_cap = (c->cfg.flags & SALUS_FLAG_CHECK) ? (1ull << 20) : 0;
+  c->off_handoff = take(sizeof(salus_handoff_rec) * std::max<uint64_t>(c->handoff_cap, 1));
   c->total = o;
 }
 
@@ -655,6 +658,8 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   P.log_cap = ctx->log_cap;
   P.stats = reinterpret_cast<salus_job_stat *>(m + ctx->off_stats);
   P.trace = reinterpret_cast<salus_trace_rec *>(m + ctx->off_trace);
+  P.handoff = reinterpret_cast<salus_handoff_rec *>(m + ctx->off_handoff);
+  P.handoff_cap = ctx->handoff_cap;
   P.trace_cap = ctx->trace_cap;
   P.dump = reinterpret_cast<float *>(m + ctx->off_dump);
   P.host_abort = ctx->host_abort_dev;
@@ -936,6 +941,7 @@ int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64
   rs.sched_wait_ns = ctrl.sched_wait_ns; rs.sched_fence_ns = ctrl.sched_fence_ns; rs.sched_ring_ns = ctrl.sched_ring_ns; rs.status = ctrl.status; rs.n_workers = ctx->grid / 2 - 1;
   rs.n_swap_out = ctrl.n_swap_out; rs.n_swap_in = ctrl.n_swap_in; rs.swap_bytes = ctrl.swap_bytes; rs.swap_ns = ctrl.swap_ns;
   ctx->n_trace = std::min<uint64_t>(ctrl.n_trace, ctx->trace_cap);
+  ctx->n_handoff = std::min<uint64_t>(ctrl.n_handoff, ctx->handoff_cap);
   rs.h2d_bytes = ctx->h2d_bytes + ctx->run_h2d;
   rs.d2h_bytes = sizeof(Ctrl) + (stats ? sizeof(salus_job_stat) * ctx->jobs.size() : 0);
   ctx->ran = true;
@@ -1035,6 +1041,17 @@ int salus_read_trace(salus_ctx *ctx, salus_trace_rec *buf, uint64_t cap_recs, ui
   cudaError_t e = cudaMemcpy(buf, ctx->meta + ctx->off_trace, ctx->n_trace * sizeof(salus_trace_rec),
                              cudaMemcpyDeviceToHost);
   return e ? cuda_fail(ctx, e, "read trace") : SALUS_OK;
+}
+
+int salus_read_handoffs(salus_ctx *ctx, salus_handoff_rec *buf, uint64_t cap_recs, uint64_t *n_recs) {
+  if (!ctx || !n_recs) return SALUS_E_INVAL;
+  if (!ctx->ran || !(ctx->cfg.flags & SALUS_FLAG_CHECK)) return fail(ctx, SALUS_E_STATE, "no hand-off record (SALUS_FLAG_CHECK)");
+  *n_recs = ctx->n_handoff;
+  if (!buf) return SALUS_OK;
+  if (cap_recs < ctx->n_handoff) return fail(ctx, SALUS_E_CAPACITY, "buffer too small");
+  cudaError_t e = cudaMemcpy(buf, ctx->meta + ctx->off_handoff, ctx->n_handoff * sizeof(salus_handoff_rec),
+                             cudaMemcpyDeviceToHost);
+  return e ? cuda_fail(ctx, e, "read hand-offs") : SALUS_OK;
 }
 
 int salus_read_wall(salus_ctx *ctx, salus_wall_rec *buf, uint64_t cap_recs, uint64_t *n_recs) {

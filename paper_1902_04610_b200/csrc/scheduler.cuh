@@ -157,7 +157,7 @@ struct Sched {
   // seq+1 of that owner's final iteration); popping it for a different
   // target slot records the fence, and the target's next record is appended
   // only after the fence iteration has physically completed.
-  __device__ void pop_pages(uint32_t *dst, uint32_t k, uint32_t target) {
+  __device__ void pop_pages(uint32_t *dst, uint32_t k, uint32_t target, uint32_t lane_id) {
     if (k > free_top) { fail(SALUS_E_CAPACITY, 1); return; }
     bool any = false;
     for (uint32_t i = tid; i < k; i += 32) {
@@ -169,6 +169,14 @@ struct Sched {
         if (fs && src != target) {
           atomicMax(&P.pend_fence[target * MAX_LANES + src], (unsigned long long)fs);
           any = true;
+          if (P.handoff_cap) {                  // I4 evidence: records of `target` from pseq on use it
+            const unsigned long long n = atomicAdd(&P.ctrl->n_handoff, 1ull);
+            if (n < P.handoff_cap) {
+              salus_handoff_rec h;
+              h.page = pg; h.to = target; h.from = src; h.to_lane = lane_id; h.from_seq = fs - 1; h.to_seq = pseq;
+              P.handoff[n] = h;
+            }
+          }
         }
         P.fence_seq[pg] = 0;
       }
@@ -643,7 +651,7 @@ struct Sched {
       // before the last shrink / close, run-ahead) must have completed.
       // Records of current residents only use entries below the backing.
       if (physical && S.tail_seq[slot]) wait_slot(slot, S.tail_seq[slot]);
-      pop_pages(lane_table(slot) + S.lane_back[li], S.ae[j] - S.lane_back[li], slot);
+      pop_pages(lane_table(slot) + S.lane_back[li], S.ae[j] - S.lane_back[li], slot, S.lane_id[li]);
       if (tid == 0) S.lane_back[li] = S.ae[j];
     }
     if (restored && physical && S.ap[j] > 0) {
@@ -652,7 +660,7 @@ struct Sched {
       const uint64_t f = P.swap_fence[j];
       wait_slot((uint32_t)(f >> 56), f & ((1ull << 56) - 1));
     }
-    pop_pages(job_table(j), S.ap[j], slot);
+    pop_pages(job_table(j), S.ap[j], slot, S.lane_id[li]);
     if (P.policy == SALUS_FAIR) {                        // A12: virtual-time start
       const int64_t m = min_svc_in(slot, NONE32, false);
       if (tid == 0) S.svc[j] = (m == IDLE_T) ? 0 : m;

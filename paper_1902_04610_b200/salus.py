@@ -78,6 +78,8 @@ WALL_DTYPE = np.dtype([("seq", "<u8"), ("lane", "<u4"), ("job", "<u4"), ("start_
                        ("end_ns", "<u8"), ("append_ns", "<u8")])
 TRACE_DTYPE = np.dtype([("task", "<u4"), ("smid", "<u4"), ("job", "<u4"), ("iter", "<u4"),
                         ("t_claim", "<u8"), ("t_ready", "<u8"), ("t_mma", "<u8"), ("t_end", "<u8")])
+HANDOFF_DTYPE = np.dtype([("page", "<u4"), ("to", "<u4"), ("from", "<u4"), ("to_lane", "<u4"),
+                          ("from_seq", "<u8"), ("to_seq", "<u8")])
 LOG_DTYPE = np.dtype([("tick", "<i8"), ("kind", "<u4"), ("lane", "<u4"), ("job", "<u4"),
                       ("a", "<u4"), ("b", "<u8")])
 
@@ -86,7 +88,7 @@ EXPORTS = ["salus_open", "salus_job_footprint", "salus_submit_job", "salus_meta_
            "salus_read_wall", "salus_read_trace", "salus_read_layers", "salus_last_error", "salus_close",
            "salus_run_async", "salus_submit_live", "salus_end_submissions", "salus_wait",
            "salus_swap_bytes", "salus_set_swap", "salus_poll_stats", "salus_read_state",
-           "salus_submit_requests", "salus_read_requests"]
+           "salus_submit_requests", "salus_read_requests", "salus_read_handoffs"]
 
 _lib = None
 _POISONED: List[tuple] = []   # buffers of poisoned contexts, kept alive for the process
@@ -119,6 +121,7 @@ def lib():
         L.salus_run_async.argtypes = [P]
         L.salus_submit_live.argtypes = [P, C.POINTER(JobDesc)]
         L.salus_end_submissions.argtypes = [P]
+        L.salus_read_handoffs.argtypes = [P, P, C.c_uint64, C.POINTER(C.c_uint64)]
         L.salus_submit_requests.argtypes = [P, C.POINTER(C.c_uint32), C.c_uint32]
         L.salus_read_requests.argtypes = [P, C.c_uint32, C.POINTER(C.c_int64), C.POINTER(C.c_uint64),
                                           C.c_uint64, C.POINTER(C.c_uint64)]
@@ -284,6 +287,15 @@ class Context:
         ids = np.ascontiguousarray(job_ids, dtype=np.uint32)
         self._check(self.L.salus_submit_requests(self.ctx, ids.ctypes.data_as(C.POINTER(C.c_uint32)), len(ids)),
                     "submit_requests")
+
+    def handoffs(self) -> np.ndarray:
+        """SALUS_FLAG_CHECK: fenced page hand-offs of the last run (I4)."""
+        n = C.c_uint64()
+        self._check(self.L.salus_read_handoffs(self.ctx, None, 0, C.byref(n)), "handoffs size")
+        out = np.zeros(n.value, dtype=HANDOFF_DTYPE)
+        self._check(self.L.salus_read_handoffs(self.ctx, C.c_void_p(out.ctypes.data), n.value, C.byref(n)),
+                    "handoffs")
+        return out
 
     def serve(self, due):
         """Submit live requests at their wall-clock times: `due` = sorted

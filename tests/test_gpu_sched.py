@@ -94,3 +94,33 @@ def test_fair_a28_hand_trace():
                                                  null_work=not real, check=True)
         ctx.close()
         assert [[t, job, it] for seq, t, lane, job, it, end in ref.dispatch] == want
+
+
+@pytest.mark.parametrize("policy", [OS.PACK, OS.SRTF])
+def test_i4_page_reuse_waits_for_the_previous_owner(policy):
+    """SURVEY §8(c) I4 from the GPU's own stamps: every page the pool hands to
+    a lane while the page's previous user (another lane slot) still had a
+    record queued is used only by records that start after that record
+    ended.  C4 with real work (run-ahead: the scheduler is far ahead of the
+    workers, so hand-offs with pending fences occur), SALUS_FLAG_CHECK."""
+    import numpy as np
+    jobs, cap = c4_trace()
+    ctx, ref, stats = assert_schedule_parity(jobs, cap, policy, null_work=False, check=True, timeout_ms=300000)
+    try:
+        h = ctx.handoffs()
+        w = ctx.wall()
+    finally:
+        ctx.close()
+    assert len(h) > 0                                   # the trace does exercise fenced reuse
+    end = {int(s): int(e) for s, e in zip(w["seq"], w["end_ns"])}
+    order = np.argsort(w["seq"])
+    seqs, lanes, starts = w["seq"][order].astype(np.int64), w["lane"][order], w["start_ns"][order].astype(np.int64)
+    pairs = {(int(a), int(b), int(c)) for a, b, c in zip(h["to_lane"], h["from_seq"], h["to_seq"])}
+    checked = 0
+    for to_lane, from_seq, to_seq in pairs:
+        later = (lanes == to_lane) & (seqs >= to_seq)
+        if later.any():
+            first = starts[later].min()
+            assert first >= end[from_seq], (to_lane, from_seq, to_seq, first - end[from_seq])
+            checked += 1
+    assert checked > 0
