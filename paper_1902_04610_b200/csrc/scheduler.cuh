@@ -407,6 +407,7 @@ struct Sched {
   }
 
   __device__ void remove_lane(uint32_t i) {     // keep id order
+    __syncwarp();                                // every lane's reads of the table are done
     for (uint32_t k = i; k + 1 < nl; k++) {
       if (tid == 0) {
         S.lane_id[k] = S.lane_id[k + 1]; S.lane_L[k] = S.lane_L[k + 1]; S.lane_slot[k] = S.lane_slot[k + 1];
@@ -454,6 +455,7 @@ struct Sched {
     {
       const uint32_t slot = S.lane_slot[i];
       const uint32_t j = S.lane_cur[i];
+      __syncwarp();                              // the lanes' earlier reads of lane_busy are done
       if (tid == 0) { S.done[j] += 1; S.svc[j] += S.c[j]; S.lane_busy[i] = IDLE_T; }
       __syncwarp();
       if (S.done[j] == S.n[j]) {
@@ -507,6 +509,7 @@ struct Sched {
     if (maxe < S.lane_L[i]) {                 // A4: L_j = max E_i of residents
       emit(SALUS_REC_LANE_SHRINK, S.lane_id[i], S.id[j], maxe, S.lane_L[i]);
       sumL -= S.lane_L[i] - maxe;
+      __syncwarp();
       if (tid == 0) S.lane_L[i] = maxe;
     }
     if (maxae < S.lane_back[i]) {
@@ -875,6 +878,7 @@ struct Sched {
     }
     uint32_t won = 0;
     DispRec rec;                                           // (thread 0) the record as appended
+    __syncwarp();                                          // every lane has read sq_tail
     if (tid == 0) {
       volatile DispRec *vr = &sl.recs[tl % RQ];
       const bool eager = kind == REC_ITER && nl <= P.eager_lanes && (nl == 1 || nl <= (uint32_t)(S.xpre[j] >> 1));

@@ -848,8 +848,8 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint
         td.kind = T_EXIT;
         td.payload = TASK_EXIT;
         ptx::mbar_arrive(&W.desc_full[d]);
-        ptx::mbar_arrive(&W.desc_ptrs[d]);
       }
+      if (lane < NPTR) ptx::mbar_arrive(&W.desc_ptrs[d]);
       break;
     }
     SlotHead head;
@@ -874,10 +874,11 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint
       ptx::fence_proxy_async_global();
       ptx::mbar_arrive(&W.desc_full[d]);
     }
+    // every pointer-writing lane releases its own write (desc_ptrs counts
+    // NPTR arrivals) rather than lane 0 on the others' behalf
     if (lane < NPTR && ((td.xt_mask >> lane) & 1u))
       td.ptr[lane] = xlate(P, td.xt_tab[(td.xt_sel >> lane) & 1u], td.xt_off[lane]);
-    __syncwarp();
-    if (lane == 0) ptx::mbar_arrive(&W.desc_ptrs[d]);
+    if (lane < NPTR) ptx::mbar_arrive(&W.desc_ptrs[d]);
     __syncwarp();
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
   }
@@ -1355,7 +1356,7 @@ __device__ void run_worker(const Params &P, uint8_t *smem_raw) {
     // completion warp (after the epilogue is done)
     for (uint32_t d = 0; d < NDESC; d++) {
       ptx::mbar_init(&W.desc_full[d], 1);
-      ptx::mbar_init(&W.desc_ptrs[d], 1);
+      ptx::mbar_init(&W.desc_ptrs[d], NPTR);
       ptx::mbar_init(&W.desc_empty[d], 4);
       ptx::mbar_init(&W.epi_done[d], 1);
       ptx::mbar_init(&W.mail_full[d], 1);
