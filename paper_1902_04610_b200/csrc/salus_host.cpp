@@ -309,6 +309,35 @@ int salus_submit_job(salus_ctx *ctx, const salus_job *job) {
   return SALUS_OK;
 }
 
+// Mapped pinned 64-byte flags (the per-context abort flag), carved from
+// process-wide 64 KiB pages: cudaHostAlloc of a fresh pinned buffer can take
+// tens of ms, which a context per run (bench.py's e2e) would pay every time.
+namespace {
+std::mutex g_flag_mu;
+std::vector<std::pair<uint32_t *, uint32_t *>> g_flag_free;   // (host, device)
+}
+static cudaError_t flag_alloc(uint32_t **host, uint32_t **dev) {
+  std::lock_guard<std::mutex> g(g_flag_mu);
+  if (g_flag_free.empty()) {
+    uint8_t *base = nullptr, *dbase = nullptr;
+    cudaError_t e = cudaHostAlloc(reinterpret_cast<void **>(&base), 65536, cudaHostAllocMapped | cudaHostAllocPortable);
+    if (e != cudaSuccess) return e;
+    if ((e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&dbase), base, 0)) != cudaSuccess) return e;
+    for (uint32_t o = 65536 - 64;; o -= 64) {
+      g_flag_free.emplace_back(reinterpret_cast<uint32_t *>(base + o), reinterpret_cast<uint32_t *>(dbase + o));
+      if (o == 0) break;
+    }
+  }
+  *host = g_flag_free.back().first;
+  *dev = g_flag_free.back().second;
+  g_flag_free.pop_back();
+  return cudaSuccess;
+}
+static void flag_free(uint32_t *host, uint32_t *dev) {
+  std::lock_guard<std::mutex> g(g_flag_mu);
+  g_flag_free.emplace_back(host, dev);
+}
+
 static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req_total, uint64_t &ppt_total,
                         uint64_t &dump_cur) {
     const salus_job &j = h.j;
@@ -609,11 +638,8 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
     return cuda_fail(ctx, e, "upload infer list");
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(ctx, e, "sync");
   ctx->h2d_bytes = sizeof(DevJob) * n + 8 * req.size() + 2 * inf.size();
-  if ((e = cudaHostAlloc(reinterpret_cast<void **>(&ctx->host_abort), 4, cudaHostAllocMapped)))
-    return cuda_fail(ctx, e, "cudaHostAlloc");
+  if ((e = flag_alloc(&ctx->host_abort, &ctx->host_abort_dev))) return cuda_fail(ctx, e, "abort flag");
   *reinterpret_cast<volatile uint32_t *>(ctx->host_abort) = 0;
-  if ((e = cudaHostGetDevicePointer(reinterpret_cast<void **>(&ctx->host_abort_dev), ctx->host_abort, 0)))
-    return cuda_fail(ctx, e, "cudaHostGetDevicePointer");
   if ((e = cudaEventCreate(&ctx->ev0)) || (e = cudaEventCreate(&ctx->ev1))) return cuda_fail(ctx, e, "events");
 
   Params &P = ctx->P;
@@ -1105,7 +1131,7 @@ int salus_close(salus_ctx *ctx) {
     if (ctx->live && !ctx->ended) salus_end_submissions(ctx);
     salus_wait(ctx, nullptr, 0, nullptr);
   }
-  if (ctx->host_abort) cudaFreeHost(ctx->host_abort);
+  if (ctx->host_abort) flag_free(ctx->host_abort, ctx->host_abort_dev);
   if (ctx->live) cudaFreeHost(ctx->live);
   if (ctx->lreq) cudaFreeHost(ctx->lreq);
   if (ctx->side) cudaStreamDestroy(ctx->side);
