@@ -22,7 +22,8 @@
 //              complete on the leader's stage barrier (.cta_group::2).
 //   warp 3     epilogue-input loader (1 thread): streams the tile's epilogue
 //              input (fp32 master weights of a dW tile, ReLU mask of a dX
-//              tile) in 32 KiB chunks through three smem buffers.
+//              tile) in 32 KiB chunks through two 48 KiB smem buffers (the
+//              last 16 KiB stage an SGD chunk's bf16 copy for its bulk store).
 //   warps 4-11 epilogue: drain TMEM (tcgen05.ld), fused epilogue, stores.
 //   warp 12    completion: gpu-scope fence, stage accounting, publication of
 //              the next stage / start of the slot's next iteration (run-ahead)
@@ -51,12 +52,26 @@ constexpr uint32_t STAGE_A_BYTES = 16384;             // 128 x 64 bf16 (this CTA
 constexpr uint32_t STAGE_B_BYTES = 16384;             // <= 128 x 64 bf16 (this CTA's half of N)
 constexpr uint32_t STAGE_BYTES = STAGE_A_BYTES + STAGE_B_BYTES;
 constexpr uint32_t ECH_BYTES = 32768;                 // epilogue-input chunk
+// SGD epilogue: the bf16 weight copy of a chunk (one 16 KiB panel block) is
+// staged in smem behind the chunk's fp32 master and both leave as bulk
+// stores -- 2 buffers of 48 KiB instead of 3 of 32 KiB (same smem)
+#ifndef SALUS_WB_BULK
+#define SALUS_WB_BULK 1
+#endif
+#if SALUS_WB_BULK
+constexpr uint32_t ECH_STRIDE = ECH_BYTES + 16384;
+#ifndef SALUS_EBUF
+#define SALUS_EBUF 2
+#endif
+#else
+constexpr uint32_t ECH_STRIDE = ECH_BYTES;
 #ifndef SALUS_EBUF
 #define SALUS_EBUF 3
 #endif
-// epilogue-input chunk buffers: 3 of the 4 chunks of a 128 x 256 fp32 master
+#endif
+// epilogue-input chunk buffers: the first chunks of a 128 x 256 fp32 master
 // tile are read from HBM while the tile's MMA runs, not during its epilogue
-// (smem: 4 operand stages x 32 KiB + 3 x 32 KiB + descriptors = 227 KiB)
+// (smem: 4 operand stages x 32 KiB + 2 x 48 KiB + descriptors = 227 KiB)
 constexpr uint32_t EBUF = SALUS_EBUF;
 #ifndef SALUS_NDESC
 #define SALUS_NDESC 4
@@ -135,7 +150,7 @@ struct TileDesc {
 
 struct WorkerSmem {
   uint8_t stage[PIPE][STAGE_BYTES];   // 1024-aligned (first member)
-  uint8_t epi_in[EBUF][ECH_BYTES];    // 1024-aligned
+  uint8_t epi_in[EBUF][ECH_STRIDE];   // 1024-aligned
   TileDesc desc[NDESC];
   uint64_t full[PIPE], empty[PIPE];
   uint64_t desc_full[NDESC], desc_empty[NDESC];
@@ -569,7 +584,15 @@ __device__ void epilogue_cols(const Params &P, const TileDesc &tds, const EpiVie
           u[q].z = pack_bf16x2(v[8 * q + 4], v[8 * q + 5]);
           u[q].w = pack_bf16x2(v[8 * q + 6], v[8 * q + 7]);
         }
-#if SALUS_L2HINT
+#if SALUS_WB_BULK
+        // into the chunk's staging panel (the global panel's exact image)
+        {
+          uint8_t *stg = buf + ECH_BYTES;
+#pragma unroll
+          for (int q = 0; q < 4; q++) *reinterpret_cast<uint4 *>(stg + swz(r, ch0 + q)) = u[q];
+          (void)pan;
+        }
+#elif SALUS_L2HINT
         store_bf16_rows<true>(tds.ptr[PTR_AUX + pan], u, r, ch0, pol_stream);
 #else
         store_bf16_rows(tds.ptr[PTR_AUX + pan], u, r, ch0);
@@ -1185,6 +1208,10 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
             named_bar(2, EPI_THREADS);
             if (et == 0) {
               ptx::bulk_s2g_hint(td.ptr[PTR_W32 + (c >> 1)] + (c & 1) * 32768u, W.epi_in[e], ECH_BYTES, pol_w32);
+#if SALUS_WB_BULK
+              // chunk c = columns [64c, 64c + 64) = the bf16 copy's panel c (this M block's 16 KiB)
+              ptx::bulk_s2g_hint(td.ptr[PTR_AUX + c], W.epi_in[e] + ECH_BYTES, 16384u, pol_w32);
+#endif
               ptx::bulk_commit();
               ptx::bulk_wait_read0();
             }
