@@ -300,9 +300,11 @@ struct Sched {
     if (live_done || arr_ptr < n_jobs) return;
     uint32_t np = 0, cl = 0;
     if (tid == 0) {
-      cl = ptx::ld_volatile_u32(P.live + 1);   // closed first: everything published before it is seen
-      __threadfence_system();
-      np = ptx::ld_volatile_u32(P.live);
+      // one 8-byte read of {n_published, closed}: a snapshot in one PCIe round
+      // trip (the host closes only after its last publication)
+      const unsigned long long v = *reinterpret_cast<const volatile unsigned long long *>(P.live);
+      np = (uint32_t)v;
+      cl = (uint32_t)(v >> 32);
     }
     cl = __shfl_sync(0xffffffffu, cl, 0);
     np = __shfl_sync(0xffffffffu, np, 0);
@@ -358,17 +360,20 @@ struct Sched {
   // Nothing scheduled and the host may still submit jobs or requests: wait.
   __device__ bool wait_live() {
     const uint64_t t0 = ptx::globaltimer();
-    while (!err) {
-      if (!live_done) {
-        poll_live();
-        if (arr_ptr < n_jobs || live_done) break;
-      }
+    // every mapped-memory read is a PCIe round trip (~1 us): requests are
+    // polled every spin, live jobs and the abort flags every 16th
+    for (uint32_t spin = 0; !err; spin++) {
       if (poll_requests()) break;
       if (live_done && lreq_seen >= P.n_lreq) break;   // nothing more can come
-      uint32_t bad = 0;
-      if (tid == 0) bad = host_abort() || *(volatile uint32_t *)&P.ctrl->abort;
-      if (__shfl_sync(0xffffffffu, bad, 0)) { fail(SALUS_E_TIMEOUT, 8); return false; }
-      __nanosleep(200);
+      if ((spin & 15) == 0) {
+        if (!live_done) {
+          poll_live();
+          if (arr_ptr < n_jobs || live_done) break;
+        }
+        uint32_t bad = 0;
+        if (tid == 0) bad = host_abort() || *(volatile uint32_t *)&P.ctrl->abort;
+        if (__shfl_sync(0xffffffffu, bad, 0)) { fail(SALUS_E_TIMEOUT, 8); return false; }
+      }
     }
     wait_ns += ptx::globaltimer() - t0;
     return !err;
@@ -888,6 +893,18 @@ struct Sched {
       rec.append_ns = ptx::globaltimer();
       vr->job = rec.job; vr->iter = rec.iter; vr->seq = rec.seq; vr->lseq = rec.lseq;
       vr->lane_id = rec.lane_id; vr->kind = rec.kind; vr->append_ns = rec.append_ns;
+    }
+    // what starting the record would publish, read before the handoff atomic
+    // so the descriptor loads overlap its round trip (used only if the slot
+    // turns out idle)
+    uint32_t first = 0, second = NONE32, n1 = 0, n2 = 0;
+    if (tid == 0) {
+      const DevJob &JJ = P.jobs[rec.job];
+      const bool narrow = (rec.kind & REC_FLAG_NARROW) != 0;
+      first = first_stage_of(rec, P.jobs);
+      second = eager_second(JJ, rec.kind, first);
+      n1 = stage_ntiles(JJ, first, narrow);
+      n2 = second != NONE32 ? stage_ntiles(JJ, second, narrow) : 0;
       // publish (release) and learn whether the slot was idle in one atomic;
       // only the scheduler ever sets `running`, so taking it needs no CAS
       won = (atom_add_release_u64(&sl.qstate, QS_TAIL_ONE) & 1ull) == 0;
@@ -898,7 +915,6 @@ struct Sched {
     __syncwarp();
     won = __shfl_sync(0xffffffffu, won, 0);
     if (!won) return;
-    uint32_t first = 0, second = NONE32, n1 = 0, n2 = 0;
     unsigned long long base = 0;
     if (tid == 0) {
       // running was clear, so the ring was empty (a holder consumes every
@@ -906,12 +922,6 @@ struct Sched {
       // the only one -- take it from registers (set running, head + 1)
       // instead of take_next's round trips through the ring
       atomicAdd(&sl.qstate, 1ull + QS_HEAD_ONE);
-      const DevJob &JJ = P.jobs[rec.job];
-      const bool narrow = (rec.kind & REC_FLAG_NARROW) != 0;
-      first = first_stage_of(rec, P.jobs);
-      second = eager_second(JJ, rec.kind, first);
-      n1 = stage_ntiles(JJ, first, narrow);
-      n2 = second != NONE32 ? stage_ntiles(JJ, second, narrow) : 0;
       base = atomicAdd(&P.ctrl->q_head, (unsigned long long)(n1 + n2));   // overlaps the fence below
       begin_iteration(sl, rec);
     }
@@ -1007,14 +1017,18 @@ struct Sched {
 #else
 #define SALUS_PH(i, stmt) stmt;
 #endif
+    bool woke = false;                       // wait_live just polled the host
     while (!err) {
-      if (!live_done && (n_ticks & 15) == 0) poll_live();
-      if ((n_ticks & 7) == 0) poll_requests();
+      if (!woke) {
+        if (!live_done && (n_ticks & 15) == 0) poll_live();
+        if ((n_ticks & 7) == 0) poll_requests();
+      }
+      woke = false;
       if (n_done == n_jobs && live_done) break;
       int64_t tn;
       SALUS_PH(0, tn = next_event())
       if (tn == IDLE_T) {
-        if (!live_done || lreq_seen < P.n_lreq) { if (!wait_live()) break; continue; }
+        if (!live_done || lreq_seen < P.n_lreq) { if (!wait_live()) break; woke = true; continue; }
         fail(SALUS_E_STUCK, 4);
         break;
       }
