@@ -291,13 +291,16 @@ def c3_live(S, device, rates=((20, 1.0), (100, 0.5), (1000, 0.2)), seed=3):
         finally:
             ctx.close()
         w = w[np.argsort(w["seq"])]
-        kreq, q, lat, sw, last = {}, [], [], [], {}
+        kreq, q, lat, sw, last, s2a, a2s = {}, [], [], [], {}, [], []
         for r in w:
             jid = int(r["job"])
             kk = kreq.get(jid, 0)
             kreq[jid] = kk + 1
             s0 = int(seen[jid][kk])
             q.append((int(r["start_ns"]) - s0) / 1e3)
+            if int(r["append_ns"]) >= s0:              # queueing split: scheduler / publication + decode
+                s2a.append((int(r["append_ns"]) - s0) / 1e3)
+                a2s.append((int(r["start_ns"]) - int(r["append_ns"])) / 1e3)
             lat.append((int(r["end_ns"]) - s0) / 1e3)
             ln = int(r["lane"])
             if ln in last and int(last[ln]["job"]) != jid:
@@ -312,6 +315,7 @@ def c3_live(S, device, rates=((20, 1.0), (100, 0.5), (1000, 0.2)), seed=3):
             "models": len(jobs), "requests": len(due), "offered_rps": len(due) / dur, "window_s": dur,
             "served": int(len(w)), "run_s": span,
             "queueing_us": pct(q), "latency_us": pct(lat), "switch_gap_us": pct(sw),
+            "seen_to_append_us": pct(s2a), "append_to_first_tile_us": pct(a2s),
             "host_submit_lag_us": pct([x * 1e6 for x in lag])}
     return {"config": "C3 live: 42 inference models (14 archs x 3), FAIR over 8 lanes, 16 GiB; "
                       "Poisson requests per model in wall time via salus_submit_requests",

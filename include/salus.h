@@ -310,7 +310,8 @@ int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64
  * iteration).  An INFER job submitted before the run with request_ticks =
  * NULL receives its n_iters requests while the kernel runs:
  * salus_submit_requests appends n job ids (host array, copied) to a mapped
- * pinned request ring and publishes them with one store; the device
+ * pinned request ring and publishes them with one 8-byte store (count and
+ * last entry, so a batch of one costs the device a single PCIe read); the device
  * scheduler polls the ring (every tick while idle, every 8 ticks while
  * busy), gives every request it finds at tick t the arrival tick t + 1 (as
  * A34 does for live jobs) and stamps the globaltimer it saw it at.  The

@@ -62,6 +62,7 @@ __device__ __forceinline__ bool take_next(Slot &sl, DispRec *rec) {
       const volatile DispRec *vr = &sl.recs[h % RQ];
       rec->job = vr->job; rec->iter = vr->iter; rec->seq = vr->seq; rec->lane_id = vr->lane_id; rec->kind = vr->kind;
       rec->append_ns = vr->append_ns; rec->lseq = vr->lseq;
+      rec->first = vr->first; rec->second = vr->second; rec->n1 = vr->n1; rec->n2 = vr->n2;
       red_add_release_u64(&sl.qstate, QS_HEAD_ONE);
       return true;
     }

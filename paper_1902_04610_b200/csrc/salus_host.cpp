@@ -787,7 +787,7 @@ int salus_run_async(salus_ctx *ctx) {
     reinterpret_cast<volatile uint32_t *>(ctx->live)[1] = 0;                           // submissions open
     ctx->ended = false;
     if (ctx->lreq) {
-      reinterpret_cast<volatile uint32_t *>(ctx->lreq)[0] = 0;
+      *reinterpret_cast<volatile uint64_t *>(ctx->lreq) = 0;
       ctx->lreq_pub = 0;
       for (uint32_t d = 0; d < (uint32_t)ctx->djobs.size(); d++) {
         const HostJob &h = ctx->jobs[ctx->dense_to_submit[d]];
@@ -839,15 +839,18 @@ int salus_submit_requests(salus_ctx *ctx, const uint32_t *job_ids, uint32_t n) {
     if (++take[it->second] > ctx->lreq_left[it->second])
       return fail(ctx, SALUS_E_CAPACITY, "job " + std::to_string(job_ids[i]) + ": more requests than n_iters");
   }
+  if (n == 0) return SALUS_OK;
   volatile uint32_t *ring = reinterpret_cast<volatile uint32_t *>(ctx->lreq);
+  uint32_t d = 0;
   for (uint32_t i = 0; i < n; i++) {
-    const uint32_t d = ctx->id_to_dense[job_ids[i]];
+    d = ctx->id_to_dense[job_ids[i]];
     ring[2 + ctx->lreq_pub + i] = d;
     ctx->lreq_left[d]--;
   }
   ctx->lreq_pub += n;
   std::atomic_thread_fence(std::memory_order_seq_cst);
-  ring[0] = ctx->lreq_pub;                                         // publish
+  // publish {count, last entry} in one 8-byte store (the device reads both at once)
+  *reinterpret_cast<volatile uint64_t *>(ctx->lreq) = ((uint64_t)d << 32) | ctx->lreq_pub;
   return SALUS_OK;
 }
 

@@ -334,19 +334,31 @@ struct Sched {
   // Returns true if any arrived.
   __device__ bool poll_requests() {
     if (!P.n_lreq || lreq_seen >= P.n_lreq) return false;
-    uint32_t np = 0;
-    if (tid == 0) np = ptx::ld_volatile_u32(P.lreq);
+    uint32_t np = 0, last = 0;
+    if (tid == 0) {
+      // {count, job of the last entry} in one 8-byte acquire read at system
+      // scope: the entries the host wrote before are read after it, and a
+      // batch of one needs no second PCIe round trip
+      unsigned long long v;
+      asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(P.lreq) : "memory");
+      np = (uint32_t)v;
+      last = (uint32_t)(v >> 32);
+    }
     np = __shfl_sync(0xffffffffu, np, 0);
     if (np == lreq_seen) return false;
     if (np > P.n_lreq) { fail(SALUS_E_CAPACITY, 9); return false; }
     if (tid == 0) {
-      __threadfence_system();                        // the entries were written before the count
       const uint64_t now = ptx::globaltimer();
       for (uint32_t k = lreq_seen; k < np; k++) {
-        const uint32_t j = ptx::ld_volatile_u32(P.lreq + 2 + k);
-        const uint32_t c = P.lreq_cnt[j]++;
-        const int64_t arr = P.jobs[j].arrival;
-        const int64_t tk = t + 1 > arr ? t + 1 : arr;
+        const uint32_t j = k + 1 == np ? last : ptx::ld_volatile_u32(P.lreq + 2 + k);
+        // requests of j seen so far: every earlier one got a tick <= t and was
+        // counted into next_req by phase_arrivals already, unless the job has
+        // not arrived or this batch holds more than one (then the global count)
+        const uint32_t c = (np == lreq_seen + 1 && S.st[j] != ST_NOT_ARRIVED) ? S.next_req[j] : P.lreq_cnt[j];
+        P.lreq_cnt[j] = c + 1;
+        // an arrived job takes t + 1; one still to arrive, its arrival tick
+        const int64_t tk = S.st[j] != ST_NOT_ARRIVED ? t + 1
+                         : (t + 1 > P.jobs[j].arrival ? t + 1 : P.jobs[j].arrival);
         P.req_ticks[S.req_off[j] + c] = tk;
         P.req_seen[S.req_off[j] + c] = now;
         if (S.next_req[j] == c && S.nrt[j] == IDLE_T) S.nrt[j] = tk;   // the job was waiting for it
@@ -891,20 +903,22 @@ struct Sched {
       rec.kind = kind | ((kind == REC_ITER && (S.xpre[j] & 1u)) ? REC_FLAG_XPRE : 0u) |
                  (eager ? REC_FLAG_EAGER : 0u) | ((eager && nl <= P.narrow_lanes) ? REC_FLAG_NARROW : 0u);
       rec.append_ns = ptx::globaltimer();
-      vr->job = rec.job; vr->iter = rec.iter; vr->seq = rec.seq; vr->lseq = rec.lseq;
-      vr->lane_id = rec.lane_id; vr->kind = rec.kind; vr->append_ns = rec.append_ns;
-    }
-    // what starting the record would publish, read before the handoff atomic
-    // so the descriptor loads overlap its round trip (used only if the slot
-    // turns out idle)
-    uint32_t first = 0, second = NONE32, n1 = 0, n2 = 0;
-    if (tid == 0) {
+      // what starting the record publishes (the record carries it, so the
+      // thread that starts it -- here or a completion warp -- reads no
+      // descriptor)
       const DevJob &JJ = P.jobs[rec.job];
       const bool narrow = (rec.kind & REC_FLAG_NARROW) != 0;
-      first = first_stage_of(rec, P.jobs);
-      second = eager_second(JJ, rec.kind, first);
-      n1 = stage_ntiles(JJ, first, narrow);
-      n2 = second != NONE32 ? stage_ntiles(JJ, second, narrow) : 0;
+      rec.first = first_stage_of(rec, P.jobs);
+      rec.second = eager_second(JJ, rec.kind, rec.first);
+      rec.n1 = stage_ntiles(JJ, rec.first, narrow);
+      rec.n2 = rec.second != NONE32 ? stage_ntiles(JJ, rec.second, narrow) : 0;
+      vr->job = rec.job; vr->iter = rec.iter; vr->seq = rec.seq; vr->lseq = rec.lseq;
+      vr->lane_id = rec.lane_id; vr->kind = rec.kind; vr->append_ns = rec.append_ns;
+      vr->first = rec.first; vr->second = rec.second; vr->n1 = rec.n1; vr->n2 = rec.n2;
+    }
+    uint32_t first = 0, second = NONE32, n1 = 0, n2 = 0;
+    if (tid == 0) {
+      first = rec.first; second = rec.second; n1 = rec.n1; n2 = rec.n2;
       // publish (release) and learn whether the slot was idle in one atomic;
       // only the scheduler ever sets `running`, so taking it needs no CAS
       won = (atom_add_release_u64(&sl.qstate, QS_TAIL_ONE) & 1ull) == 0;

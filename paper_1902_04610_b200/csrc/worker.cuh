@@ -1319,12 +1319,7 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
           // run-ahead: start the slot's next queued iteration right here
           DispRec rec;
           if (take_next(sl, &rec)) {
-            pst = first_stage_of(rec, P.jobs);
-            const DevJob &JN = P.jobs[rec.job];
-            const bool narrow = (rec.kind & REC_FLAG_NARROW) != 0;
-            pub = 1; ps = td.slot; pn = stage_ntiles(JN, pst, narrow);
-            pst2 = eager_second(JN, rec.kind, pst);
-            pn2 = pst2 != NONE32 ? stage_ntiles(JN, pst2, narrow) : 0;
+            pub = 1; ps = td.slot; pst = rec.first; pn = rec.n1; pst2 = rec.second; pn2 = rec.n2;
             // reserve the ring positions first: the atomic's round trip
             // overlaps begin_iteration's fence
             pb = atomicAdd(&P.ctrl->q_head, (unsigned long long)(pn + pn2));
