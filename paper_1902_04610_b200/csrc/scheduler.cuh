@@ -360,6 +360,7 @@ struct Sched {
         const int64_t tk = S.st[j] != ST_NOT_ARRIVED ? t + 1
                          : (t + 1 > P.jobs[j].arrival ? t + 1 : P.jobs[j].arrival);
         P.req_ticks[S.req_off[j] + c] = tk;
+        if (rq != P.req_ticks) S.req_stage[S.req_off[j] + c] = tk;   // the staged copy the tick loop reads
         P.req_seen[S.req_off[j] + c] = now;
         if (S.next_req[j] == c && S.nrt[j] == IDLE_T) S.nrt[j] = tk;   // the job was waiting for it
       }
@@ -393,7 +394,7 @@ struct Sched {
 
   __device__ void init() {
     const uint32_t N = P.n_jobs;
-    if (P.n_req <= REQ_STAGE && !P.n_lreq) {          // live requests write the global array
+    if (P.n_req <= REQ_STAGE) {                       // live requests write both copies
       for (uint32_t i = tid; i < P.n_req; i += 32) S.req_stage[i] = P.req_ticks[i];
       __syncwarp();
       rq = S.req_stage;
