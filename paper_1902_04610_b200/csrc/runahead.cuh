@@ -83,10 +83,43 @@ __device__ __forceinline__ uint32_t first_stage_of(const DispRec &rec, const Dev
   return (rec.kind & REC_FLAG_XPRE) ? 2u : 1u;
 }
 
+// Publish `n1` tiles of stage st1 of `slot` (then `n2` of st2) at ring
+// positions base..: by lane 0 alone behind one fence.acq_rel for a handful
+// of tiles (release pattern: the fence orders everything lane 0 wrote or
+// acquired before it -- begin_iteration's slot fields, a stage counter --
+// ahead of every entry), by all lanes with release stores for more (lane 0
+// fences its own writes first).  Warp-collective.
+constexpr uint32_t PUBLISH_BY_ONE = 16;
+__device__ __forceinline__ void publish_tiles(unsigned long long *ring, uint32_t ring_mask, uint32_t lane,
+                                              unsigned long long base, uint32_t slot, uint32_t st1, uint32_t n1,
+                                              uint32_t st2, uint32_t n2) {
+  const uint32_t n = n1 + n2;
+  if (n <= PUBLISH_BY_ONE) {
+    if (lane == 0) {
+      asm volatile("fence.acq_rel.gpu;" ::: "memory");
+      for (uint32_t x = 0; x < n; x++) {
+        const unsigned long long pos = base + x;
+        const uint32_t task = x < n1 ? task_pack(slot, st1, x) : task_pack(slot, st2, x - n1);
+        asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(&ring[pos & ring_mask]),
+                     "l"(((pos + 1) << 32) | task) : "memory");
+      }
+    }
+  } else {
+    if (lane == 0) __threadfence();
+    __syncwarp();
+    for (uint32_t x = lane; x < n; x += 32) {
+      const unsigned long long pos = base + x;
+      const uint32_t task = x < n1 ? task_pack(slot, st1, x) : task_pack(slot, st2, x - n1);
+      ptx::st_release_u64(&ring[pos & ring_mask], ((pos + 1) << 32) | task);
+    }
+  }
+  __syncwarp();
+}
+
 // Single thread: make `rec` the slot's in-flight record.  The caller
-// publishes the first stage's tiles after this returns (the fence orders
-// these writes first); it may reserve their ring positions before calling,
-// so that atomic's round trip overlaps this fence.
+// publishes the first stage's tiles after this returns with publish_tiles,
+// whose fence orders these writes first; it may reserve their ring
+// positions before calling, so that atomic's round trip overlaps the fence.
 __device__ __forceinline__ void begin_iteration(Slot &sl, const DispRec &rec) {
   sl.job = rec.job;
   sl.iter = rec.iter | ((rec.kind & REC_FLAG_EAGER) ? ITER_EAGER_BIT : 0u) |
@@ -102,7 +135,6 @@ __device__ __forceinline__ void begin_iteration(Slot &sl, const DispRec &rec) {
   sl.end_ticket = 0;
   for (uint32_t k = 0; k < MAX_STAGES; k++) sl.pub_ticket[k] = 0;
   if ((rec.kind & REC_KIND_MASK) != REC_ITER) { sl.stage_done[STAGE_SWAP_OUT] = 0; sl.stage_done[STAGE_SWAP_IN] = 0; }
-  __threadfence();
 }
 
 }  // namespace salus

@@ -947,12 +947,7 @@ struct Sched {
     base = __shfl_sync(0xffffffffu, base, 0);
     // eager: the second stage's tiles go behind the first's (higher ring
     // positions), so every tile's dependency sits at a lower position
-    for (uint32_t k = tid; k < n1 + n2; k += 32) {
-      const unsigned long long pos = base + k;
-      const uint32_t task = k < n1 ? task_pack(slot, first, k) : task_pack(slot, second, k - n1);
-      ptx::st_release_u64(&P.ring[pos & P.ring_mask], ((pos + 1) << 32) | task);
-    }
-    __syncwarp();
+    publish_tiles(P.ring, P.ring_mask, tid, base, slot, first, n1, second, n2);
   }
 
   // End of the schedule: wait for every slot to drain its ring.

@@ -1350,11 +1350,7 @@ __device__ void completion_warp(const Params &P, WorkerSmem &W, uint32_t lane, u
       pn2 = __shfl_sync(0xffffffffu, pn2, 0);
       pb = __shfl_sync(0xffffffffu, pb, 0);
       // the first stage's tiles, then (eager) the second's at higher positions
-      for (uint32_t x = lane; x < pn + pn2; x += 32) {
-        const unsigned long long pos = pb + x;
-        const uint32_t task = x < pn ? task_pack(ps, pst, x) : task_pack(ps, pst2, x - pn);
-        ptx::st_release_u64(&P.ring[pos & P.ring_mask], ((pos + 1) << 32) | task);
-      }
+      publish_tiles(P.ring, P.ring_mask, lane, pb, ps, pst, pn, pst2, pn2);
     }
     __syncwarp();
     if (lane == 0) release_desc(W, d, h);
