@@ -156,6 +156,11 @@ bool swap_enabled() {
   const char *e = getenv("SALUS_SWAP");
   return e && e[0] == '1';
 }
+// Split-K in narrow records (DevJob.splitk): SALUS_SPLITK=0 disables
+bool splitk_enabled() {
+  const char *e = getenv("SALUS_SPLITK");
+  return !(e && e[0] == '0');
+}
 bool relax_enabled() {
   const char *e = getenv("SALUS_RELAX");
   return !(e && e[0] == '0');
@@ -447,6 +452,57 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
         xl = x_tiles(128);
       }
       D.stage_tiles_lat[s] = (uint16_t)std::min<uint32_t>(xl + wl + extra, 0xFFFF);
+    }
+    // split-K (narrow records): a stage whose F / dX part has few pair tasks
+    // at N = 128 and a long K runs S K-slices of it (S x the tasks, each a
+    // 1/S of the weight stream): S in {4, 2} with npair x S <= SK_PAIRS
+    // (one wave of CTA pairs), K >= 2048 (below, a slice's partial write
+    // and reduction, ~4 us, cost what the shorter K saves), K-slices of >= 8
+    // chunks, whole double chunks;
+    // the workspace comes from the declared E's slack like the relaxed
+    // barrier's third G buffer
+    for (uint32_t s = 0; s < MAX_STAGES; s++) D.splitk[s] = 1;
+    D.ws_off = 0;
+    if (splitk_enabled() && !(c->cfg.flags & SALUS_FLAG_NULL_WORK)) {
+      constexpr uint32_t SK_PAIRS = 74;
+      uint8_t sk[MAX_STAGES];
+      uint32_t np[MAX_STAGES];
+      uint64_t need = 0;
+      for (uint32_t s = 0; s < MAX_STAGES; s++) { sk[s] = 1; np[s] = 0; }
+      for (uint32_t s = 2; s < D.n_stages; s++) {
+        const bool fwd = s <= L + 1;
+        if (!fwd && j.kind != SALUS_TRAIN) break;
+        const uint32_t l = fwd ? s - 1 : L - (s - (L + 2));
+        if (!fwd && l == 1) continue;                           // B_1 has no dX part
+        const uint32_t dn = fwd ? D.dpad[l] : D.dpad[l - 1];
+        const uint32_t nk = (fwd ? D.dpad[l - 1] : D.dpad[l]) / 64;
+        const uint32_t npair = pairs(D.bpad / 128) * (dn / 128);
+        for (uint32_t cand = SK_MAX; cand >= 2; cand /= 2) {
+          if (nk >= 32 && npair * cand <= SK_PAIRS && nk % (2 * cand) == 0 && nk / cand >= 8 &&
+              16 * npair <= SK_COUNTERS) {
+            sk[s] = (uint8_t)cand;
+            np[s] = npair;
+            need = std::max<uint64_t>(need, (uint64_t)npair * 2 * cand * 65536);
+            break;
+          }
+        }
+      }
+      const uint64_t end = D.relax ? (uint64_t)D.g_off3 + 2 * bp * mx : off;
+      const uint64_t ws = align_up(end, 65536);
+      if (need && (uint64_t)D.e_pages * G >= ws + need && ws + need < (1ull << 32)) {
+        D.ws_off = (uint32_t)ws;
+        D.ae_pages = std::max<uint32_t>(D.ae_pages, (uint32_t)((ws + need + G - 1) / G));
+        for (uint32_t s = 2; s < D.n_stages; s++) {
+          if (sk[s] < 2) continue;
+          const bool fwd = s <= L + 1;
+          const uint32_t l = fwd ? s - 1 : L - (s - (L + 2));
+          const uint32_t dn = fwd ? D.dpad[l] : D.dpad[l - 1];
+          const uint32_t nt0 = ntile_for(dn);
+          const uint32_t nx_old = pairs(D.bpad / 128) * (dn / (((D.lat_narrow >> s) & 1u) ? 128u : nt0));
+          D.splitk[s] = sk[s];
+          D.stage_tiles_lat[s] = (uint16_t)std::min<uint32_t>(D.stage_tiles_lat[s] - nx_old + np[s] * sk[s], 0xFFFF);
+        }
+      }
     }
     {
       uint64_t tot = 0;

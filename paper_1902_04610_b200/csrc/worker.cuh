@@ -107,6 +107,10 @@ struct OpDesc {
 #ifndef SALUS_L2HINT
 #define SALUS_L2HINT 1
 #endif
+#ifndef SALUS_KD
+#define SALUS_KD 1
+#endif
+static_assert(PIPE % 2 == 0, "double K-chunks take two operand stages");
 // SGD epilogue: the fp32 master chunk is updated in its smem buffer and
 // written back with one 32 KiB bulk (TMA) store per chunk
 #ifndef SALUS_W32_BULK
@@ -127,7 +131,14 @@ struct TileDesc {
   uint32_t dep_want, next2_ntiles;
   // K9: transposed (swap-AB) tile; ech_load: the epilogue-input chunk is
   // loaded (else only reserved as the output block's staging buffer)
-  uint8_t swap, ech_load, pad_k9[2];
+  uint8_t swap, ech_load, pad_k9;
+  // double K-chunks (tiles with an MN-major B: dW and dX): each operand
+  // block is a 128-row (16 KiB) box, one K-chunk of 128 spans two ring
+  // stages (A in the first, B in the second) -- half the copies per byte
+  uint8_t kd;
+  // split-K: K-slices of this tile (1 = none), this slice, base tile index
+  uint8_t sk, skz;
+  uint16_t sku;
   uint32_t valid;          // this CTA's half exists (odd block counts leave the peer's empty)
   uint32_t peer_valid;     // the pair's second M block exists
   uint32_t peer_nca;       // (leader) A copies per K-chunk of the peer CTA
@@ -323,7 +334,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   td.n_ech = 0;
   td.xt_mask = 0;
   td.xt_sel = 0;
-  td.swap = 0; td.ech_load = 1;
+  td.swap = 0; td.ech_load = 1; td.kd = 0; td.sk = 1; td.skz = 0; td.sku = 0;
   td.valid = 1;
   td.ptr[PTR_W32] = nullptr;
   const uint32_t *lt = P.lpt + (uint64_t)slot * P.lpt_stride;   // lane (ephemeral) space
@@ -414,13 +425,23 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     }
   } else if (stage <= L + 1) {                        // forward F_l
     const uint32_t l = stage - 1;
-    const uint32_t N = narrow && ((J.lat_narrow >> stage) & 1u) ? 128u : ntile_for(J.dpad[l]), ntn = J.dpad[l] / N;
-    const uint32_t mb = 2 * (tile / ntn) + h, nb = tile % ntn;
+    const uint32_t S = narrow ? J.splitk[stage] : 1u;
+    const uint32_t N = S > 1 || (narrow && ((J.lat_narrow >> stage) & 1u)) ? 128u : ntile_for(J.dpad[l]);
+    const uint32_t ntn = J.dpad[l] / N, z = tile % S, u = tile / S;
+    const uint32_t mb = 2 * (u / ntn) + h, nb = u % ntn;
     td.valid = mb < bp / 128;
     td.peer_valid = (mb | 1u) < bp / 128;
-    td.layer = l; td.N = N; td.nk = J.dpad[l - 1] / 64;
-    td.a = l == 1 ? OpDesc{xt, xo, bp, mb * 128, 0} : OpDesc{lt, J.act_off[l - 1], bp, mb * 128, 0};
-    td.b = OpDesc{jt, J.wb_off[l - 1][kg & 1], J.dpad[l], nb * N + h * (N / 2), 0};
+    td.layer = l; td.N = N; td.nk = J.dpad[l - 1] / 64 / S;
+    // K-slice z: chunks [z nk, (z+1) nk) of both K-major operands
+    const uint32_t kc0 = z * td.nk;
+    td.a = l == 1 ? OpDesc{xt, xo + kc0 * bp * 128u, bp, mb * 128, 0}
+                  : OpDesc{lt, J.act_off[l - 1] + kc0 * bp * 128u, bp, mb * 128, 0};
+    td.b = OpDesc{jt, J.wb_off[l - 1][kg & 1] + kc0 * J.dpad[l] * 128u, J.dpad[l], nb * N + h * (N / 2), 0};
+    if (S > 1) {
+      td.sk = (uint8_t)S; td.skz = (uint8_t)z; td.sku = (uint16_t)u;
+      if (td.valid)
+        for (uint32_t q = 0; q < S; q++) defer(td, PTR_AUX + q, lt, J.ws_off + ((2 * u + h) * S + q) * 65536u);
+    }
     td.m0 = mb * 128; td.n0 = nb * N;
     td.rows_valid = J.batch; td.cols_valid = J.dims[l]; td.ld_logical = J.dims[l];
     uint32_t out_off;
@@ -443,20 +464,22 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   } else {                                            // backward B_l
     const uint32_t tile_in = tile;
     const uint32_t l = L - (stage - (L + 2));
-    const uint32_t N = narrow && ((J.lat_narrow >> stage) & 1u) ? 128u : ntile_for(J.dpad[l - 1]);
-    const uint32_t ntn = J.dpad[l - 1] / N;
-    const uint32_t nW = ((J.dpad[l] / 128 + 1) / 2) * ntn;     // dW pair tasks
+    const uint32_t Nw = narrow && ((J.lat_narrow >> stage) & 1u) ? 128u : ntile_for(J.dpad[l - 1]);
+    const uint32_t S = narrow ? J.splitk[stage] : 1u;           // K-slices of the dX part (N = 128)
+    const uint32_t nW = ((J.dpad[l] / 128 + 1) / 2) * (J.dpad[l - 1] / Nw);     // dW pair tasks
     // G_l lives in buffer (L - l) mod 2, or mod 3 in a relaxed record
     const uint32_t g3[3] = {J.g_off[0], J.g_off[1], J.g_off3};
     const uint32_t gin = relaxed ? g3[(L - l) % 3] : J.g_off[(L - l) & 1];
     const uint32_t gout = relaxed ? g3[(L - l + 1) % 3] : J.g_off[(L - l + 1) & 1];
-    td.layer = l; td.N = N;
+    td.layer = l;
     // the long-K dX tiles take the stage's first task indices, so they are
     // claimed first (longest first within the stage)
     const uint32_t nX = td.ntiles - nW;
     if (relaxed && tile_in < nX) td.dx_ctr = dx_counter(L, stage);
     const uint32_t tile = tile_in < nX ? nW + tile_in : tile_in - nX;
     if (tile < nW) {                                  // dW_l^T = G_l^T A_{l-1}; SGD
+      const uint32_t N = Nw, ntn = J.dpad[l - 1] / N;
+      td.N = N;
       const uint32_t mb = 2 * (tile / ntn) + h, nb = tile % ntn;
       td.valid = mb < J.dpad[l] / 128;
       td.peer_valid = (mb | 1u) < J.dpad[l] / 128;
@@ -483,12 +506,21 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
         td.dump_off = (int64_t)base;
       }
     } else {                                          // G_{l-1} = (G_l W_l^T) * [A_{l-1} > 0]
-      const uint32_t u = tile - nW, mb = 2 * (u / ntn) + h, nb = u % ntn;
+      const uint32_t N = S > 1 ? 128u : Nw, ntn = J.dpad[l - 1] / N;
+      td.N = N;
+      const uint32_t ux = tile - nW, z = ux % S, u = ux / S, mb = 2 * (u / ntn) + h, nb = u % ntn;
       td.valid = mb < bp / 128;
       td.peer_valid = (mb | 1u) < bp / 128;
-      td.epi = EPI_DX; td.nk = J.dpad[l] / 64;
-      td.a = OpDesc{lt, gin, bp, mb * 128, 0};
-      td.b = OpDesc{jt, J.wb_off[l - 1][kg & 1], J.dpad[l], nb * N + h * (N / 2), 1};
+      td.epi = EPI_DX; td.nk = J.dpad[l] / 64 / S;
+      // K-slice z: A (G, K-major) chunks [z nk, +nk), B (W, MN-major) rows of the panels
+      const uint32_t kc0 = z * td.nk;
+      td.a = OpDesc{lt, gin + kc0 * bp * 128u, bp, mb * 128, 0};
+      td.b = OpDesc{jt, J.wb_off[l - 1][kg & 1] + kc0 * 8192u, J.dpad[l], nb * N + h * (N / 2), 1};
+      if (S > 1) {
+        td.sk = (uint8_t)S; td.skz = (uint8_t)z; td.sku = (uint16_t)u;
+        if (td.valid)
+          for (uint32_t q = 0; q < S; q++) defer(td, PTR_AUX + q, lt, J.ws_off + ((2 * u + h) * S + q) * 65536u);
+      }
       td.m0 = mb * 128; td.n0 = nb * N;
       td.rows_valid = J.batch; td.cols_valid = J.dims[l - 1];
       if (td.valid) {
@@ -509,6 +541,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   td.ncopy_b = td.b.mn ? nh / 64 : (nh + 127) / 128;
   td.bbytes = td.b.mn ? 8192u : (nh >= 128 ? 16384u : nh * 128u);
   td.idesc = ptx::idesc_bf16(256, td.N, td.a.mn, td.b.mn);
+  td.kd = SALUS_KD && td.b.mn && !td.swap;
 }
 
 // global byte offset (inside the operand's space) of copy q of K-chunk kc
@@ -943,6 +976,89 @@ __device__ __forceinline__ void wait_stage(const Params &P, uint32_t slot, uint3
   ptx::fence_proxy_async_global();
 }
 
+// Double K-chunk kc2 (K rows [128 kc2, +128)): byte offset of copy q.  An
+// MN-major operand's copy q is panel q's 128-row block (16 KiB, inside one
+// page: panels are multiples of 16 KiB); a K-major A's copy q is the
+// 128-row block of the 64-wide K-chunk 2 kc2 + q.
+__device__ __forceinline__ uint32_t kd_off(const OpDesc &o, uint32_t kc2, uint32_t q) {
+  return o.mn ? o.off + (o.start / 64 + q) * o.R * 128u + kc2 * 16384u
+              : o.off + (2 * kc2 + q) * o.R * 128u + o.start * 128u;
+}
+
+__device__ __forceinline__ ChunkPages kd_pages(const OpDesc &a, const OpDesc &b, uint32_t nca, uint32_t ncb,
+                                               uint32_t kc2) {
+  ChunkPages p = {0, 0, 0, 0};
+  if (nca > 0) { p.a0 = a.table[kd_off(a, kc2, 0) >> PAGE_SHIFT]; p.a1 = a.table[kd_off(a, kc2, 1) >> PAGE_SHIFT]; }
+  if (ncb > 0) p.b0 = b.table[kd_off(b, kc2, 0) >> PAGE_SHIFT];
+  if (ncb > 1) p.b1 = b.table[kd_off(b, kc2, 1) >> PAGE_SHIFT];
+  return p;
+}
+
+// Operand loads of a double-K tile: double chunk kc2 takes two ring stages,
+// A (two 16 KiB blocks) in the first and B (one 16 KiB block per 64 columns
+// of this CTA's half of N) in the second, each armed on its own leader
+// barrier.  Eager tiles issue the first PIPE/2 chunks' B (weights / earlier
+// activations) before waiting for the predecessor stage, whose output A is.
+__device__ void load_kd(const Params &P, WorkerSmem &W, const TileDesc &td, uint32_t h, uint32_t &s,
+                        uint32_t &s_phase, uint64_t pol_a, uint64_t pol_b) {
+  const OpDesc a = td.a, b = td.b;
+  const uint32_t nk2 = td.nk / 2, nca = td.valid ? 2u : 0u, ncb = td.N / 128;
+  const uint32_t tx_a = (nca + (td.peer_valid ? 2u : 0u)) * 16384u, tx_b = 2 * ncb * 16384u;
+  const void *tm = &P.tmap16;
+  const bool dep_init = td.wait && td.dep_stage == 0;
+  if (dep_init) wait_stage(P, td.slot, 0, td.dep_want);
+  const uint32_t pre = (td.wait && !dep_init) ? min(nk2, PIPE / 2) : 0;
+  if (pre) {
+    uint32_t s2 = s, ph2 = s_phase;
+    ChunkPages pg[PIPE / 2];
+    for (uint32_t kc = 0; kc < pre; kc++) {
+      pg[kc] = kd_pages(a, b, nca, ncb, kc);
+      const uint32_t sa = s2;
+      if (++s2 == PIPE) { s2 = 0; ph2 ^= 1; }
+      const uint32_t sb = s2, phb = ph2;
+      if (++s2 == PIPE) { s2 = 0; ph2 ^= 1; }
+      ptx::mbar_wait_abortable(&W.empty[sb], phb ^ 1, &P.ctrl->abort);
+      if (h == 0) ptx::mbar_arrive_expect_tx(&W.full[sb], tx_b);
+      const uint32_t bar = ptx::mapa(&W.full[sb], 0);
+      ptx::tma_load_2d_pair(W.stage[sb], tm, 0, tma_row(pg[kc].b0, kd_off(b, kc, 0)), bar, pol_b);
+      if (ncb > 1) ptx::tma_load_2d_pair(W.stage[sb] + 16384u, tm, 0, tma_row(pg[kc].b1, kd_off(b, kc, 1)), bar, pol_b);
+      (void)sa;
+    }
+    wait_stage(P, td.slot, td.dep_stage, td.dep_want);
+    for (uint32_t kc = 0; kc < pre; kc++) {
+      const uint32_t sa = s, pha = s_phase;
+      if (++s == PIPE) { s = 0; s_phase ^= 1; }
+      if (++s == PIPE) { s = 0; s_phase ^= 1; }
+      ptx::mbar_wait_abortable(&W.empty[sa], pha ^ 1, &P.ctrl->abort);
+      if (h == 0) ptx::mbar_arrive_expect_tx(&W.full[sa], tx_a);
+      if (nca) {
+        const uint32_t bar = ptx::mapa(&W.full[sa], 0);
+        ptx::tma_load_2d_pair(W.stage[sa], tm, 0, tma_row(pg[kc].a0, kd_off(a, kc, 0)), bar, pol_a);
+        ptx::tma_load_2d_pair(W.stage[sa] + 16384u, tm, 0, tma_row(pg[kc].a1, kd_off(a, kc, 1)), bar, pol_a);
+      }
+    }
+  }
+  ChunkPages p0 = pre < nk2 ? kd_pages(a, b, nca, ncb, pre) : ChunkPages{0, 0, 0, 0};
+  for (uint32_t kc = pre; kc < nk2; kc++) {
+    const ChunkPages cur = p0;
+    if (kc + 1 < nk2) p0 = kd_pages(a, b, nca, ncb, kc + 1);
+    const uint32_t sa = s, pha = s_phase;
+    if (++s == PIPE) { s = 0; s_phase ^= 1; }
+    const uint32_t sb = s, phb = s_phase;
+    if (++s == PIPE) { s = 0; s_phase ^= 1; }
+    ptx::mbar_wait_abortable(&W.empty[sa], pha ^ 1, &P.ctrl->abort);
+    ptx::mbar_wait_abortable(&W.empty[sb], phb ^ 1, &P.ctrl->abort);
+    if (h == 0) { ptx::mbar_arrive_expect_tx(&W.full[sa], tx_a); ptx::mbar_arrive_expect_tx(&W.full[sb], tx_b); }
+    const uint32_t bar_a = ptx::mapa(&W.full[sa], 0), bar_b = ptx::mapa(&W.full[sb], 0);
+    if (nca) {
+      ptx::tma_load_2d_pair(W.stage[sa], tm, 0, tma_row(cur.a0, kd_off(a, kc, 0)), bar_a, pol_a);
+      ptx::tma_load_2d_pair(W.stage[sa] + 16384u, tm, 0, tma_row(cur.a1, kd_off(a, kc, 1)), bar_a, pol_a);
+    }
+    ptx::tma_load_2d_pair(W.stage[sb], tm, 0, tma_row(cur.b0, kd_off(b, kc, 0)), bar_b, pol_b);
+    if (ncb > 1) ptx::tma_load_2d_pair(W.stage[sb] + 16384u, tm, 0, tma_row(cur.b1, kd_off(b, kc, 1)), bar_b, pol_b);
+  }
+}
+
 // Operand loader (1 thread).  The page-table reads of chunk kc + 2 are issued
 // before the copies of chunk kc, so their latency (an L2 round trip: the
 // completion warp's gpu-scope fences keep invalidating L1) is off the
@@ -968,6 +1084,12 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W, uint32_t h) {
 #else
       const uint64_t pol_a = normal, pol_b = normal;
 #endif
+      if (td.kd) {
+        load_kd(P, W, td, h, s, s_phase, pol_a, pol_b);
+        release_desc(W, d, h);
+        if (++d == NDESC) { d = 0; d_phase ^= 1; }
+        continue;
+      }
       const void *ta = ab == 16384u ? (const void *)&P.tmap16 : (const void *)&P.tmap8;
       const void *tb = bb == 16384u ? (const void *)&P.tmap16 : (const void *)&P.tmap8;
       // eager (td.wait): operand A is what the previous stage produces.  The
@@ -1109,6 +1231,36 @@ __device__ void mma_thread(const Params &P, WorkerSmem &W, uint32_t tmem) {
       ptx::mbar_wait_abortable(&W.acc_empty[b], b_phase ^ 1, &P.ctrl->abort);
       ptx::tc_fence_after();
       const uint32_t tacc = tmem + b * ACC_COLS, idesc = td.idesc, nk = td.nk;
+      if (td.kd) {
+        // double chunks: A's two 16 KiB blocks in stage sa (MN-major: the
+        // 128-row panels, LBO 16 KiB; K-major: K-chunks 2kc, 2kc+1), B's
+        // 128-row panels in stage sb
+        const bool amn = td.a.mn;
+        for (uint32_t kc = 0; kc < nk / 2; kc++) {
+          const uint32_t sa_i = s;
+          ptx::mbar_wait_abortable(&W.full[s], s_phase, &P.ctrl->abort);
+          if (++s == PIPE) { s = 0; s_phase ^= 1; }
+          const uint32_t sb_i = s;
+          ptx::mbar_wait_abortable(&W.full[s], s_phase, &P.ctrl->abort);
+          if (++s == PIPE) { s = 0; s_phase ^= 1; }
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(W.stage[sa_i]), sb = ptx::smem_u32(W.stage[sb_i]);
+#pragma unroll
+          for (uint32_t ks = 0; ks < 8; ks++) {
+            const uint64_t ad = amn ? ptx::smem_desc_sw128(sa + ks * 2048u, 16384u, 1024)
+                                    : ptx::smem_desc_sw128(sa + (ks >> 2) * 16384u + (ks & 3u) * 32u, 16u, 1024);
+            const uint64_t bd = ptx::smem_desc_sw128(sb + ks * 2048u, 16384u, 1024);
+            ptx::mma_bf16(tacc, ad, bd, idesc, (kc | ks) != 0);
+          }
+          ptx::mma_commit_pair(&W.empty[sa_i]);
+          ptx::mma_commit_pair(&W.empty[sb_i]);
+        }
+        ptx::mma_commit_pair(&W.acc_full[b]);
+        if (++b == 2) { b = 0; b_phase ^= 1; }
+        release_desc(W, d, 0, true);
+        if (++d == NDESC) { d = 0; d_phase ^= 1; }
+        continue;
+      }
       const uint32_t a_lbo = td.a.mn ? 8192u : 16u, b_lbo = td.b.mn ? 8192u : 16u;
       const uint32_t a_step = td.a.mn ? 2048u : 32u, b_step = td.b.mn ? 2048u : 32u;
       for (uint32_t kc = 0; kc < nk; kc++) {
@@ -1160,6 +1312,100 @@ __device__ void peer_mma_role(const Params &P, WorkerSmem &W) {
   }
 }
 
+// Split-K (DevJob.splitk): every K-slice of a tile writes its fp32 partial
+// (this CTA's 128 rows x N = 128 columns, 64 KiB, layout sk_off) to its
+// workspace page, then counts itself on the
+// slot's counter for (base tile, CTA half, epilogue warp).  The slice that
+// arrives last at a warp's counter sums that warp's region of the S
+// partials in slice order -- its own straight from TMEM -- and
+// stores the sum back into its accumulator, so the ordinary epilogue
+// (ReLU / loss / mask, bf16 stores) runs once per tile on the full sum,
+// independent of which slice finished last.  Returns whether this warp runs
+// that epilogue on its region.
+// Partial layout (private to the slices of one tile): column block cc of
+// TMEM lane quarter w is 4 KiB at cc x 16 KiB + w x 4 KiB, holding float4 g
+// (columns 4g..4g+3) of lane t at g x 512 B + t x 16 B -- every warp store
+// and load of a float4 column group covers 512 contiguous bytes.
+__device__ __forceinline__ uint32_t sk_off(uint32_t cc, uint32_t r) {
+  return cc * 16384u + (r >> 5) * 4096u + (r & 31u) * 16u;
+}
+
+__device__ bool splitk_reduce(const Params &P, WorkerSmem &W, const TileDesc &td, uint32_t tacc, uint32_t r,
+                              uint32_t hh, uint32_t et) {
+  const uint32_t S = td.sk, z = td.skz;
+  const uint32_t taddr = tacc + (((r >> 5) * 32u) << 16);
+  const uint32_t sub = (td.N / 32) / EPI_HALVES, cc0 = hh * sub;
+  for (uint32_t cc = cc0; cc < cc0 + sub; cc++) {
+    uint32_t raw[32];
+    ptx::tmem_ld32(taddr + cc * 32u, raw);
+    ptx::tmem_ld_wait();
+    float4 *dst = reinterpret_cast<float4 *>(td.ptr[PTR_AUX + z] + sk_off(cc, r));
+#pragma unroll
+    for (int q = 0; q < 8; q++)
+      __stcg(dst + 32 * q, make_float4(__uint_as_float(raw[4 * q]), __uint_as_float(raw[4 * q + 1]),
+                                  __uint_as_float(raw[4 * q + 2]), __uint_as_float(raw[4 * q + 3])));
+  }
+  // per warp (each owns 32 rows x its column half of the tile): one acq_rel
+  // atomic on the warp's own counter -- its release is cumulative over the
+  // warp's partial stores (ordered before it by __syncwarp), its acquire
+  // orders the other slices' partials of the same region before the reads
+  __syncwarp();
+  uint32_t last = 0;
+  if ((r & 31u) == 0) {
+    uint32_t *cnt = &P.slots[td.slot].sk_cnt[(2 * td.sku + ptx::cluster_ctarank()) * EPI_WARPS + (et >> 5)];
+    last = ptx::atom_add_acqrel_u32(cnt, 1u) + 1 == S;
+    // the next split stage of this slot starts from 0 (it runs after this
+    // stage's completion, which the completion warp releases after this tile)
+    if (last) asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(cnt), "r"(0u) : "memory");
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+#if SALUS_DBG_SK   // trace field re-purposed: partials written and counted
+  if (et == 0) const_cast<TileDesc &>(td).t_claim = ptx::globaltimer();
+#endif
+  if (!last) return false;
+  // all other slices' loads of a 16-column half in flight at once (one L2
+  // round trip per half instead of one per slice), then the sum in slice order
+  for (uint32_t c16 = 2 * cc0; c16 < 2 * (cc0 + sub); c16++) {
+    uint32_t raw[16];
+    ptx::tmem_ld16(taddr + c16 * 16u, raw);
+    float4 pv[SK_MAX - 1][4];                 // remote slice i = q < z ? q : q - 1
+#pragma unroll
+    for (uint32_t i = 0; i < SK_MAX - 1; i++) {
+      if (i + 1 < S) {
+        const uint32_t q = i < z ? i : i + 1;
+        const float4 *src = reinterpret_cast<const float4 *>(td.ptr[PTR_AUX + q] + sk_off(c16 >> 1, r)) +
+                            32 * 4 * (c16 & 1u);
+#pragma unroll
+        for (int g = 0; g < 4; g++) pv[i][g] = __ldcg(src + 32 * g);
+      }
+    }
+    ptx::tmem_ld_wait();
+#pragma unroll
+    for (int g = 0; g < 4; g++) {
+      float a[4];
+#pragma unroll
+      for (uint32_t q = 0; q < SK_MAX; q++) {
+        if (q >= S) break;
+        // static indices only (q is unrolled): remote slice q sits at q - 1 above z, else at q
+        const float4 lo = pv[q < SK_MAX - 1 ? q : SK_MAX - 2][g], hi = pv[q > 0 ? q - 1 : 0][g];
+        const float4 f = q < z ? lo : hi;
+        float v[4] = {f.x, f.y, f.z, f.w};
+        if (q == z) {
+#pragma unroll
+          for (int x = 0; x < 4; x++) v[x] = __uint_as_float(raw[4 * g + x]);
+        }
+#pragma unroll
+        for (int x = 0; x < 4; x++) a[x] = q == 0 ? v[x] : a[x] + v[x];
+      }
+#pragma unroll
+      for (int x = 0; x < 4; x++) raw[4 * g + x] = __float_as_uint(a[x]);
+    }
+    ptx::tmem_st16(taddr + c16 * 16u, raw);
+  }
+  ptx::tmem_st_wait();
+  return true;
+}
+
 __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, uint32_t tid,
                                unsigned long long &my_tasks) {
   const uint32_t warp = tid >> 5, lane = tid & 31;
@@ -1186,19 +1432,22 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
       ptx::tc_fence_after();
       t_mma = ptx::globaltimer();
       const uint32_t tacc = tmem + b * ACC_COLS;
+      // split-K: only the tile's last K-slice (holding the summed partials) runs the epilogue
+      const bool epi = !td.valid || td.sk < 2 || splitk_reduce(P, W, td, tacc, r, h, et);
       if (!td.valid) {
         // the peer half of a super-tile past the last M block: nothing to store
       } else if (td.swap) {
         epilogue_swap(P, W, td, tacc, r, h, et, lane, e, e_phase);
       } else if (n == 0) {
         const uint32_t sub = ncc / EPI_HALVES;
-        epilogue_cols(P, td, ev, tacc, r, 0, h * sub, (h + 1) * sub, nullptr);
+        if (epi) epilogue_cols(P, td, ev, tacc, r, 0, h * sub, (h + 1) * sub, nullptr);
       } else {
         const uint32_t per = ncc / n;                 // column blocks per input chunk
         const uint32_t sub = per / EPI_HALVES;
         for (uint32_t c = 0; c < n; c++) {
           ptx::mbar_wait_abortable(&W.epi_full[e], e_phase, &P.ctrl->abort);
-          epilogue_cols(P, td, ev, tacc, r, c * per, c * per + h * sub, c * per + (h + 1) * sub, W.epi_in[e]);
+          if (epi)
+            epilogue_cols(P, td, ev, tacc, r, c * per, c * per + h * sub, c * per + (h + 1) * sub, W.epi_in[e]);
 #if SALUS_W32_BULK
           if (td.epi == EPI_SGD) {
             // the updated master chunk (contiguous in HBM: half a 64 KiB page)

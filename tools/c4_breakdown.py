@@ -1,6 +1,6 @@
 """Where C4's time goes (SRTF, real work): per job, measured iteration time
 (device wall stamps) against its roofline time max(F/peak, B/BW), grouped by
-width.  usage: python tools/c4_breakdown.py"""
+width.  usage: python tools/c4_breakdown.py [c4|c5] [srtf|pack|fifo]"""
 import json
 import os
 import sys
@@ -14,12 +14,14 @@ sys.path.insert(0, ROOT)
 
 def main():
     from paper_1902_04610_b200 import build, salus as S
-    from workloads import algorithmic_bytes, algorithmic_flops, c4_trace
+    from workloads import algorithmic_bytes, algorithmic_flops, c4_trace, c5_trace
     build.build()
+    cfg = sys.argv[1] if len(sys.argv) > 1 else "c4"
+    pol = {"srtf": S.SRTF, "pack": S.PACK, "fifo": S.FIFO}[sys.argv[2] if len(sys.argv) > 2 else "srtf"]
     pk = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     bw, tf = pk["hbm_gbs"] * 1e9, pk["bf16_tflops_sustained"] * 1e12
-    jobs, cap = c4_trace()
-    ctx = S.Context(jobs, cap, S.SRTF, log=True)
+    jobs, cap = c4_trace() if cfg == "c4" else c5_trace()
+    ctx = S.Context(jobs, cap, pol, log=True)
     try:
         ctx.run()
         w = ctx.wall()
@@ -42,7 +44,8 @@ def main():
             g[2] += j.n_iters
     kern = rs["kernel_ns"] / 1e9
     busy = sum(meas.values())
-    out = {"kernel_s": kern, "sum_iteration_s": busy, "gap_s": kern - busy,
+    out = {"config": cfg, "policy": int(pol), "kernel_s": kern, "sum_iteration_s": busy, "gap_s": kern - busy,
+           "mean_concurrent_iterations": busy / kern,
            "groups": {f"w{k[0]}_L{k[1]}": {"measured_s": v[0], "ideal_s": v[1], "frac": v[1] / v[0] if v[0] else None,
                                           "iters": v[2], "us_per_iter": 1e6 * v[0] / v[2]}
                       for k, v in sorted(groups.items())},
