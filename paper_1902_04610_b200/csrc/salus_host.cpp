@@ -454,19 +454,22 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
       D.stage_tiles_lat[s] = (uint16_t)std::min<uint32_t>(xl + wl + extra, 0xFFFF);
     }
     // split-K (narrow records): a stage whose F / dX part has few pair tasks
-    // at N = 128 and a long K runs S K-slices of it (S x the tasks, each a
-    // 1/S of the weight stream): S in {4, 2} with npair x S <= SK_PAIRS
-    // (one wave of CTA pairs), K >= 2048 (below, a slice's partial write
-    // and reduction, ~4 us, cost what the shorter K saves), K-slices of >= 8
-    // chunks, whole double chunks;
-    // the workspace comes from the declared E's slack like the relaxed
-    // barrier's third G buffer
+    // and a long K (>= 2048: below, a slice's partial write and reduction,
+    // ~4 us, cost what the shorter K saves) runs S K-slices of it.  Among
+    // N in {128, 256} and S in {2, 4} with npair(N) x S <= SK_PAIRS (one wave
+    // of CTA pairs), slices of >= 8 chunks and whole double chunks, take the
+    // least bytes per CTA per task: (K / S) x (16 KiB of A + N/2 rows of B)
+    // per 64-chunk, plus the S partials (128 x N fp32 each) the last slice
+    // writes and reads (measured: N = 256 x 4 slices lost to N = 128 x 2 on
+    // a 4096-wide layer of batch 64).  The workspace comes from the declared E's
+    // slack like the relaxed barrier's third G buffer.
     for (uint32_t s = 0; s < MAX_STAGES; s++) D.splitk[s] = 1;
     D.ws_off = 0;
+    D.sk_wide = 0;
     if (splitk_enabled() && !(c->cfg.flags & SALUS_FLAG_NULL_WORK)) {
       constexpr uint32_t SK_PAIRS = 74;
       uint8_t sk[MAX_STAGES];
-      uint32_t np[MAX_STAGES];
+      uint32_t np[MAX_STAGES], wide = 0;
       uint64_t need = 0;
       for (uint32_t s = 0; s < MAX_STAGES; s++) { sk[s] = 1; np[s] = 0; }
       for (uint32_t s = 2; s < D.n_stages; s++) {
@@ -476,21 +479,31 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
         if (!fwd && l == 1) continue;                           // B_1 has no dX part
         const uint32_t dn = fwd ? D.dpad[l] : D.dpad[l - 1];
         const uint32_t nk = (fwd ? D.dpad[l - 1] : D.dpad[l]) / 64;
-        const uint32_t npair = pairs(D.bpad / 128) * (dn / 128);
-        for (uint32_t cand = SK_MAX; cand >= 2; cand /= 2) {
-          if (nk >= 32 && npair * cand <= SK_PAIRS && nk % (2 * cand) == 0 && nk / cand >= 8 &&
-              16 * npair <= SK_COUNTERS) {
-            sk[s] = (uint8_t)cand;
-            np[s] = npair;
-            need = std::max<uint64_t>(need, (uint64_t)npair * 2 * cand * 65536);
-            break;
+        if (nk < 32) continue;
+        uint64_t best = ~0ull;
+        for (uint32_t nt = 128; nt <= 256; nt *= 2) {
+          if (dn % nt) continue;
+          const uint32_t npair = pairs(D.bpad / 128) * (dn / nt);
+          for (uint32_t cand = 2; cand <= SK_MAX; cand *= 2) {
+            if (npair * cand > SK_PAIRS || nk % (2 * cand) || nk / cand < 8 || 16 * npair > SK_COUNTERS) continue;
+            // operand bytes of one slice + the last slice's partial traffic
+            const uint64_t cost = (uint64_t)(nk / cand) * (16384 + nt * 64) + (uint64_t)cand * nt * 512;
+            if (cost < best) {
+              best = cost;
+              sk[s] = (uint8_t)cand;
+              np[s] = npair;
+              wide = nt == 256 ? (wide | 1u << s) : (wide & ~(1u << s));
+            }
           }
         }
+        if (sk[s] > 1)
+          need = std::max<uint64_t>(need, (uint64_t)np[s] * 2 * sk[s] * (((wide >> s) & 1u) ? 2 : 1) * 65536);
       }
       const uint64_t end = D.relax ? (uint64_t)D.g_off3 + 2 * bp * mx : off;
       const uint64_t ws = align_up(end, 65536);
       if (need && (uint64_t)D.e_pages * G >= ws + need && ws + need < (1ull << 32)) {
         D.ws_off = (uint32_t)ws;
+        D.sk_wide = wide;
         D.ae_pages = std::max<uint32_t>(D.ae_pages, (uint32_t)((ws + need + G - 1) / G));
         for (uint32_t s = 2; s < D.n_stages; s++) {
           if (sk[s] < 2) continue;

@@ -96,8 +96,11 @@ constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;          // all of TMEM: 2 accumula
 enum : uint32_t { T_EXIT = 0, T_INIT = 1, T_GEN = 2, T_GEMM = 3, T_COPY = 4 };
 enum : uint32_t { EPI_RELU = 0, EPI_OUT = 1, EPI_LOSS = 2, EPI_DX = 3, EPI_SGD = 4 };
 // translated pointers of a tile: bf16 output panels, Wb panels (SGD/INIT),
-// fp32 master pages, epilogue-input panels (DX mask)
-enum : uint32_t { PTR_OUT = 0, PTR_AUX = 4, PTR_W32 = 8, PTR_EPI = 10, NPTR = 14 };
+// fp32 master pages, epilogue-input panels (DX mask); split-K partial
+// pages k = 0..7 (slice q, page p of an N/128-page partial: k = q N/128 + p)
+// in PTR_AUX..+3 then PTR_SK2..+3
+enum : uint32_t { PTR_OUT = 0, PTR_AUX = 4, PTR_W32 = 8, PTR_EPI = 10, PTR_SK2 = 14, NPTR = 18 };
+__host__ __device__ __forceinline__ uint32_t sk_ptr(uint32_t k) { return k < 4 ? PTR_AUX + k : PTR_SK2 + (k - 4); }
 
 struct OpDesc {
   const uint32_t *table;   // page table of the operand's space
@@ -283,6 +286,15 @@ __device__ __forceinline__ void decode_gen(TileDesc &td, const DevJob &J, uint32
   td.key = targets ? gen_key(J.seed, J.job_id, GEN_T, L, kx) : gen_key(J.seed, J.job_id, GEN_X, 0, kx);
 }
 
+// split-K: the partial pages of every slice of base tile u, CTA half h
+// (np = N / 128 pages per partial) -- the last slice reads them all
+__device__ __forceinline__ void defer_partials(TileDesc &td, const uint32_t *lt, uint32_t ws_off, uint32_t u,
+                                               uint32_t h, uint32_t S, uint32_t np) {
+  for (uint32_t q = 0; q < S; q++)
+    for (uint32_t p = 0; p < np; p++)
+      defer(td, sk_ptr(q * np + p), lt, ws_off + (((2 * u + h) * S + q) * np + p) * 65536u);
+}
+
 __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, const SlotHead &sl,
                             TileDesc &td, uint32_t h) {
   td.payload = payload;
@@ -426,7 +438,8 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
   } else if (stage <= L + 1) {                        // forward F_l
     const uint32_t l = stage - 1;
     const uint32_t S = narrow ? J.splitk[stage] : 1u;
-    const uint32_t N = S > 1 || (narrow && ((J.lat_narrow >> stage) & 1u)) ? 128u : ntile_for(J.dpad[l]);
+    const uint32_t N = S > 1 ? (((J.sk_wide >> stage) & 1u) ? 256u : 128u)
+                             : (narrow && ((J.lat_narrow >> stage) & 1u)) ? 128u : ntile_for(J.dpad[l]);
     const uint32_t ntn = J.dpad[l] / N, z = tile % S, u = tile / S;
     const uint32_t mb = 2 * (u / ntn) + h, nb = u % ntn;
     td.valid = mb < bp / 128;
@@ -439,8 +452,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     td.b = OpDesc{jt, J.wb_off[l - 1][kg & 1] + kc0 * J.dpad[l] * 128u, J.dpad[l], nb * N + h * (N / 2), 0};
     if (S > 1) {
       td.sk = (uint8_t)S; td.skz = (uint8_t)z; td.sku = (uint16_t)u;
-      if (td.valid)
-        for (uint32_t q = 0; q < S; q++) defer(td, PTR_AUX + q, lt, J.ws_off + ((2 * u + h) * S + q) * 65536u);
+      if (td.valid) defer_partials(td, lt, J.ws_off, u, h, S, N / 128);
     }
     td.m0 = mb * 128; td.n0 = nb * N;
     td.rows_valid = J.batch; td.cols_valid = J.dims[l]; td.ld_logical = J.dims[l];
@@ -506,7 +518,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
         td.dump_off = (int64_t)base;
       }
     } else {                                          // G_{l-1} = (G_l W_l^T) * [A_{l-1} > 0]
-      const uint32_t N = S > 1 ? 128u : Nw, ntn = J.dpad[l - 1] / N;
+      const uint32_t N = S > 1 ? (((J.sk_wide >> stage) & 1u) ? 256u : 128u) : Nw, ntn = J.dpad[l - 1] / N;
       td.N = N;
       const uint32_t ux = tile - nW, z = ux % S, u = ux / S, mb = 2 * (u / ntn) + h, nb = u % ntn;
       td.valid = mb < bp / 128;
@@ -518,8 +530,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
       td.b = OpDesc{jt, J.wb_off[l - 1][kg & 1] + kc0 * 8192u, J.dpad[l], nb * N + h * (N / 2), 1};
       if (S > 1) {
         td.sk = (uint8_t)S; td.skz = (uint8_t)z; td.sku = (uint16_t)u;
-        if (td.valid)
-          for (uint32_t q = 0; q < S; q++) defer(td, PTR_AUX + q, lt, J.ws_off + ((2 * u + h) * S + q) * 65536u);
+        if (td.valid) defer_partials(td, lt, J.ws_off, u, h, S, N / 128);
       }
       td.m0 = mb * 128; td.n0 = nb * N;
       td.rows_valid = J.batch; td.cols_valid = J.dims[l - 1];
@@ -1313,8 +1324,8 @@ __device__ void peer_mma_role(const Params &P, WorkerSmem &W) {
 }
 
 // Split-K (DevJob.splitk): every K-slice of a tile writes its fp32 partial
-// (this CTA's 128 rows x N = 128 columns, 64 KiB, layout sk_off) to its
-// workspace page, then counts itself on the
+// (this CTA's 128 rows x N columns, 64 KiB per 128 columns, layout sk_off)
+// to its workspace pages, then counts itself on the
 // slot's counter for (base tile, CTA half, epilogue warp).  The slice that
 // arrives last at a warp's counter sums that warp's region of the S
 // partials in slice order -- its own straight from TMEM -- and
@@ -1332,14 +1343,14 @@ __device__ __forceinline__ uint32_t sk_off(uint32_t cc, uint32_t r) {
 
 __device__ bool splitk_reduce(const Params &P, WorkerSmem &W, const TileDesc &td, uint32_t tacc, uint32_t r,
                               uint32_t hh, uint32_t et) {
-  const uint32_t S = td.sk, z = td.skz;
+  const uint32_t S = td.sk, z = td.skz, np = td.N / 128;   // partial pages (N = 128 or 256)
   const uint32_t taddr = tacc + (((r >> 5) * 32u) << 16);
   const uint32_t sub = (td.N / 32) / EPI_HALVES, cc0 = hh * sub;
   for (uint32_t cc = cc0; cc < cc0 + sub; cc++) {
     uint32_t raw[32];
     ptx::tmem_ld32(taddr + cc * 32u, raw);
     ptx::tmem_ld_wait();
-    float4 *dst = reinterpret_cast<float4 *>(td.ptr[PTR_AUX + z] + sk_off(cc, r));
+    float4 *dst = reinterpret_cast<float4 *>(td.ptr[sk_ptr(z * np + (cc >> 2))] + sk_off(cc & 3u, r));
 #pragma unroll
     for (int q = 0; q < 8; q++)
       __stcg(dst + 32 * q, make_float4(__uint_as_float(raw[4 * q]), __uint_as_float(raw[4 * q + 1]),
@@ -1373,7 +1384,8 @@ __device__ bool splitk_reduce(const Params &P, WorkerSmem &W, const TileDesc &td
     for (uint32_t i = 0; i < SK_MAX - 1; i++) {
       if (i + 1 < S) {
         const uint32_t q = i < z ? i : i + 1;
-        const float4 *src = reinterpret_cast<const float4 *>(td.ptr[PTR_AUX + q] + sk_off(c16 >> 1, r)) +
+        const uint32_t cc = c16 >> 1;
+        const float4 *src = reinterpret_cast<const float4 *>(td.ptr[sk_ptr(q * np + (cc >> 2))] + sk_off(cc & 3u, r)) +
                             32 * 4 * (c16 & 1u);
 #pragma unroll
         for (int g = 0; g < 4; g++) pv[i][g] = __ldcg(src + 32 * g);
