@@ -161,6 +161,10 @@ __device__ __forceinline__ void bulk_s2g_hint(void *gmem_dst, const void *smem_s
                "r"(smem_u32(smem_src)), "r"(bytes), "l"(policy)
                : "memory");
 }
+// bulk prefetch of [gmem, gmem + bytes) into L2 (no smem, no completion)
+__device__ __forceinline__ void bulk_prefetch_l2(const void *gmem, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(gmem), "r"(bytes) : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }

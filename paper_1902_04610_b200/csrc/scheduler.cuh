@@ -132,6 +132,11 @@ struct Sched {
     if (tid == 0 && err == 0) {
       atomicCAS(reinterpret_cast<int *>(&P.ctrl->status), 0, code);
       P.ctrl->err_info[0] = info;
+      if (P.host_abort) {   // the workers trap on the abort: leave the reason in the mapped slot
+        volatile uint32_t *h = const_cast<volatile uint32_t *>(P.host_abort);
+        h[1] = (uint32_t)code; h[2] = info; h[3] = (uint32_t)t;
+        __threadfence_system();
+      }
       atomicExch(&P.ctrl->abort, 1u);
     }
     err = 1;

@@ -113,6 +113,9 @@ struct OpDesc {
 #ifndef SALUS_KD
 #define SALUS_KD 1
 #endif
+#ifndef SALUS_W32_PF
+#define SALUS_W32_PF 0
+#endif
 static_assert(PIPE % 2 == 0, "double K-chunks take two operand stages");
 // SGD epilogue: the fp32 master chunk is updated in its smem buffer and
 // written back with one 32 KiB bulk (TMA) store per chunk
@@ -943,8 +946,15 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint
     }
     // every pointer-writing lane releases its own write (desc_ptrs counts
     // NPTR arrivals) rather than lane 0 on the others' behalf
-    if (lane < NPTR && ((td.xt_mask >> lane) & 1u))
+    if (lane < NPTR && ((td.xt_mask >> lane) & 1u)) {
       td.ptr[lane] = xlate(P, td.xt_tab[(td.xt_sel >> lane) & 1u], td.xt_off[lane]);
+#if SALUS_W32_PF
+      // SGD tiles: start pulling the fp32 master pages into L2 now, up to
+      // NDESC tiles before the epilogue-input loader streams them
+      if (lane >= PTR_W32 && lane < PTR_W32 + 2 && td.kind == T_GEMM && td.epi == EPI_SGD)
+        ptx::bulk_prefetch_l2(td.ptr[lane], PAGE_BYTES);
+#endif
+    }
     if (lane < NPTR) ptx::mbar_arrive(&W.desc_ptrs[d]);
     __syncwarp();
     if (++d == NDESC) { d = 0; d_phase ^= 1; }
