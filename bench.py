@@ -707,9 +707,13 @@ def side_section(key, S, device, jobs=None, cap=None):
     """One secondary measurement of the bench line; errors are recorded, not raised."""
     if jobs is None:
         jobs, cap = workload(1, 0)
+    t0 = time.time()
     try:
-        return SIDE_SECTIONS[key][1](S, device, jobs, cap)
+        out = SIDE_SECTIONS[key][1](S, device, jobs, cap)
+        print(f"[bench] section {key}: ok ({time.time() - t0:.1f} s)", file=sys.stderr, flush=True)
+        return out
     except Exception as exc:  # noqa: BLE001
+        print(f"[bench] section {key}: ERROR {exc}", file=sys.stderr, flush=True)
         return {"error": str(exc)[:200]}
 
 
@@ -897,7 +901,11 @@ def main():
     ctx.close()
     # C5 (configs[4], the metric's multi-GPU config): every rank takes part
     if not args.no_c5:
-        c5 = c5_section(S, local, rank, world, with_cpu_baseline=(not args.no_cpu_baseline and world == 1))
+        try:
+            c5 = c5_section(S, local, rank, world, with_cpu_baseline=(not args.no_cpu_baseline and world == 1))
+        except Exception as exc:  # noqa: BLE001  (recorded; the headline line still prints)
+            print(f"[bench] section c5: ERROR {exc}", file=sys.stderr, flush=True)
+            c5 = {"error": str(exc)[:200]}
         if rank == 0:
             line["c5"] = c5
     if rank == 0:

@@ -239,6 +239,10 @@ class Context:
         mb = C.c_uint64()
         self._check(self.L.salus_meta_bytes(self.ctx, C.byref(mb)), "meta_bytes")
         self.meta = torch.empty(max(256, mb.value), dtype=torch.uint8, device=f"cuda:{device}")
+        if self.poison:
+            # ... and the meta buffer all ones: a read of a table entry the
+            # library never wrote (a lane page not backed) faults at once
+            self.meta.fill_(0xFF)
         self._check(self.L.salus_prepare(self.ctx, C.c_void_p(self.meta.data_ptr()), mb.value), "prepare")
 
     def _poison(self):

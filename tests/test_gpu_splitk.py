@@ -37,8 +37,9 @@ CASES = [
 
 def _run(jobs, env=None):
     from paper_1902_04610_b200 import salus as S
-    old = {k: os.environ.get(k) for k in (env or {})}
-    os.environ.update(env or {})
+    env = {"SALUS_SPLITK": "1", **(env or {})}     # split-K is opt-in
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
     try:
         dump = {j.job_id: S.DUMP_OUTPUTS | (S.DUMP_WEIGHTS if j.kind == TRAIN else 0) for j in jobs}
         return assert_schedule_parity(jobs, 1 << 34, OS.FIFO, null_work=False, dump=dump)
