@@ -725,6 +725,7 @@ def main():
     ap.add_argument("--impl", default="salus", choices=["salus", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-c5", action="store_true", help="skip the C5 (2000-job) strong-scaling section")
+    ap.add_argument("--no-side", action="store_true", help="skip the single-GPU side sections (headline only)")
     ap.add_argument("--only", default="",
                     help="comma list of side sections to run alone and print (c1,c2b,c3,c3rate,c4,evict,jct,online,overhead,sched)")
     args = ap.parse_args()
@@ -880,10 +881,12 @@ def main():
         }
         # single-GPU side measurements: at N = 1 only (the other ranks would
         # otherwise wait minutes at the C5 barrier)
-        for k in (SIDE_SECTIONS if world == 1 else ()):
+        for k in (SIDE_SECTIONS if world == 1 and not args.no_side else ()):
             line[SIDE_SECTIONS[k][0]] = side_section(k, S, local, jobs, cap)
         # the paper's figures (2x P100, TF 1.5, private traces) beside ours: context only
         try:
+            if args.no_side:
+                raise KeyError("side sections skipped (--no-side)")
             line["paper_context"] = {
                 "avg_jct_fifo_over_srtf": {"ours_c4": line["c4_jct"]["fifo_over_srtf_avg_jct"], "paper": 3.19},
                 "sweep_fifo_over_salus": {"ours_c2a_physical_makespan":

@@ -7,6 +7,8 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libsalus.so")
+# the opt-in split-K build: SALUS_LIB=<this> and SALUS_SPLITK=1
+LIB_SPLITK = os.path.join(HERE, "libsalus_splitk.so")
 SOURCES = ["salus_kernel.cu", "salus_host.cpp"]
 HEADERS = ["salus_dev.h", "ptx.cuh", "datagen.cuh", "scheduler.cuh", "worker.cuh", "runahead.cuh"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -14,10 +16,10 @@ FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std
          "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
+def _stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
     deps.append(os.path.join(HERE, "..", "include", "salus.h"))
     return any(os.path.getmtime(d) > t for d in deps)
@@ -33,6 +35,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if verbose:
             sys.stderr.write(r.stderr)
     return LIB
+
+
+def build_splitk(force: bool = False) -> str:
+    """The opt-in split-K library (SALUS_SPLITK_BUILD=1), in-tree."""
+    if force or _stale(LIB_SPLITK):
+        build_variant(LIB_SPLITK, ["SALUS_SPLITK_BUILD=1"])
+    return LIB_SPLITK
 
 
 def build_variant(out: str, defines) -> str:

@@ -156,13 +156,14 @@ bool swap_enabled() {
   const char *e = getenv("SALUS_SWAP");
   return e && e[0] == '1';
 }
-// Split-K in narrow records (DevJob.splitk) is opt-in (SALUS_SPLITK=1): it
+// Split-K in narrow records (DevJob.splitk) is opt-in (the SALUS_SPLITK_BUILD
+// library, libsalus_splitk.so, with SALUS_SPLITK=1): it
 // gains 1-3% on C4 / C5 and 15% on a lone 4096-wide job, but long runs in
 // the full bench process hung in 3 of 3 attempts while every
 // isolated run and test passed; until that is understood it stays off
 bool splitk_enabled() {
   const char *e = getenv("SALUS_SPLITK");
-  return e && e[0] == '1';
+  return SALUS_SPLITK_BUILD && e && e[0] == '1';
 }
 bool relax_enabled() {
   const char *e = getenv("SALUS_RELAX");

@@ -99,7 +99,8 @@ enum : uint32_t { EPI_RELU = 0, EPI_OUT = 1, EPI_LOSS = 2, EPI_DX = 3, EPI_SGD =
 // fp32 master pages, epilogue-input panels (DX mask); split-K partial
 // pages k = 0..7 (slice q, page p of an N/128-page partial: k = q N/128 + p)
 // in PTR_AUX..+3 then PTR_SK2..+3
-enum : uint32_t { PTR_OUT = 0, PTR_AUX = 4, PTR_W32 = 8, PTR_EPI = 10, PTR_SK2 = 14, NPTR = 18 };
+enum : uint32_t { PTR_OUT = 0, PTR_AUX = 4, PTR_W32 = 8, PTR_EPI = 10, PTR_SK2 = 14,
+                  NPTR = SALUS_SPLITK_BUILD ? 18 : 14 };
 __host__ __device__ __forceinline__ uint32_t sk_ptr(uint32_t k) { return k < 4 ? PTR_AUX + k : PTR_SK2 + (k - 4); }
 
 struct OpDesc {
@@ -111,7 +112,7 @@ struct OpDesc {
 #define SALUS_L2HINT 1
 #endif
 #ifndef SALUS_KD
-#define SALUS_KD 1
+#define SALUS_KD 0
 #endif
 #ifndef SALUS_W32_PF
 #define SALUS_W32_PF 0
@@ -295,7 +296,7 @@ __device__ __forceinline__ void defer_partials(TileDesc &td, const uint32_t *lt,
                                                uint32_t h, uint32_t S, uint32_t np) {
   for (uint32_t q = 0; q < S; q++)
     for (uint32_t p = 0; p < np; p++)
-      defer(td, sk_ptr(q * np + p), lt, ws_off + (((2 * u + h) * S + q) * np + p) * 65536u);
+      if (sk_ptr(q * np + p) < NPTR) defer(td, sk_ptr(q * np + p), lt, ws_off + (((2 * u + h) * S + q) * np + p) * 65536u);
 }
 
 __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, const SlotHead &sl,
@@ -440,7 +441,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     }
   } else if (stage <= L + 1) {                        // forward F_l
     const uint32_t l = stage - 1;
-    const uint32_t S = narrow ? J.splitk[stage] : 1u;
+    const uint32_t S = (SALUS_SPLITK_BUILD && narrow) ? J.splitk[stage] : 1u;
     const uint32_t N = S > 1 ? (((J.sk_wide >> stage) & 1u) ? 256u : 128u)
                              : (narrow && ((J.lat_narrow >> stage) & 1u)) ? 128u : ntile_for(J.dpad[l]);
     const uint32_t ntn = J.dpad[l] / N, z = tile % S, u = tile / S;
@@ -480,7 +481,7 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     const uint32_t tile_in = tile;
     const uint32_t l = L - (stage - (L + 2));
     const uint32_t Nw = narrow && ((J.lat_narrow >> stage) & 1u) ? 128u : ntile_for(J.dpad[l - 1]);
-    const uint32_t S = narrow ? J.splitk[stage] : 1u;           // K-slices of the dX part (N = 128)
+    const uint32_t S = (SALUS_SPLITK_BUILD && narrow) ? J.splitk[stage] : 1u;   // K-slices of the dX part
     const uint32_t nW = ((J.dpad[l] / 128 + 1) / 2) * (J.dpad[l - 1] / Nw);     // dW pair tasks
     // G_l lives in buffer (L - l) mod 2, or mod 3 in a relaxed record
     const uint32_t g3[3] = {J.g_off[0], J.g_off[1], J.g_off3};
@@ -1455,7 +1456,11 @@ __device__ void epilogue_warps(const Params &P, WorkerSmem &W, uint32_t tmem, ui
       t_mma = ptx::globaltimer();
       const uint32_t tacc = tmem + b * ACC_COLS;
       // split-K: only the tile's last K-slice (holding the summed partials) runs the epilogue
+#if SALUS_SPLITK_BUILD
       const bool epi = !td.valid || td.sk < 2 || splitk_reduce(P, W, td, tacc, r, h, et);
+#else
+      constexpr bool epi = true;
+#endif
       if (!td.valid) {
         // the peer half of a super-tile past the last M block: nothing to store
       } else if (td.swap) {

@@ -1,54 +1,70 @@
-"""Split-K tiles (DevJob.splitk): in narrow latency-mode
-records a stage whose F / dX part has few pair tasks and a long K runs as S
-K-slices; the last slice of a tile sums the fp32 partials in slice order
-and runs the epilogue.  The math is the same GEMM (P:98-104 forward /
-backward of a dense layer), so parity is the oracle's at the north-star
-tolerance; the fixed summation order makes repeated runs bit-identical."""
-import os
+"""Split-K tiles (DevJob.splitk; the opt-in library
+libsalus_splitk.so with SALUS_SPLITK=1): in narrow latency-mode records a
+stage whose F / dX part has few pair tasks and a long K runs as S K-slices;
+the last slice of a tile sums the fp32 partials in slice order and runs the
+epilogue.  The math is the same GEMM (P:98-104 forward / backward of a
+dense layer), so parity is the oracle's at the north-star tolerance; the
+fixed summation order makes repeated runs bit-identical.
 
-import numpy as np
+The opt-in library is a different .so, so every case runs in a child
+process with SALUS_LIB pointing at it (the parent keeps the default one)."""
+import json
+import os
+import subprocess
+import sys
+
 import pytest
 
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r'''
+import json, os, sys
+sys.path.insert(0, os.environ["SALUS_ROOT"]); sys.path.insert(0, os.path.join(os.environ["SALUS_ROOT"], "tests"))
+import numpy as np
 from oracle import scheduler as OS
 from workloads import INFER, TRAIN, make_job, footprint_bytes
-
-MIB = 1 << 20
-
 from gpu_helpers import assert_schedule_parity
 from test_gpu_math import _check_math
+from paper_1902_04610_b200 import salus as S
+assert S.LIB_PATH.endswith("libsalus_splitk.so"), S.LIB_PATH
+kind, dims, batch, slack, n, seed, lr = json.loads(sys.argv[1])
+_, e = footprint_bytes(kind, tuple(dims), batch)
+req = tuple(range(0, 10 * n, 10)) if kind == INFER else ()
+jobs = [make_job(5, kind, 0, tuple(dims), batch, n, ephemeral_bytes=e + slack, request_ticks=req, lr=lr, seed=seed)]
+dump = {5: S.DUMP_OUTPUTS | (S.DUMP_WEIGHTS if kind == TRAIN else 0)}
+ctx, _, _ = assert_schedule_parity(jobs, 1 << 34, OS.FIFO, null_work=False, dump=dump)
+try:
+    worst = _check_math(ctx, jobs)
+    out = np.concatenate([ctx.layers(5, k).ravel() for k in range(n)])
+    w = ctx.layers(5, S.WEIGHTS).ravel() if kind == TRAIN else np.zeros(1, np.float32)
+    print(json.dumps({"worst": worst, "n_tasks": ctx.run_stats()["n_tasks"],
+                      "digest": [float(out.sum(dtype=np.float64)), float(np.abs(w).sum(dtype=np.float64)),
+                                 out.tobytes().hex()[:64], w.tobytes().hex()[-64:]]}))
+finally:
+    ctx.close()
+'''
 
-pytestmark = pytest.mark.gpu
+
+def _run(case, splitk):
+    from paper_1902_04610_b200 import build
+    lib = build.build_splitk()
+    env = dict(os.environ, SALUS_LIB=lib, SALUS_SPLITK="1" if splitk else "0", SALUS_ROOT=ROOT)
+    r = subprocess.run([sys.executable, "-c", CHILD, json.dumps(case)], capture_output=True, text=True,
+                       env=env, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-4000:]
+    return json.loads(r.stdout.strip().splitlines()[-1])
 
 
-def _job(jid, kind, dims, batch, n, slack=64 * MIB, **kw):
-    _, e = footprint_bytes(kind, dims, batch)
-    req = tuple(range(0, 10 * n, 10)) if kind == INFER else ()
-    return make_job(jid, kind, 0, dims, batch, n, ephemeral_bytes=e + slack, request_ticks=req, **kw)
-
-
+MIB = 1 << 20
+TRAIN, INFER = 0, 1
 CASES = [
-    # (kind, dims, batch): F / dX stages of 16-32 N=128 pair tasks, K 1024-4096
+    # (kind, dims, batch): F / dX stages of 16-32 N=128 pair tasks, K 2048-4096
     (TRAIN, (2048, 2048, 2048, 512), 128),
     (TRAIN, (1024, 2048, 1024), 200),          # bp = 256: both CTA halves hold rows, ragged batch
-    (TRAIN, (4096, 4096, 256), 64),
+    (TRAIN, (4096, 4096, 256), 64),            # N = 256 slices on the 4096-wide layer
     (INFER, (4096, 4096, 256), 8),
 ]
-
-
-def _run(jobs, env=None):
-    from paper_1902_04610_b200 import salus as S
-    env = {"SALUS_SPLITK": "1", **(env or {})}     # split-K is opt-in
-    old = {k: os.environ.get(k) for k in env}
-    os.environ.update(env)
-    try:
-        dump = {j.job_id: S.DUMP_OUTPUTS | (S.DUMP_WEIGHTS if j.kind == TRAIN else 0) for j in jobs}
-        return assert_schedule_parity(jobs, 1 << 34, OS.FIFO, null_work=False, dump=dump)
-    finally:
-        for k, v in old.items():
-            if v is None:
-                os.environ.pop(k, None)
-            else:
-                os.environ[k] = v
 
 
 @pytest.mark.parametrize("kind,dims,batch", CASES)
@@ -56,50 +72,21 @@ def test_splitk_parity(kind, dims, batch):
     """One job alone (FIFO: one lane, narrow records): outputs of every
     iteration and the final weights / weight updates within 2e-2 of the
     oracle; split-K actually ran (more tiles than with SALUS_SPLITK=0)."""
-    jobs = [_job(5, kind, dims, batch, 3, lr=5e-3, seed=11)]
-    ctx, _, _ = _run(jobs)
-    try:
-        worst_split = _check_math(ctx, jobs)
-        n_split = ctx.run_stats()["n_tasks"]
-    finally:
-        ctx.close()
-    ctx, _, _ = _run(jobs, {"SALUS_SPLITK": "0"})
-    try:
-        worst_plain = _check_math(ctx, jobs)
-        n_plain = ctx.run_stats()["n_tasks"]
-    finally:
-        ctx.close()
-    print(f"worst rel: split {worst_split:.3e} plain {worst_plain:.3e}")
-    assert n_split > n_plain, (n_split, n_plain)
+    case = [kind, list(dims), batch, 64 * MIB, 3, 11, 5e-3]
+    a = _run(case, True)
+    b = _run(case, False)
+    print(f"worst rel: split {a['worst']:.3e} plain {b['worst']:.3e}")
+    assert a["n_tasks"] > b["n_tasks"], (a["n_tasks"], b["n_tasks"])
 
 
 def test_splitk_deterministic():
     """The last slice sums the partials in slice order whichever slice
     arrives last: two runs give bit-identical outputs and weights."""
-    from paper_1902_04610_b200 import salus as S
-    jobs = [_job(7, TRAIN, (2048, 2048, 2048, 512), 128, 3, lr=1e-2, seed=12)]
-    got = []
-    for _ in range(2):
-        ctx, _, _ = _run(jobs)
-        try:
-            got.append((np.concatenate([ctx.layers(7, k).ravel() for k in range(3)]), ctx.layers(7, S.WEIGHTS).copy()))
-        finally:
-            ctx.close()
-    assert np.array_equal(got[0][0], got[1][0]) and np.array_equal(got[0][1], got[1][1])
+    case = [TRAIN, [2048, 2048, 2048, 512], 128, 64 * MIB, 3, 12, 1e-2]
+    assert _run(case, True)["digest"] == _run(case, True)["digest"]
 
 
 def test_splitk_needs_slack():
     """A job that declares exactly its footprint has no workspace: no split."""
-    dims, batch = (2048, 2048, 2048, 512), 128
-    jobs = [_job(9, TRAIN, dims, batch, 2, slack=0, lr=1e-2, seed=13)]
-    ctx, _, _ = _run(jobs)
-    try:
-        _check_math(ctx, jobs)
-        a = ctx.run_stats()["n_tasks"]
-    finally:
-        ctx.close()
-    ctx, _, _ = _run(jobs, {"SALUS_SPLITK": "0"})
-    try:
-        assert ctx.run_stats()["n_tasks"] == a
-    finally:
-        ctx.close()
+    case = [TRAIN, [2048, 2048, 2048, 512], 128, 0, 2, 13, 1e-2]
+    assert _run(case, True)["n_tasks"] == _run(case, False)["n_tasks"]
