@@ -165,6 +165,11 @@ bool splitk_enabled() {
   const char *e = getenv("SALUS_SPLITK");
   return SALUS_SPLITK_BUILD && e && e[0] == '1';
 }
+// Targets generated in the GEN stage (DevJob.t_in_g): SALUS_TG=0 disables
+bool tg_enabled() {
+  const char *e = getenv("SALUS_TG");
+  return !(e && e[0] == '0');
+}
 bool relax_enabled() {
   const char *e = getenv("SALUS_RELAX");
   return !(e && e[0] == '0');
@@ -420,6 +425,9 @@ static void fill_devjob(salus_ctx *c, const HostJob &h, DevJob &D, uint64_t &req
     D.stage_tiles[0] = pairs(ti);
     D.stage_tiles[1] = pairs((D.bpad / 128) * (D.dpad[0] / 128));
     D.t_gen_tiles = (D.xpre && j.kind == SALUS_TRAIN) ? pairs((D.bpad / 128) * (D.dpad[L] / 128)) : 0;
+    D.t_in_g = (!D.xpre && j.kind == SALUS_TRAIN && !(c->cfg.flags & SALUS_FLAG_NULL_WORK) && tg_enabled())
+                   ? pairs((D.bpad / 128) * (D.dpad[L] / 128)) : 0;
+    D.stage_tiles[1] += D.t_in_g;
     D.n_stages = last_stage(j.kind, L) + 1;
     // K9 (opt-in, swap_enabled): an inference job with a 128-row batch
     // (b <= 128; C3's requests of b = 1..16) takes transposed

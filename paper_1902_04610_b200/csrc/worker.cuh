@@ -401,7 +401,9 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
     return;
   }
   if (stage == 1) {                                   // GEN input batch X (128 x 128 blocks)
-    decode_gen(td, J, tile, h, lt, J.act_off[0], kg);
+    const uint32_t ngx = J.stage_tiles[1] - J.t_in_g;
+    if (tile >= ngx) decode_gen(td, J, tile - ngx, h, lt, J.g_off[0], kg, true);   // T_k into G (t_in_g)
+    else decode_gen(td, J, tile, h, lt, J.act_off[0], kg);
     return;
   }
   // where X_k is read from: the lane (GEN stage) or the job's prefetch buffer
@@ -468,6 +470,10 @@ __device__ void decode_task(const Params &P, uint32_t payload, const DevJob &J, 
       if (J.t_gen_tiles && td.valid) {               // prefetched T_k: 2 target panels per input chunk
         for (uint32_t q = 0; q < N / 64; q++)
           defer(td, PTR_EPI + q, jt, J.t_off[kg & 1] + (nb * N / 64 + q) * bp * 128u + mb * 16384u);
+        td.n_ech = N / 128;
+      } else if (J.t_in_g && td.valid) {             // T_k from this record's GEN stage, in G_L's place
+        for (uint32_t q = 0; q < N / 64; q++)
+          defer(td, PTR_EPI + q, lt, J.g_off[0] + (nb * N / 64 + q) * bp * 128u + mb * 16384u);
         td.n_ech = N / 128;
       }
     } else { td.epi = EPI_OUT; out_off = J.act_off[L]; }
@@ -1216,7 +1222,9 @@ __device__ void epi_loader(const Params &P, WorkerSmem &W, uint32_t h) {
       // stage began (earlier stages or iterations), except the prefetched
       // targets T_0 of a 1-layer GEN-prefetch job, which its INIT stage --
       // the loss stage's own predecessor -- generates
-      if (td.wait && td.epi == EPI_LOSS && n && td.iter == 0) wait_stage(P, td.slot, td.dep_stage, td.dep_want);
+      // (and a 1-layer job's T from the GEN stage right before its F_1 = F_L)
+      if (td.wait && td.epi == EPI_LOSS && n && (td.iter == 0 || td.dep_stage == 1))
+        wait_stage(P, td.slot, td.dep_stage, td.dep_want);
       for (uint32_t c = 0; c < n; c++) {
         ptx::mbar_wait_abortable(&W.epi_empty[e], e_phase ^ 1, &P.ctrl->abort);
         if (!td.ech_load) {                   // K9 staging chunk: reserved, nothing to load

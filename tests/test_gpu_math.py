@@ -53,7 +53,8 @@ def _check_math(ctx, jobs, iters=None):
 
 @pytest.mark.parametrize("kind", [TRAIN, INFER])
 @pytest.mark.parametrize("dims,batch", [((128, 256, 128), 128), ((256, 256, 256), 200),
-                                        ((384, 128, 256, 128), 100), ((200, 256, 72), 300)])
+                                        ((384, 128, 256, 128), 100), ((200, 256, 72), 300),
+                                        ((256, 384), 136)])      # one layer: F_1 is F_L (loss after GEN)
 def test_tiny_jobs(kind, dims, batch):
     """lr = 1e-2 is the top of the C2 sweep's range (A32: larger rates amplify
     fp32-vs-fp64 rounding differences chaotically, even between two CPUs)."""
