@@ -117,9 +117,6 @@ struct OpDesc {
 #ifndef SALUS_W32_PF
 #define SALUS_W32_PF 0
 #endif
-#ifndef SALUS_GEN_T4
-#define SALUS_GEN_T4 1
-#endif
 static_assert(PIPE % 2 == 0, "double K-chunks take two operand stages");
 // SGD epilogue: the fp32 master chunk is updated in its smem buffer and
 // written back with one 32 KiB bulk (TMA) store per chunk
@@ -836,26 +833,6 @@ __device__ void gen_tile(const TileDesc &td, uint32_t r, uint32_t h) {
   const uint64_t key = td.key, base = (uint64_t)m * cols + n0;
   uint8_t *const out0 = td.ptr[PTR_OUT], *const out1 = td.ptr[PTR_OUT + 1];
   const int ncol = m < td.rows_valid ? (int)cols - (int)n0 : 0;
-#if SALUS_GEN_T4
-  // 32 columns (4 chunks) at a time, stored through the 4x4 chunk transpose:
-  // every store instruction writes 8 rows x 64 contiguous bytes instead of
-  // 32 rows x 16 bytes
-#pragma unroll 1
-  for (uint32_t c32 = h * (128 / EPI_HALVES); c32 < (h + 1) * (128 / EPI_HALVES); c32 += 32) {
-    uint4 u[4];
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const uint32_t cg = c32 + 8 * q;
-      float v[8];
-      gen_run(key, base + cg, 1.0f, v);
-#pragma unroll
-      for (int x = 0; x < 8; x++) v[x] = (int)(cg + x) < ncol ? v[x] : 0.f;
-      u[q].x = pack_bf16x2(v[0], v[1]); u[q].y = pack_bf16x2(v[2], v[3]);
-      u[q].z = pack_bf16x2(v[4], v[5]); u[q].w = pack_bf16x2(v[6], v[7]);
-    }
-    store_bf16_rows(c32 < 64 ? out0 : out1, u, r, (c32 % 64) / 8);
-  }
-#else
 #pragma unroll 2
   for (uint32_t cg = h * (128 / EPI_HALVES); cg < (h + 1) * (128 / EPI_HALVES); cg += 8) {
     float v[8];
@@ -867,7 +844,6 @@ __device__ void gen_tile(const TileDesc &td, uint32_t r, uint32_t h) {
     u.z = pack_bf16x2(v[4], v[5]); u.w = pack_bf16x2(v[6], v[7]);
     *reinterpret_cast<uint4 *>((cg < 64 ? out0 : out1) + swz(r, (cg % 64) / 8)) = u;
   }
-#endif
 }
 
 // A35 swap copy: one 64 KiB page between the arena and the pinned host swap
