@@ -957,8 +957,12 @@ __device__ void decoder_warp(const Params &P, WorkerSmem &W, uint32_t lane, uint
       td.ptr[lane] = xlate(P, td.xt_tab[(td.xt_sel >> lane) & 1u], td.xt_off[lane]);
 #if SALUS_W32_PF
       // SGD tiles: start pulling the fp32 master pages into L2 now, up to
-      // NDESC tiles before the epilogue-input loader streams them
-      if (lane >= PTR_W32 && lane < PTR_W32 + 2 && td.kind == T_GEMM && td.epi == EPI_SGD)
+      // NDESC tiles before the epilogue-input loader streams them -- in
+      // eager (latency-mode) records only (SALUS_W32_PF=1; 2 = every
+      // record, measured -3.5% on C2a): a claimed eager tile usually waits
+      // for its predecessor stage, and with few lanes L2 has the room
+      if (lane >= PTR_W32 && lane < PTR_W32 + 2 && td.kind == T_GEMM && td.epi == EPI_SGD &&
+          (SALUS_W32_PF == 2 || td.eager))
         ptx::bulk_prefetch_l2(td.ptr[lane], PAGE_BYTES);
 #endif
     }
