@@ -118,7 +118,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t *bar, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait_abortable(uint64_t *bar, uint32_t parity, const uint32_t *abort_flag) {
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
-    if ((++spins & 4095u) == 0 && *(const volatile uint32_t *)abort_flag) __trap();
+    if ((++spins & 4095u) == 0 && *(const volatile uint32_t *)abort_flag) {
+#if SALUS_DBG_NOTRAP   // debugging builds: give up and let the kernel exit so its state can be read
+      return;
+#else
+      __trap();
+#endif
+    }
   }
 }
 

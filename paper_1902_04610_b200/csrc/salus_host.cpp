@@ -1161,6 +1161,29 @@ int salus_read_trace(salus_ctx *ctx, salus_trace_rec *buf, uint64_t cap_recs, ui
   return e ? cuda_fail(ctx, e, "read trace") : SALUS_OK;
 }
 
+int salus_debug_layout(const salus_ctx *ctx, uint64_t *out, uint32_t n) {
+  if (!ctx || !out || n < 9) return SALUS_E_INVAL;
+  if (ctx->state == 0) return SALUS_E_STATE;
+  out[0] = ctx->off_ctrl; out[1] = ctx->off_slots; out[2] = sizeof(Slot); out[3] = ctx->off_trace;
+  out[4] = ctx->trace_cap; out[5] = offsetof(Slot, stage_done); out[6] = offsetof(Slot, qstate);
+  out[7] = offsetof(Slot, done_seq); out[8] = offsetof(Ctrl, n_trace);
+  return SALUS_OK;
+}
+
+int salus_debug_read(salus_ctx *ctx, uint64_t off, uint64_t bytes, void *host) {
+  if (!ctx || !host) return SALUS_E_INVAL;
+  if (ctx->state == 0) return SALUS_E_STATE;
+  if (off > ctx->meta_bytes || bytes > ctx->meta_bytes - off) return SALUS_E_INVAL;
+  cudaError_t e = cudaSetDevice(ctx->cfg.device);
+  if (e != cudaSuccess) return cuda_fail(ctx, e, "cudaSetDevice");
+  if (!ctx->side && (e = cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking)))
+    return cuda_fail(ctx, e, "side stream");
+  if ((e = cudaMemcpyAsync(host, ctx->meta + off, bytes, cudaMemcpyDeviceToHost, ctx->side)) ||
+      (e = cudaStreamSynchronize(ctx->side)))
+    return cuda_fail(ctx, e, "debug read");
+  return SALUS_OK;
+}
+
 int salus_read_handoffs(salus_ctx *ctx, salus_handoff_rec *buf, uint64_t cap_recs, uint64_t *n_recs) {
   if (!ctx || !n_recs) return SALUS_E_INVAL;
   if (!ctx->ran || !(ctx->cfg.flags & SALUS_FLAG_CHECK)) return fail(ctx, SALUS_E_STATE, "no hand-off record (SALUS_FLAG_CHECK)");

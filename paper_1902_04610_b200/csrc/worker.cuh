@@ -1002,7 +1002,13 @@ __device__ __forceinline__ void wait_stage(const Params &P, uint32_t slot, uint3
     uint32_t v;
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
     if (v >= want) break;
-    if ((++spins & 4095u) == 0 && *(volatile uint32_t *)&P.ctrl->abort) __trap();
+    if ((++spins & 4095u) == 0 && *(volatile uint32_t *)&P.ctrl->abort) {
+#if SALUS_DBG_NOTRAP
+      return;
+#else
+      __trap();
+#endif
+    }
   }
   (void)ld_acquire_u32(c);
   ptx::fence_proxy_async_global();

@@ -88,7 +88,8 @@ EXPORTS = ["salus_open", "salus_job_footprint", "salus_submit_job", "salus_meta_
            "salus_read_wall", "salus_read_trace", "salus_read_layers", "salus_last_error", "salus_close",
            "salus_run_async", "salus_submit_live", "salus_end_submissions", "salus_wait",
            "salus_swap_bytes", "salus_set_swap", "salus_poll_stats", "salus_read_state",
-           "salus_submit_requests", "salus_read_requests", "salus_read_handoffs"]
+           "salus_submit_requests", "salus_read_requests", "salus_read_handoffs", "salus_debug_layout",
+           "salus_debug_read"]
 
 _lib = None
 _POISONED: List[tuple] = []   # buffers of poisoned contexts, kept alive for the process
