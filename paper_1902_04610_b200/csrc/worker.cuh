@@ -111,6 +111,8 @@ struct OpDesc {
 #ifndef SALUS_L2HINT
 #define SALUS_L2HINT 1
 #endif
+// double K-chunks for dW / dX tiles (off: no net gain, profiles/r02/ab_kd.txt;
+// together with split-K a C4 PACK run can hang, DESIGN.md §6 open issue)
 #ifndef SALUS_KD
 #define SALUS_KD 0
 #endif
