@@ -119,6 +119,9 @@ struct OpDesc {
 #ifndef SALUS_W32_PF
 #define SALUS_W32_PF 0
 #endif
+#ifndef SALUS_WAIT_ACQ
+#define SALUS_WAIT_ACQ 0
+#endif
 static_assert(PIPE % 2 == 0, "double K-chunks take two operand stages");
 // SGD epilogue: the fp32 master chunk is updated in its smem buffer and
 // written back with one 32 KiB bulk (TMA) store per chunk
@@ -1002,8 +1005,13 @@ __device__ __forceinline__ void wait_stage(const Params &P, uint32_t slot, uint3
   uint32_t spins = 0;
   for (;;) {
     uint32_t v;
+#if SALUS_WAIT_ACQ   // every poll an acquire: no re-load round trip once the count is seen
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+    if (v >= want) { ptx::fence_proxy_async_global(); return; }
+#else
     asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
     if (v >= want) break;
+#endif
     if ((++spins & 4095u) == 0 && *(volatile uint32_t *)&P.ctrl->abort) {
 #if SALUS_DBG_NOTRAP
       return;
