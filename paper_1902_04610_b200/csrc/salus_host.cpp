@@ -720,7 +720,7 @@ int salus_prepare(salus_ctx *ctx, void *meta, uint64_t meta_bytes) {
   if ((e = cudaStreamSynchronize(st))) return cuda_fail(ctx, e, "sync");
   ctx->h2d_bytes = sizeof(DevJob) * n + 8 * req.size() + 2 * inf.size();
   if ((e = flag_alloc(&ctx->host_abort, &ctx->host_abort_dev))) return cuda_fail(ctx, e, "abort flag");
-  for (int k = 0; k < 4; k++) reinterpret_cast<volatile uint32_t *>(ctx->host_abort)[k] = 0;
+  for (int k = 0; k < 8; k++) reinterpret_cast<volatile uint32_t *>(ctx->host_abort)[k] = 0;
   if ((e = cudaEventCreate(&ctx->ev0)) || (e = cudaEventCreate(&ctx->ev1))) return cuda_fail(ctx, e, "events");
 
   Params &P = ctx->P;
@@ -852,7 +852,7 @@ int salus_run_async(salus_ctx *ctx) {
       return cuda_fail(ctx, e, "reset stats");
     ctx->run_h2d = sizeof(salus_job_stat) * ctx->stats_img.size();
   }
-  for (int k = 0; k < 4; k++) reinterpret_cast<volatile uint32_t *>(ctx->host_abort)[k] = 0;
+  for (int k = 0; k < 8; k++) reinterpret_cast<volatile uint32_t *>(ctx->host_abort)[k] = 0;
   // migration: every run starts from the resume images (a DUMP_STATE job's
   // region is overwritten with its final state by the previous run)
   for (uint32_t d = 0; d < (uint32_t)ctx->djobs.size() && d < ctx->n_pre; d++) {
@@ -1027,9 +1027,12 @@ int salus_wait(salus_ctx *ctx, salus_job_stat *stats, uint64_t max_stats, uint64
       ctx->running = false;
       // a scheduler failure aborts the workers, which trap: its code is in the mapped slot
       const volatile uint32_t *h = ctx->host_abort;
-      const std::string where = h[1] ? "kernel (scheduler failure " + std::to_string((int32_t)h[1]) + ", info " +
-                                           std::to_string(h[2]) + ", tick " + std::to_string(h[3]) + ")"
-                                     : std::string("kernel");
+      std::string where = h[1] ? "kernel (scheduler failure " + std::to_string((int32_t)h[1]) + ", info " +
+                                     std::to_string(h[2]) + ", tick " + std::to_string(h[3]) + ")"
+                               : std::string("kernel");
+      if (h[4])   // SALUS_DBG_BOUNDS builds: a page number outside the arena
+        where += " (bad page: site " + std::to_string(h[4]) + ", offset/chunk " + std::to_string(h[5]) +
+                 ", entry " + std::to_string(h[6]) + ")";
       return cuda_fail(ctx, e, where.c_str());
     }
     const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

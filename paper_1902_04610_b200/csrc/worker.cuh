@@ -190,8 +190,32 @@ struct WorkerSmem {
 
 static_assert(sizeof(DevJob) <= 512, "DevJob must fit the decoder cache");
 
+#ifndef SALUS_DBG_BOUNDS
+#define SALUS_DBG_BOUNDS 0
+#endif
+// Debugging builds (SALUS_DBG_BOUNDS): a page number outside the arena --
+// with SALUS_POISON's all-ones meta, a table entry the scheduler never
+// wrote -- is reported through the mapped abort slot (words 4..7: site,
+// offset, entry, table address low bits) and traps.
+__device__ __forceinline__ uint32_t check_page(const Params &P, uint32_t page, uint32_t site, uint32_t off,
+                                               const uint32_t *table) {
+#if SALUS_DBG_BOUNDS
+  if (page >= P.Cp) {
+    if (P.host_abort) {
+      volatile uint32_t *h = const_cast<volatile uint32_t *>(P.host_abort);
+      h[4] = site; h[5] = off; h[6] = page; h[7] = (uint32_t)(uintptr_t)table;
+      __threadfence_system();
+    }
+    __trap();
+  }
+#else
+  (void)P; (void)site; (void)off; (void)table;
+#endif
+  return page;
+}
+
 __device__ __forceinline__ uint8_t *xlate(const Params &P, const uint32_t *table, uint32_t off) {
-  const uint32_t page = table[off >> PAGE_SHIFT];
+  const uint32_t page = check_page(P, table[off >> PAGE_SHIFT], 1, off, table);
   return P.arena + ((uint64_t)page << PAGE_SHIFT) + (off & (PAGE_BYTES - 1));
 }
 
@@ -1042,6 +1066,18 @@ __device__ __forceinline__ ChunkPages kd_pages(const OpDesc &a, const OpDesc &b,
   return p;
 }
 
+__device__ __forceinline__ void check_chunk(const Params &P, const ChunkPages &p, uint32_t nca, uint32_t ncb,
+                                            uint32_t site, uint32_t kc) {
+#if SALUS_DBG_BOUNDS
+  if (nca > 0) check_page(P, p.a0, site, kc, nullptr);
+  if (nca > 1) check_page(P, p.a1, site + 1, kc, nullptr);
+  if (ncb > 0) check_page(P, p.b0, site + 2, kc, nullptr);
+  if (ncb > 1) check_page(P, p.b1, site + 3, kc, nullptr);
+#else
+  (void)P; (void)p; (void)nca; (void)ncb; (void)site; (void)kc;
+#endif
+}
+
 // Operand loads of a double-K tile: double chunk kc2 takes two ring stages,
 // A (two 16 KiB blocks) in the first and B (one 16 KiB block per 64 columns
 // of this CTA's half of N) in the second, each armed on its own leader
@@ -1061,6 +1097,7 @@ __device__ void load_kd(const Params &P, WorkerSmem &W, const TileDesc &td, uint
     ChunkPages pg[PIPE / 2];
     for (uint32_t kc = 0; kc < pre; kc++) {
       pg[kc] = kd_pages(a, b, nca, ncb, kc);
+      check_chunk(P, pg[kc], nca, ncb, 10, kc);
       const uint32_t sa = s2;
       if (++s2 == PIPE) { s2 = 0; ph2 ^= 1; }
       const uint32_t sb = s2, phb = ph2;
@@ -1089,6 +1126,7 @@ __device__ void load_kd(const Params &P, WorkerSmem &W, const TileDesc &td, uint
   ChunkPages p0 = pre < nk2 ? kd_pages(a, b, nca, ncb, pre) : ChunkPages{0, 0, 0, 0};
   for (uint32_t kc = pre; kc < nk2; kc++) {
     const ChunkPages cur = p0;
+    check_chunk(P, cur, nca, ncb, 20, kc);
     if (kc + 1 < nk2) p0 = kd_pages(a, b, nca, ncb, kc + 1);
     const uint32_t sa = s, pha = s_phase;
     if (++s == PIPE) { s = 0; s_phase ^= 1; }
@@ -1157,6 +1195,7 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W, uint32_t h) {
         ChunkPages pg[PIPE];
         for (uint32_t kc = 0; kc < pre; kc++) {
           pg[kc] = chunk_pages(a, b, nca, ncb, kc);
+          check_chunk(P, pg[kc], nca, ncb, 40, kc);
           ptx::mbar_wait_abortable(&W.empty[s2], ph2 ^ 1, &P.ctrl->abort);
           const uint32_t bar = ptx::mapa(&W.full[s2], 0);
           if (h == 0) ptx::mbar_arrive_expect_tx(&W.full[s2], tx_pair);
@@ -1188,6 +1227,7 @@ __device__ void operand_loader(const Params &P, WorkerSmem &W, uint32_t h) {
       ChunkPages p1 = pre + 1 < nk ? chunk_pages(a, b, nca, ncb, pre + 1) : p0;
       for (uint32_t kc = pre; kc < nk; kc++) {
         const ChunkPages cur = p0;
+        check_chunk(P, cur, nca, ncb, 30, kc);
         p0 = p1;
         if (kc + 2 < nk) p1 = chunk_pages(a, b, nca, ncb, kc + 2);
         // stage s is free once the pair's MMA has consumed it (multicast commit)
